@@ -1,0 +1,115 @@
+/* exspace_b200.h -- C ABI of the B200 stray-call analyser.
+ *
+ * Drop-in boundary for the reference's hot path.  The reference has no FFI:
+ * its boundary is the Python API
+ *     exspace.spacecheck.analyze(text, path, profile, mode, cfg)      spacecheck.py:687-739
+ *     exspace.spacecheck.check_unit(text, path, profile, mode, cfg)   spacecheck.py:742-750
+ * applied one unit at a time (cli.py:82-91, corpus.py:123-175).  This ABI is
+ * the batch form of that call: one exs_run() analyses many units; the
+ * Python mirror (paper_2309_03912_b200.exspace) rebuilds Diagnostic objects,
+ * messages and ordering exactly as the reference does.
+ * for the ctypes binding the reference-side shim uses.
+ *
+ * Plain pointers and sizes only; no torch types.  All entry points return 0
+ * on success and a negative code on error (exs_last_error() has the text);
+ * they never abort the process.
+ */
+#ifndef EXSPACE_B200_H
+#define EXSPACE_B200_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct exs_handle_s* exs_handle;
+
+/* per-unit configuration byte (replaces CompileProfile/Mode/TraitConfig,
+ * preprocess.py:46-63, spacecheck.py:53-58, sema.py:54-62) */
+#define EXS_MODE_CLASSIC 0
+#define EXS_MODE_FIDELITY 1
+#define EXS_MODE_SOUND 2
+#define EXS_MODE_PROPOSAL1 3
+#define EXS_MODE_PROPOSAL2 4
+#define EXS_CFG_PLAIN 8        /* CompileProfile(compiler="plain")      */
+#define EXS_CFG_RELAXED 16     /* relaxed_constexpr=True                */
+#define EXS_CFG_ERASE 32       /* erase_specifiers=True                 */
+#define EXS_CFG_FUND_HSTDEV 64 /* TraitConfig(fundamentals_hstdev=True) */
+
+/* One diagnostic (diagnostics.py:56-62).  code: 1=E0001 .. 20=W1502, 21 =
+ * out-of-contract marker.  msg + a0..a3: message template and arguments
+ * (spans are raw-byte (pos<<32 | len) into the batch; bit 63 marks the
+ * directive-text arena). */
+typedef struct {
+  uint32_t file, line, col;
+  uint16_t code, msg;
+  uint64_t a0, a1, a2;
+  uint32_t a3;
+  uint8_t suppressed, pad0, pad1, pad2;
+} exs_diag;
+
+typedef struct {
+  uint64_t bytes, files, lines, directives, tokens, views, view_tokens, items;
+  uint64_t functions, structs, instances, edges, callsites, levels, diagnostics;
+  uint64_t retries, gpu_launches;
+  float ms_lex, ms_parse, ms_sema, ms_walk, ms_total, ms_h2d, ms_d2h;
+} exs_stats;
+
+/* per (file, pass) preprocessing / lexing status, pass 0 host, 1 device */
+typedef struct {
+  uint32_t pp_line; /* 0 = no E0002 */
+  uint16_t pp_msg, exists;
+  uint32_t lex_line, lex_col; /* 0 = no lexical error */
+  uint16_t lex_msg, pad;
+  uint32_t eof_line, eof_col, view, parse_failed;
+} exs_pass_status;
+
+/* a token record (lexer.py:16-20): kind 1 ident 2 int 3 string 4 punct 5 pragma */
+typedef struct {
+  uint32_t pos, end, line, col;
+  uint64_t hv;
+  uint8_t kind, id, mask, flags;
+  uint32_t file;
+} exs_token;
+
+/* per walk (2*file + pass) counts, as exposed by Analysis.walks */
+typedef struct {
+  uint32_t instances, edges, demands, exists;
+} exs_walk_stats;
+
+/* description of a declaration or instance (for E1201 display names) */
+typedef struct {
+  uint64_t name, owner, otype;  /* spans; 0 = none */
+  uint8_t otarg, nb, pad[6];
+  uint64_t bname[2], bval[2];   /* binding names (spans) and values (type spans) */
+  uint8_t bkind[2], bvx[2], pad2[4]; /* bkind 1 type 2 hdc; bvx: type targ / hdc */
+} exs_desc;
+
+int exs_create(int device, exs_handle* out);
+int exs_destroy(exs_handle h);
+const char* exs_last_error(void);
+
+/* Analyse a batch of units held in HOST memory (copied to HBM inside). */
+int exs_run(exs_handle h, const uint8_t* bytes, uint64_t n_bytes, const uint64_t* file_off,
+            uint32_t n_files, const uint8_t* file_cfg);
+/* Same with the bytes already in device memory (d_bytes is not modified). */
+int exs_run_device(exs_handle h, const uint8_t* d_bytes, uint64_t n_bytes,
+                   const uint64_t* file_off, uint32_t n_files, const uint8_t* file_cfg);
+
+int exs_get_stats(exs_handle h, exs_stats* out);
+/* diagnostics ordered by (file, line, col, code), duplicates removed */
+int exs_get_diags(exs_handle h, exs_diag* out, uint64_t cap, uint64_t* n);
+int exs_get_arena(exs_handle h, uint8_t* out, uint64_t cap, uint64_t* n);
+int exs_get_pass_status(exs_handle h, exs_pass_status* out, uint64_t cap);
+int exs_get_tokens(exs_handle h, uint32_t file, exs_token* out, uint64_t cap, uint64_t* n);
+int exs_get_walk_stats(exs_handle h, exs_walk_stats* out, uint64_t cap);
+int exs_describe(exs_handle h, const uint32_t* ids, const uint8_t* kinds, uint32_t n,
+                 exs_desc* out);
+/* options: 1 = also compute per-walk demand counts (Analysis.walks parity) */
+int exs_set_option(exs_handle h, int key, int value);
+/* per-stage device time of the last run (ms): lex, parse, sema, walk */
+int exs_stage_times(exs_handle h, float* out4);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,191 @@
+"""ctypes binding of the C ABI in include/exspace_b200.h.
+
+The product library is ``libexspace_b200.so`` (sm_100a, built in-tree by
+``__graft_entry__.build()``).  There is no CPU fallback: if the library or a
+CUDA device is missing, ``Engine()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libexspace_b200.so"
+
+DIAG_DTYPE = np.dtype([
+    ("file", "<u4"), ("line", "<u4"), ("col", "<u4"), ("code", "<u2"), ("msg", "<u2"),
+    ("a0", "<u8"), ("a1", "<u8"), ("a2", "<u8"), ("a3", "<u4"),
+    ("suppressed", "u1"), ("pad", "u1", (3,)),
+])
+assert DIAG_DTYPE.itemsize == 48
+
+TOKEN_DTYPE = np.dtype([
+    ("pos", "<u4"), ("end", "<u4"), ("line", "<u4"), ("col", "<u4"), ("hv", "<u8"),
+    ("kind", "u1"), ("id", "u1"), ("mask", "u1"), ("flags", "u1"), ("file", "<u4"),
+])
+assert TOKEN_DTYPE.itemsize == 32
+
+PASS_DTYPE = np.dtype([
+    ("pp_line", "<u4"), ("pp_msg", "<u2"), ("exists", "<u2"), ("lex_line", "<u4"),
+    ("lex_col", "<u4"), ("lex_msg", "<u2"), ("pad", "<u2"), ("eof_line", "<u4"),
+    ("eof_col", "<u4"), ("view", "<u4"), ("parse_failed", "<u4"),
+])
+
+WALK_DTYPE = np.dtype([("instances", "<u4"), ("edges", "<u4"), ("demands", "<u4"), ("exists", "<u4")])
+
+DESC_DTYPE = np.dtype([
+    ("name", "<u8"), ("owner", "<u8"), ("otype", "<u8"), ("otarg", "u1"), ("nb", "u1"),
+    ("pad", "u1", (6,)), ("bname", "<u8", (2,)), ("bval", "<u8", (2,)), ("bkind", "u1", (2,)),
+    ("bvx", "u1", (2,)), ("pad2", "u1", (4,)),
+])
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "bytes", "files", "lines", "directives", "tokens", "views", "view_tokens", "items",
+        "functions", "structs", "instances", "edges", "callsites", "levels", "diagnostics",
+        "retries", "gpu_launches")] + [(n, C.c_float) for n in (
+        "ms_lex", "ms_parse", "ms_sema", "ms_walk", "ms_total", "ms_h2d", "ms_d2h")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+EXPORTS = [
+    "exs_create", "exs_destroy", "exs_last_error", "exs_run", "exs_run_device", "exs_get_stats",
+    "exs_get_diags", "exs_get_arena", "exs_get_pass_status", "exs_get_tokens",
+    "exs_get_walk_stats", "exs_describe", "exs_set_option", "exs_stage_times",
+]
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise NativeError(
+            f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (the analyser has no CPU fallback)")
+    lib = C.CDLL(str(p))
+    vp, u8p, u32p, u64p = C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
+    lib.exs_create.argtypes = [C.c_int, C.POINTER(vp)]
+    lib.exs_destroy.argtypes = [vp]
+    lib.exs_last_error.restype = C.c_char_p
+    lib.exs_run.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
+    lib.exs_run_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
+    lib.exs_get_stats.argtypes = [vp, C.POINTER(Stats)]
+    lib.exs_get_diags.argtypes = [vp, vp, C.c_uint64, u64p]
+    lib.exs_get_arena.argtypes = [vp, vp, C.c_uint64, u64p]
+    lib.exs_get_pass_status.argtypes = [vp, vp, C.c_uint64]
+    lib.exs_get_tokens.argtypes = [vp, C.c_uint32, vp, C.c_uint64, u64p]
+    lib.exs_get_walk_stats.argtypes = [vp, vp, C.c_uint64]
+    lib.exs_describe.argtypes = [vp, vp, vp, C.c_uint32, vp]
+    lib.exs_set_option.argtypes = [vp, C.c_int, C.c_int]
+    lib.exs_stage_times.argtypes = [vp, C.POINTER(C.c_float)]
+    for name in EXPORTS:
+        if name not in ("exs_last_error",):
+            getattr(lib, name).restype = C.c_int
+    _ = (u8p, u32p)
+    return lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Handle:
+    """One analyser instance bound to one GPU."""
+
+    def __init__(self, device: int = 0, lib_path=None):
+        self.lib = load_library(lib_path)
+        h = C.c_void_p()
+        self._check(self.lib.exs_create(device, C.byref(h)))
+        self.h = h
+
+    def _check(self, rc):
+        if rc != 0:
+            raise NativeError(self.lib.exs_last_error().decode(errors="replace"))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.exs_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_option(self, key: int, value: int):
+        self._check(self.lib.exs_set_option(self.h, key, value))
+
+    def run(self, data: np.ndarray, offsets: np.ndarray, cfg: np.ndarray):
+        data = np.ascontiguousarray(data, dtype=np.uint8)
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        cfg = np.ascontiguousarray(cfg, dtype=np.uint8)
+        self._check(self.lib.exs_run(self.h, _ptr(data), data.size, _ptr(offsets),
+                                     len(offsets) - 1, _ptr(cfg)))
+
+    def run_device(self, dev_ptr: int, n_bytes: int, offsets: np.ndarray, cfg: np.ndarray):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        cfg = np.ascontiguousarray(cfg, dtype=np.uint8)
+        self._check(self.lib.exs_run_device(self.h, C.c_void_p(dev_ptr), n_bytes, _ptr(offsets),
+                                            len(offsets) - 1, _ptr(cfg)))
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(self.lib.exs_get_stats(self.h, C.byref(s)))
+        return s.as_dict()
+
+    def diags(self) -> np.ndarray:
+        n = C.c_uint64()
+        self._check(self.lib.exs_get_diags(self.h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=DIAG_DTYPE)
+        if n.value:
+            self._check(self.lib.exs_get_diags(self.h, _ptr(out), n.value, C.byref(n)))
+        return out
+
+    def arena(self) -> bytes:
+        n = C.c_uint64()
+        self._check(self.lib.exs_get_arena(self.h, None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), dtype=np.uint8)
+        if n.value:
+            self._check(self.lib.exs_get_arena(self.h, _ptr(out), n.value, C.byref(n)))
+        return out[: n.value].tobytes()
+
+    def pass_status(self, n_files: int) -> np.ndarray:
+        out = np.zeros(2 * n_files, dtype=PASS_DTYPE)
+        self._check(self.lib.exs_get_pass_status(self.h, _ptr(out), 2 * n_files))
+        return out
+
+    def tokens(self, file: int) -> np.ndarray:
+        n = C.c_uint64()
+        self._check(self.lib.exs_get_tokens(self.h, file, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=TOKEN_DTYPE)
+        if n.value:
+            self._check(self.lib.exs_get_tokens(self.h, file, _ptr(out), n.value, C.byref(n)))
+        return out
+
+    def walk_stats(self, n_files: int) -> np.ndarray:
+        out = np.zeros(2 * n_files, dtype=WALK_DTYPE)
+        self._check(self.lib.exs_get_walk_stats(self.h, _ptr(out), 2 * n_files))
+        return out
+
+    def describe(self, ids, kinds) -> np.ndarray:
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        kinds = np.ascontiguousarray(kinds, dtype=np.uint8)
+        out = np.zeros(len(ids), dtype=DESC_DTYPE)
+        if len(ids):
+            self._check(self.lib.exs_describe(self.h, _ptr(ids), _ptr(kinds), len(ids), _ptr(out)))
+        return out
+
+    def stage_times(self):
+        out = (C.c_float * 4)()
+        self._check(self.lib.exs_stage_times(self.h, out))
+        return list(out)

@@ -1,0 +1,507 @@
+// exs_lex.cuh -- K1..K3: byte-parallel splice map, logical-line scanner,
+// directive parser and tokenizer (reference: syntax/preprocess.py:81-203,
+// syntax/lexer.py:46-118).
+//
+// Layout in HBM (one batch = concatenated files):
+//   src[N]          corpus bytes
+//   fstart[N/32+1]  bit p set iff p is a file start
+//   splice[N/32+1]  bit p set iff byte p is removed by backslash-newline
+//                   splicing (preprocess.py:81-95: the last min(k,m) bytes of
+//                   a k-backslash run and the first min(k,m) of the m-newline
+//                   run that follows it)
+//   line_start[L]   logical line starts (file start, or after a non-spliced \n)
+// A logical line is processed by one thread (the reference's line loop,
+// preprocess.py:163); the comment DFA state at a line start is CODE or BLOCK,
+// so lines compose as {CODE,BLOCK}->{CODE,BLOCK} maps under a scan.
+#pragma once
+#include "exs_common.cuh"
+
+namespace exs {
+
+EXS_HD inline bool bit_get(const u32* b, u32 p) { return (b[p >> 5] >> (p & 31)) & 1u; }
+
+// comment DFA (same formulation as oracle/exs_oracle.py:_step)
+enum { S_CODE = 0, S_SLASH, S_STR, S_LINE, S_BLOCK, S_STAR };
+
+EXS_HD inline u8 dfa_step(u8 s, u8 c) {
+  if (s == S_SLASH) {
+    if (c == '/') return S_LINE;
+    if (c == '*') return S_BLOCK;
+    s = S_CODE;
+  }
+  switch (s) {
+    case S_CODE: return c == '"' ? S_STR : (c == '/' ? S_SLASH : S_CODE);
+    case S_STR: return (c == '"' || c == '\n') ? S_CODE : S_STR;
+    case S_LINE: return c == '\n' ? S_CODE : S_LINE;
+    case S_BLOCK: return c == '*' ? S_STAR : S_BLOCK;
+    default: return c == '/' ? S_CODE : (c == '*' ? S_STAR : S_BLOCK);
+  }
+}
+
+struct SrcView {
+  const u8* src;
+  const u32* splice;
+  const u32* fstart;
+  u32 n;
+};
+
+// Is the byte at p removed by splicing?  (p must hold '\\' or '\n')
+EXS_HD inline bool compute_spliced(const SrcView& v, u32 p) {
+  const u8* s = v.src;
+  if (s[p] == '\\') {
+    u32 e = p;
+    while (e < v.n && s[e] == '\\' && (e == p || !bit_get(v.fstart, e))) e++;
+    u32 need = e - p, m = 0;
+    u32 q = e;
+    while (q < v.n && m < need && s[q] == '\n' && !bit_get(v.fstart, q)) { m++; q++; }
+    return m >= need;
+  }
+  if (s[p] == '\n') {
+    u32 idx = 0, q = p;
+    while (!bit_get(v.fstart, q) && q > 0 && s[q - 1] == '\n') { idx++; q--; }
+    // q = newline run start; count backslashes before it (need idx+1)
+    u32 lb = 0;
+    while (!bit_get(v.fstart, q) && q > 0 && s[q - 1] == '\\' && lb <= idx) { lb++; q--; }
+    return idx < lb;
+  }
+  return false;
+}
+
+// Iterator over the comment-blanked logical characters of one logical line
+// (preprocess.py:98-145 applied after splicing).  Yields (char, raw pos, width);
+// width is 0 for UTF-8 continuation bytes so columns count code points.
+struct Blanker {
+  const u8* src;
+  const u32* splice;
+  u32 p, hi;   // next raw position, logical line end (terminator or file end)
+  u8 st;       // S_CODE / S_STR / S_LINE / S_BLOCK  (S_SLASH/S_STAR never stored)
+  u8 pend;     // a second blank of a 2-char comment token is pending
+  u32 pend_pos;
+
+  EXS_HD void init(const u8* s, const u32* sp, u32 lo, u32 hi_, u8 start_state) {
+    src = s; splice = sp; p = lo; hi = hi_; st = start_state; pend = 0; pend_pos = 0;
+  }
+  EXS_HD u32 next_logical(u32 q) const {
+    while (q < hi && bit_get(splice, q)) q++;
+    return q;
+  }
+  // returns false at line end
+  EXS_HD bool next(u8& c, u32& pos, u8& width) {
+    if (pend) {
+      pend = 0; c = ' '; pos = pend_pos; width = 1;
+      return true;
+    }
+    u32 q = next_logical(p);
+    if (q >= hi) { p = q; return false; }
+    u8 ch = src[q];
+    u32 q2 = next_logical(q + 1);
+    u8 nx = q2 < hi ? src[q2] : 0;   // '\n' never appears inside a logical line
+    width = is_cont_byte(ch) ? 0 : 1;
+    pos = q;
+    p = q + 1;
+    switch (st) {
+      case S_BLOCK:
+        if (ch == '*' && nx == '/') {
+          c = ' '; pend = 1; pend_pos = q2; p = q2 + 1; st = S_CODE;
+        } else {
+          c = ' ';
+        }
+        return true;
+      case S_LINE:
+        c = ' ';
+        return true;
+      case S_STR:
+        c = ch;
+        if (ch == '"') st = S_CODE;
+        return true;
+      default:
+        if (ch == '"') { st = S_STR; c = ch; return true; }
+        if (ch == '/' && nx == '/') { c = ' '; pend = 1; pend_pos = q2; p = q2 + 1; st = S_LINE; return true; }
+        if (ch == '/' && nx == '*') { c = ' '; pend = 1; pend_pos = q2; p = q2 + 1; st = S_BLOCK; return true; }
+        c = ch;
+        return true;
+    }
+  }
+  // comment state after the line terminator ('\n' resets STR and LINE)
+  EXS_HD u8 end_state() const { return st == S_BLOCK ? S_BLOCK : S_CODE; }
+};
+
+// Run the blanker from CODE and from BLOCK; return 2-bit map (bit0: end from
+// CODE is BLOCK, bit1: end from BLOCK is BLOCK).
+EXS_HD inline u8 line_fsm_map(const u8* s, const u32* sp, u32 lo, u32 hi) {
+  u8 r = 0;
+  for (int k = 0; k < 2; k++) {
+    Blanker b;
+    b.init(s, sp, lo, hi, k ? S_BLOCK : S_CODE);
+    u8 c, w; u32 pos;
+    while (b.next(c, pos, w)) {}
+    if (b.end_state() == S_BLOCK) r |= (1u << k);
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// vocabulary (exs_common.cuh Word) -- matched on logical token text
+
+#define EXS_VOCAB_TEXT                                                                   \
+  "struct\0class\0enum\0template\0typename\0requires\0return\0if\0else\0for\0void\0int\0" \
+  "bool\0true\0false\0constexpr\0static\0static_assert\0HDC\0__host__\0__device__\0"      \
+  "__global__\0main\0cuda_arch\0hdc\0std\0Hst\0Dev\0HstDev\0printf\0release_assert\0"    \
+  "__trap\0abort\0cudaDeviceSynchronize\0hd_warning_disable\0nv_exec_check_disable\0!\0(\0"
+#ifndef EXS_EMU
+__constant__ char kVocabDev[] = EXS_VOCAB_TEXT;
+#endif
+static const char kVocabHost[] = EXS_VOCAB_TEXT;
+
+EXS_HD inline u8 vocab_lookup(const u8* t, u32 len) {
+  if (len == 0 || len > 24) return W_NONE;
+  // body-only __CUDA_ARCH__ switch, never in a signature
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  const char* v = kVocabDev;
+#else
+  const char* v = kVocabHost;
+#endif
+  for (u8 id = 1; id < W_COUNT; id++) {
+    u32 l = 0;
+    while (v[l]) l++;
+    if (l == len) {
+      bool eq = true;
+      for (u32 i = 0; i < len; i++)
+        if ((u8)v[i] != t[i]) { eq = false; break; }
+      if (eq) return id;
+    }
+    v += l + 1;
+  }
+  return W_NONE;
+}
+
+// directive kinds (per logical line)
+enum {
+  LK_NORMAL = 0, LK_PRAGMA_DIR, LK_IFDEF, LK_IFNDEF, LK_ELSE, LK_ENDIF, LK_ERROR,
+  LK_UNKNOWN, LK_BAD_ARITY, LK_BAD_MACRO,
+};
+enum { MAC_CUDACC = 1, MAC_CUDA_ARCH = 2, MAC_RELAXED = 4 };
+
+struct LineInfo {
+  u8 kind;      // LK_*
+  u8 macro;     // MAC_* for ifdef/ifndef
+  u8 has_splice;
+  u8 is_ifndef; // for LK_BAD_ARITY / LK_BAD_MACRO: which directive
+  u32 cps;      // code points of the logical line (for the EOF column)
+  u64 span;     // text-arena span (offset<<32 | len) for messages
+};
+
+EXS_HD inline bool text_eq(const u8* a, u32 la, const char* b) {
+  u32 lb = 0;
+  while (b[lb]) lb++;
+  if (la != lb) return false;
+  for (u32 i = 0; i < la; i++)
+    if (a[i] != (u8)b[i]) return false;
+  return true;
+}
+
+// Directive detection and parsing for one logical line (preprocess.py:163-200).
+// Writes message text (if any) into the arena.
+EXS_HD inline LineInfo scan_line_directive(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st,
+                                           u8* arena, u32* arena_top, u32 arena_cap) {
+  LineInfo li;
+  li.kind = LK_NORMAL; li.macro = 0; li.has_splice = 0; li.is_ifndef = 0; li.cps = 0; li.span = 0;
+  Blanker b;
+  b.init(s, sp, lo, hi, st);
+  u8 c, w; u32 pos;
+  // pass 1: first non-space char, code points
+  bool seen = false, directive = false;
+  u32 hash_pos = 0;
+  while (b.next(c, pos, w)) {
+    li.cps += w;
+    if (!seen && !(w == 0 || is_pyspace(c))) {
+      seen = true;
+      if (c == '#') { directive = true; hash_pos = pos; }
+    }
+  }
+  for (u32 q = lo; q < hi; q++)
+    if (bit_get(sp, q)) { li.has_splice = 1; break; }
+  if (!directive) return li;
+  // pass 2: words after '#': name = first run of non-space chars; rest = stripped remainder
+  b.init(s, sp, lo, hi, st);
+  while (b.next(c, pos, w) && pos != hash_pos) {}
+  u8 name[16]; u32 nlen = 0;
+  u8 rest[32]; u32 rlen = 0;       // first 32 chars of rest (for macro compare)
+  u32 rest_first = NONE, rest_last_end = 0;  // positions in blanked-char order
+  bool rest_has_inner_space = false;
+  int phase = 0;  // 0 before name, 1 in name, 2 after name, 3 in rest
+  u32 idx = 0, rest_start_idx = 0, rest_end_idx = 0, name_start_idx = 0, name_end_idx = 0;
+  bool pending_space = false;
+  while (b.next(c, pos, w)) {
+    bool sp_ = (w != 0) && is_pyspace(c);
+    if (w == 0) {   // continuation byte: part of the current char
+      if (c != ' ') {
+        if (phase == 1) name_end_idx = idx + 1;
+        else if (phase == 3 && !pending_space) rest_end_idx = idx + 1;
+      }
+      idx++;
+      continue;
+    }
+    if (phase == 0) {
+      if (!sp_) { phase = 1; name_start_idx = idx; if (nlen < 16) name[nlen] = c; nlen++; name_end_idx = idx + 1; }
+    } else if (phase == 1) {
+      if (sp_) phase = 2;
+      else { if (nlen < 16) name[nlen] = c; nlen++; name_end_idx = idx + 1; }
+    } else {
+      if (!sp_) {
+        if (phase == 2) { phase = 3; rest_start_idx = idx; rest_first = idx; }
+        else if (pending_space) rest_has_inner_space = true;
+        pending_space = false;
+        if (rlen < 32) rest[rlen] = c;
+        rlen++;
+        rest_end_idx = idx + 1; rest_last_end = idx + 1;
+      } else if (phase == 3) {
+        pending_space = true;
+      }
+    }
+    idx++;
+  }
+  (void)rest_first; (void)rest_last_end;
+  bool n_pragma = nlen <= 16 && text_eq(name, nlen, "pragma");
+  if (n_pragma) { li.kind = LK_PRAGMA_DIR; return li; }
+  bool n_ifdef = nlen <= 16 && text_eq(name, nlen, "ifdef");
+  bool n_ifndef = nlen <= 16 && text_eq(name, nlen, "ifndef");
+  u32 span_from = 0, span_to = 0;  // blanked-char index range to copy to the arena
+  bool want_text = false;
+  if (n_ifdef || n_ifndef) {
+    li.is_ifndef = n_ifndef;
+    if (phase < 3 || rest_has_inner_space) {
+      li.kind = LK_BAD_ARITY;
+    } else {
+      u8 m = 0;
+      if (rlen <= 32) {
+        if (text_eq(rest, rlen, "__CUDACC__")) m = MAC_CUDACC;
+        else if (text_eq(rest, rlen, "__CUDA_ARCH__")) m = MAC_CUDA_ARCH;
+        else if (text_eq(rest, rlen, "__CUDACC_RELAXED_CONSTEXPR__")) m = MAC_RELAXED;
+      }
+      if (m) { li.kind = n_ifdef ? LK_IFDEF : LK_IFNDEF; li.macro = m; }
+      else { li.kind = LK_BAD_MACRO; want_text = true; span_from = rest_start_idx; span_to = rest_end_idx; }
+    }
+  } else if (nlen <= 16 && text_eq(name, nlen, "else")) {
+    li.kind = LK_ELSE;
+  } else if (nlen <= 16 && text_eq(name, nlen, "endif")) {
+    li.kind = LK_ENDIF;
+  } else if (nlen <= 16 && text_eq(name, nlen, "error")) {
+    li.kind = LK_ERROR;
+    want_text = true;
+    if (phase == 3) { span_from = rest_start_idx; span_to = rest_end_idx; }
+  } else {
+    li.kind = LK_UNKNOWN;
+    want_text = true;
+    if (nlen) { span_from = name_start_idx; span_to = name_end_idx; }
+  }
+  if (want_text && span_to > span_from) {
+    // copy blanked chars [span_from, span_to) (indices count every yielded byte)
+    b.init(s, sp, lo, hi, st);
+    while (b.next(c, pos, w) && pos != hash_pos) {}
+    u32 len = 0, i = 0;
+    // measure bytes first
+    Blanker b2 = b;
+    while (b2.next(c, pos, w)) {
+      if (i >= span_from && i < span_to && !(w == 0 && c == ' ')) len++;
+      i++;
+      if (i >= span_to) break;
+    }
+    u32 off = at_add(arena_top, len);
+    if (off + len <= arena_cap) {
+      i = 0;
+      u32 k = 0;
+      while (b.next(c, pos, w)) {
+        if (i >= span_from && i < span_to && !(w == 0 && c == ' ')) {
+          arena[off + k++] = c;  // blanked continuation bytes vanish; real ones are copied
+        }
+        i++;
+        if (i >= span_to) break;
+      }
+      li.span = (1ull << 63) | ((u64)off << 32) | len;  // arena-tagged span
+    } else {
+      li.span = ((u64)0xFFFFFFFFu << 32);
+    }
+  }
+  return li;
+}
+
+// Tokenizer over one active logical line (lexer.py:46-118).  mode 0 counts,
+// mode 1 emits into out[].  Returns the token count; on a lexical error sets
+// *err (M_LEX_*), *err_col, *err_pos and stops.
+struct LexErr { u16 msg; u32 col, pos; };
+
+EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u32 line_no,
+                           u32 file, u8 mask, Tok* out, LexErr* err) {
+  Blanker b;
+  b.init(s, sp, lo, hi, st);
+  u32 col = 1, n = 0;
+  err->msg = 0;
+  u8 c, w; u32 pos;
+  bool have = b.next(c, pos, w);
+  while (have) {
+    if (c == ' ' || c == '\t' || c == '\r') {
+      col += w;
+      have = b.next(c, pos, w);
+      continue;
+    }
+    if (w == 0) {  // stray continuation byte of a blanked char or string: width 0
+      have = b.next(c, pos, w);
+      continue;
+    }
+    u32 tcol = col, tpos = pos;
+    if (c == '#') {
+      // scan [alnum _ space tab]*, then words must be exactly "pragma NAME"
+      u32 consumed = 1;
+      int nw = 0; bool inword = false, first_ok = true;
+      u8 wbuf[8]; u32 wl = 0;
+      u32 name_pos = 0, name_end = 0; u64 h = fnv_init(); u8 nb[24]; u32 nl = 0;
+      have = b.next(c, pos, w);
+      while (have && (w ? (is_ident_char(c) || c == ' ' || c == '\t') : c == ' ')) {
+        bool spc = (c == ' ' || c == '\t');
+        if (!spc) {
+          if (!inword) { nw++; inword = true; if (nw == 2) name_pos = pos; }
+          if (nw == 1) { if (wl < 8) wbuf[wl] = c; wl++; }
+          if (nw == 2) { h = fnv_step(h, c); if (nl < 24) nb[nl] = c; nl++; name_end = pos + 1; }
+        } else {
+          inword = false;
+        }
+        consumed += w;
+        have = b.next(c, pos, w);
+      }
+      first_ok = (wl == 6 && text_eq(wbuf, 6, "pragma"));
+      if (nw != 2 || !first_ok) {
+        err->msg = M_LEX_PRAGMA; err->col = tcol; err->pos = tpos;
+        return n;
+      }
+      if (out) {
+        Tok& t = out[n];
+        t.pos = name_pos; t.end = name_end; t.line = line_no; t.col = tcol; t.hv = h;
+        t.kind = TK_PRAGMA; t.id = nl <= 24 ? vocab_lookup(nb, nl) : 0; t.mask = mask; t.flags = 0; t.file = file;
+      }
+      n++;
+      col += consumed;
+      continue;
+    }
+    if (c == '"') {
+      u32 cw = 1;
+      u64 h = fnv_init(); u8 nb[24]; u32 nl = 0;
+      u32 cstart = NONE, cend = 0;
+      bool closed = false;
+      have = b.next(c, pos, w);
+      while (have) {
+        if (c == '"' && w) { closed = true; cw += 1; break; }
+        if (cstart == NONE) cstart = pos;
+        cend = pos + 1;
+        h = fnv_step(h, c);
+        if (nl < 24) nb[nl] = c;
+        nl++;
+        cw += w;
+        have = b.next(c, pos, w);
+      }
+      if (!closed) {
+        err->msg = M_LEX_STRING; err->col = tcol; err->pos = tpos;
+        return n;
+      }
+      if (out) {
+        Tok& t = out[n];
+        t.pos = cstart == NONE ? pos : cstart; t.end = cstart == NONE ? pos : cend;
+        t.line = line_no; t.col = tcol; t.hv = h;
+        t.kind = TK_STRING; t.id = nl <= 24 ? vocab_lookup(nb, nl) : 0; t.mask = mask; t.flags = 0; t.file = file;
+      }
+      n++;
+      col += cw;
+      have = b.next(c, pos, w);
+      continue;
+    }
+    // identifiers: ASCII [A-Za-z_][A-Za-z0-9_]* plus any non-ASCII code point
+    // treated as a letter (Python str.isalpha for letters such as 'é')
+    if (is_digit(c) || is_ident_start(c) || c >= 0xC0) {
+      bool digits = is_digit(c);
+      u64 h = fnv_init(), val = 0; bool ovf = false;
+      u8 nb[24]; u32 nl = 0, ncp = 0; u32 last = pos; bool spl = false;
+      u32 prevpos = pos;
+      while (have && (digits ? (w && is_digit(c))
+                             : (w ? (is_ident_char(c) || c >= 0xC0) : (c >= 0x80)))) {
+        if (pos != prevpos + 1 && nl) spl = true;
+        prevpos = pos;
+        h = fnv_step(h, c);
+        if (digits) {
+          u64 nv = val * 10 + (c - '0');
+          if (val > 1844674407370955161ull || nv < val) ovf = true;
+          val = nv;
+        }
+        if (nl < 24) nb[nl] = c;
+        nl++;
+        ncp += w;
+        last = pos;
+        have = b.next(c, pos, w);
+      }
+      if (out) {
+        Tok& t = out[n];
+        t.pos = tpos; t.end = last + 1; t.line = line_no; t.col = tcol;
+        t.hv = digits ? val : h;
+        t.kind = digits ? TK_INT : TK_IDENT;
+        t.id = digits ? 0 : vocab_lookup(nb, nl);
+        t.mask = mask; t.flags = (ovf ? TF_INT_OVERFLOW : 0) | (spl ? TF_HAS_SPLICE : 0); t.file = file;
+      }
+      n++;
+      col += ncp;
+      continue;
+    }
+    // punctuators, greedy in reference order
+    {
+      Blanker la = b;
+      u8 c1 = 0, c2 = 0, w1 = 0, w2 = 0; u32 p1 = 0, p2 = 0;
+      bool h1 = la.next(c1, p1, w1);
+      Blanker la2 = la;
+      bool h2 = h1 && la2.next(c2, p2, w2);
+      if (!h1 || !w1) c1 = 0;
+      if (!h2 || !w2) c2 = 0;
+      u8 pid = 0, plen = 0;
+      if (c == '<' && c1 == '<' && c2 == '<') { pid = P_LLL; plen = 3; }
+      else if (c == '>' && c1 == '>' && c2 == '>') { pid = P_GGG; plen = 3; }
+      else if (c == ':' && c1 == ':') { pid = P_SCOPE; plen = 2; }
+      else if (c == '=' && c1 == '=') { pid = P_EQ; plen = 2; }
+      else if (c == '!' && c1 == '=') { pid = P_NE; plen = 2; }
+      else if (c == '&' && c1 == '&') { pid = P_AND; plen = 2; }
+      else if (c == '|' && c1 == '|') { pid = P_OR; plen = 2; }
+      else if (c == '+' && c1 == '+') { pid = P_INC; plen = 2; }
+      else {
+        plen = 1;
+        switch (c) {
+          case '{': pid = P_LBRACE; break;
+          case '}': pid = P_RBRACE; break;
+          case '(': pid = P_LPAREN; break;
+          case ')': pid = P_RPAREN; break;
+          case '<': pid = P_LT; break;
+          case '>': pid = P_GT; break;
+          case ',': pid = P_COMMA; break;
+          case ';': pid = P_SEMI; break;
+          case '.': pid = P_DOT; break;
+          case '!': pid = P_BANG; break;
+          case '=': pid = P_ASSIGN; break;
+          default: pid = 0;
+        }
+      }
+      if (!pid) {
+        err->msg = M_LEX_CHAR; err->col = tcol; err->pos = tpos;
+        return n;
+      }
+      u32 endp = plen == 1 ? tpos + 1 : (plen == 2 ? p1 + 1 : p2 + 1);
+      if (out) {
+        Tok& t = out[n];
+        t.pos = tpos; t.end = endp; t.line = line_no; t.col = tcol; t.hv = 0;
+        t.kind = TK_PUNCT; t.id = pid; t.mask = mask; t.flags = 0; t.file = file;
+      }
+      n++;
+      col += plen;
+      if (plen == 1) have = b.next(c, pos, w);
+      else if (plen == 2) { b = la; have = b.next(c, pos, w); }
+      else { b = la2; have = b.next(c, pos, w); }
+    }
+  }
+  return n;
+}
+
+}  // namespace exs

@@ -1,0 +1,224 @@
+// exs_par.cuh -- parallel primitives used by the pipeline driver.
+// Device build: grid-stride kernels + CUB.  EXS_EMU: sequential host loops.
+#pragma once
+#include "exs_common.cuh"
+#include <vector>
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
+#ifndef EXS_EMU
+#include <cub/cub.cuh>
+#endif
+
+namespace exs {
+
+struct Err : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#ifndef EXS_EMU
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e__ = (x);                                                           \
+    if (e__ != cudaSuccess)                                                          \
+      throw exs::Err(std::string("CUDA error ") + cudaGetErrorString(e__) + " at " + \
+                     __FILE__ + ":" + std::to_string(__LINE__));                     \
+  } while (0)
+#else
+#define CK(x) (void)0
+#endif
+
+// ----------------------------------------------------------------- memory
+template <class T>
+T* dalloc(size_t n) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+#ifndef EXS_EMU
+  CK(cudaMalloc(&p, n * sizeof(T)));
+#else
+  p = calloc(n, sizeof(T));
+  if (!p) throw Err("out of host memory");
+#endif
+  return (T*)p;
+}
+inline void dfree(void* p) {
+  if (!p) return;
+#ifndef EXS_EMU
+  cudaFree(p);
+#else
+  free(p);
+#endif
+}
+inline void dzero(void* p, size_t bytes, cudaStream_t s) {
+#ifndef EXS_EMU
+  CK(cudaMemsetAsync(p, 0, bytes, s));
+#else
+  (void)s;
+  memset(p, 0, bytes);
+#endif
+}
+inline void dfill_ff(void* p, size_t bytes, cudaStream_t s) {
+#ifndef EXS_EMU
+  CK(cudaMemsetAsync(p, 0xFF, bytes, s));
+#else
+  (void)s;
+  memset(p, 0xFF, bytes);
+#endif
+}
+inline void h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
+#ifndef EXS_EMU
+  CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+#else
+  (void)s;
+  memcpy(d, h, bytes);
+#endif
+}
+inline void d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
+#ifndef EXS_EMU
+  CK(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
+#else
+  (void)s;
+  memcpy(h, d, bytes);
+#endif
+}
+inline void d2d(void* d, const void* s_, size_t bytes, cudaStream_t s) {
+#ifndef EXS_EMU
+  CK(cudaMemcpyAsync(d, s_, bytes, cudaMemcpyDeviceToDevice, s));
+#else
+  (void)s;
+  memcpy(d, s_, bytes);
+#endif
+}
+inline void sync(cudaStream_t s) {
+#ifndef EXS_EMU
+  CK(cudaStreamSynchronize(s));
+#else
+  (void)s;
+#endif
+}
+template <class T>
+T get1(const T* d, cudaStream_t s) {
+  T v;
+  d2h(&v, d, sizeof(T), s);
+  sync(s);
+  return v;
+}
+
+// ------------------------------------------------------------------ for
+#ifndef EXS_EMU
+template <class F>
+__global__ void __launch_bounds__(256) k_for(F f, i64 n) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) f(i);
+}
+extern int g_sm_count;
+extern u64 g_launches;
+#endif
+
+template <class F>
+void par_for(i64 n, F f, cudaStream_t s, int block = 256) {
+  if (n <= 0) return;
+#ifndef EXS_EMU
+  i64 want = (n + block - 1) / block;
+  i64 cap = (i64)g_sm_count * 16;
+  int grid = (int)(want < cap ? want : cap);
+  k_for<<<grid, block, 0, s>>>(f, n);
+  CK(cudaGetLastError());
+  g_launches++;
+#else
+  (void)s; (void)block;
+  for (i64 i = 0; i < n; i++) f(i);
+#endif
+}
+
+// ------------------------------------------------------------ scratch
+struct Scratch {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      dfree(p);
+      cap = bytes + (bytes >> 2) + 1024;
+      p = dalloc<u8>(cap);
+    }
+    return p;
+  }
+  ~Scratch() { dfree(p); }
+};
+
+// exclusive scan of u32 in place-able; returns nothing (total = last+count)
+inline void excl_scan_u32(const u32* in, u32* out, i64 n, Scratch& sc, cudaStream_t s) {
+  if (n <= 0) return;
+#ifndef EXS_EMU
+  size_t tb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, s));
+  CK(cub::DeviceScan::ExclusiveSum(sc.get(tb), tb, in, out, (int)n, s));
+  g_launches += 2;
+#else
+  (void)sc; (void)s;
+  u32 acc = 0;
+  for (i64 i = 0; i < n; i++) { u32 v = in[i]; out[i] = acc; acc += v; }
+#endif
+}
+
+template <class T, class Op>
+void incl_scan(const T* in, T* out, i64 n, Op op, Scratch& sc, cudaStream_t s) {
+  if (n <= 0) return;
+#ifndef EXS_EMU
+  size_t tb = 0;
+  CK(cub::DeviceScan::InclusiveScan(nullptr, tb, in, out, op, (int)n, s));
+  CK(cub::DeviceScan::InclusiveScan(sc.get(tb), tb, in, out, op, (int)n, s));
+  g_launches += 2;
+#else
+  (void)sc; (void)s;
+  T acc = in[0];
+  out[0] = acc;
+  for (i64 i = 1; i < n; i++) { acc = op(acc, in[i]); out[i] = acc; }
+#endif
+}
+
+// indices i in [0,n) with pred(i) -> out (ordered); returns count
+template <class P>
+u32 select_idx(i64 n, P pred, u32* out, u32* d_count, Scratch& sc, cudaStream_t s) {
+  if (n <= 0) return 0;
+#ifndef EXS_EMU
+  cub::CountingInputIterator<u32> it(0);
+  size_t tb = 0;
+  CK(cub::DeviceSelect::If(nullptr, tb, it, out, d_count, (int)n, pred, s));
+  CK(cub::DeviceSelect::If(sc.get(tb), tb, it, out, d_count, (int)n, pred, s));
+  g_launches += 2;
+  return get1(d_count, s);
+#else
+  (void)d_count; (void)sc; (void)s;
+  u32 c = 0;
+  for (i64 i = 0; i < n; i++)
+    if (pred((u32)i)) out[c++] = (u32)i;
+  return c;
+#endif
+}
+
+// stable sort of (u64 key, u32 value) pairs; results written back in place
+inline void sort_pairs(u64* keys, u32* vals, i64 n, Scratch& sc, cudaStream_t s, int end_bit = 64) {
+  if (n <= 1) return;
+#ifndef EXS_EMU
+  u64* k2 = dalloc<u64>(n);
+  u32* v2 = dalloc<u32>(n);
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, k2, vals, v2, (int)n, 0, end_bit, s));
+  CK(cub::DeviceRadixSort::SortPairs(sc.get(tb), tb, keys, k2, vals, v2, (int)n, 0, end_bit, s));
+  CK(cudaMemcpyAsync(keys, k2, n * 8, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(vals, v2, n * 4, cudaMemcpyDeviceToDevice, s));
+  sync(s);
+  dfree(k2);
+  dfree(v2);
+  g_launches += 2;
+#else
+  (void)sc; (void)s; (void)end_bit;
+  std::vector<std::pair<u64, u32>> v(n);
+  for (i64 i = 0; i < n; i++) v[i] = {keys[i], vals[i]};
+  std::stable_sort(v.begin(), v.end(), [](auto& a, auto& b) { return a.first < b.first; });
+  for (i64 i = 0; i < n; i++) { keys[i] = v[i].first; vals[i] = v[i].second; }
+#endif
+}
+
+}  // namespace exs

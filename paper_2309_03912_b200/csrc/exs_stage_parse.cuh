@@ -1,0 +1,347 @@
+// exs_stage_parse.cuh -- driver for K4: views, token-parallel item
+// segmentation, item-parallel parsing, sequential repair of views whose items
+// do not chain, final ordered item lists.
+#pragma once
+#include "exs_stage_lex.cuh"
+#include "exs_parse.cuh"
+
+namespace exs {
+
+struct ParseState {
+  u32 V = 0, VT = 0, I = 0, FI = 0;
+  u32* vbase = nullptr;   // V+1
+  u32* vfile = nullptr;
+  u8* vpass = nullptr;    // passes served (bit0 host, bit1 device)
+  u32* veof = nullptr;    // 2V (line, col)
+  u32* vtok = nullptr;    // VT
+  u32* vview = nullptr;   // VT
+  u32* item_start = nullptr, *item_view = nullptr, *item_root = nullptr, *item_end = nullptr;
+  u8* item_stat = nullptr;
+  PErr* item_err = nullptr;
+  u32* vfirst = nullptr;  // V+1 first segment item of each view
+  u32* vbad = nullptr;    // V
+  u8* vstat = nullptr;    // 0 ok, 1 failed, 2 fallback ok
+  u32* vfb_base = nullptr, *vfb_cnt = nullptr;
+  u32* fb_items = nullptr;
+  u32* vfi = nullptr;     // V+1 final item range
+  u32* fitems = nullptr;  // FI root nodes
+  u32* fitem_view = nullptr;
+  Node* nodes = nullptr;
+  u64 n_nodes = 0;
+  void free_all() {
+    void* ps[] = {vbase, vfile, vpass, veof, vtok, vview, item_start, item_view, item_root,
+                  item_end, item_stat, item_err, vfirst, vbad, vstat, vfb_base, vfb_cnt,
+                  fb_items, vfi, fitems, fitem_view, nodes};
+    for (void* p : ps) dfree(p);
+  }
+};
+
+EXS_HD inline u64 node_base(const u32* item_start, u32 j) { return 2ull * item_start[j] + 4ull * j; }
+
+inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& sc, cudaStream_t st) {
+  const u32 F = L.F, T = L.T;
+  // 1. files whose passes see different token sets
+  u32* split = dalloc<u32>(F + 1);
+  dzero(split, (F + 1) * 4, st);
+  {
+    const Tok* tk = L.toks;
+    par_for(T, [=] EXS_HD (i64 t) {
+      u8 m = tk[t].mask;
+      if (m == 1 || m == 2) at_or(&split[tk[t].file], 1u);
+    }, st);
+  }
+  // 2. views per file
+  u32* fvc = dalloc<u32>(F + 1);
+  u32* fvb = dalloc<u32>(F + 1);
+  {
+    const FP* fp = L.fp; const u8* cf = L.cfg;
+    par_for(F + 1, [=] EXS_HD (i64 f) {
+      if (f == F) { fvc[f] = 0; return; }
+      bool ok[2];
+      for (int p = 0; p < 2; p++) ok[p] = fp[2 * f + p].pp_line == NONE && fp[2 * f + p].lex_line == NONE;
+      u32 c;
+      if (cf[f] & CFG_PLAIN) c = ok[0];
+      else if (ok[0] && ok[1] && !split[f]) c = 1;
+      else c = (u32)ok[0] + (u32)ok[1];
+      fvc[f] = c;
+    }, st);
+  }
+  excl_scan_u32(fvc, fvb, F + 1, sc, st);
+  P.V = get1(fvb + F, st);
+  const u32 V = P.V;
+  P.vbase = dalloc<u32>(V + 1);
+  P.vfile = dalloc<u32>(V + 1);
+  P.vpass = dalloc<u8>(V + 1);
+  P.veof = dalloc<u32>(2 * (size_t)V + 2);
+  u32* vcnt = dalloc<u32>(V + 1);
+  // token pass flags and their scans
+  u32* s0 = dalloc<u32>(T + 1);
+  u32* s1 = dalloc<u32>(T + 1);
+  {
+    u32* f0 = dalloc<u32>(T + 1);
+    u32* f1 = dalloc<u32>(T + 1);
+    const Tok* tk = L.toks;
+    par_for(T + 1, [=] EXS_HD (i64 t) {
+      if (t == T) { f0[t] = f1[t] = 0; return; }
+      f0[t] = tk[t].mask & 1;
+      f1[t] = (tk[t].mask >> 1) & 1;
+    }, st);
+    excl_scan_u32(f0, s0, T + 1, sc, st);
+    excl_scan_u32(f1, s1, T + 1, sc, st);
+    sync(st);
+    dfree(f0);
+    dfree(f1);
+  }
+  {
+    FP* fp = L.fp; const u8* cf = L.cfg; const u32* fl = L.fline; const u32* lt = L.line_tok;
+    u32* vf = P.vfile; u8* vp = P.vpass; u32* ve = P.veof;
+    par_for(F, [=] EXS_HD (i64 f) {
+      u32 v = fvb[f];
+      u32 c = fvc[f];
+      if (!c) return;
+      u32 tf0 = lt[fl[f]], tf1 = lt[fl[f + 1]];
+      bool ok0 = fp[2 * f].pp_line == NONE && fp[2 * f].lex_line == NONE;
+      bool ok1 = !(cf[f] & CFG_PLAIN) && fp[2 * f + 1].pp_line == NONE && fp[2 * f + 1].lex_line == NONE;
+      if (c == 1 && ok0 && ok1) {
+        vf[v] = (u32)f; vp[v] = 3;
+        fp[2 * f].view = v; fp[2 * f + 1].view = v;
+        ve[2 * v] = fp[2 * f].eof_line; ve[2 * v + 1] = fp[2 * f].eof_col;
+        vcnt[v] = s0[tf1] - s0[tf0];
+        return;
+      }
+      for (u32 p = 0; p < 2; p++) {
+        bool okp = p ? ok1 : ok0;
+        if (!okp) continue;
+        vf[v] = (u32)f; vp[v] = (u8)(1u << p);
+        fp[2 * f + p].view = v;
+        ve[2 * v] = fp[2 * f + p].eof_line; ve[2 * v + 1] = fp[2 * f + p].eof_col;
+        vcnt[v] = p ? (s1[tf1] - s1[tf0]) : (s0[tf1] - s0[tf0]);
+        v++;
+      }
+    }, st);
+  }
+  h2d(vcnt + V, "\0\0\0\0", 4, st);
+  excl_scan_u32(vcnt, P.vbase, V + 1, sc, st);
+  P.VT = get1(P.vbase + V, st);
+  const u32 VT = P.VT;
+  P.vtok = dalloc<u32>(VT + 1);
+  P.vview = dalloc<u32>(VT + 1);
+  {
+    const Tok* tk = L.toks; const FP* fp = L.fp; const u32* fl = L.fline; const u32* lt = L.line_tok;
+    const u32* vb = P.vbase; const u8* vp = P.vpass; u32* vt = P.vtok; u32* vv = P.vview;
+    par_for(T, [=] EXS_HD (i64 t) {
+      u32 f = tk[t].file;
+      u8 m = tk[t].mask;
+      u32 tf0 = lt[fl[f]];
+      for (u32 p = 0; p < 2; p++) {
+        u32 v = fp[2 * f + p].view;
+        if (v == NONE) continue;
+        if (p == 1 && vp[v] == 3) continue;
+        if (!((m >> p) & 1)) continue;
+        u32 i = vb[v] + (p ? (s1[t] - s1[tf0]) : (s0[t] - s0[tf0]));
+        vt[i] = (u32)t;
+        vv[i] = v;
+      }
+    }, st);
+  }
+  sync(st);
+  dfree(s0); dfree(s1); dfree(vcnt); dfree(fvc); dfree(fvb); dfree(split);
+  // 3. segmentation: depth scan and item starts (depth over ( ) { })
+  {
+    i64* el = dalloc<i64>(VT + 1);
+    i64* inc = dalloc<i64>(VT + 1);
+    const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vv = P.vview; const u32* vb = P.vbase;
+    par_for(VT, [=] EXS_HD (i64 i) {
+      const Tok& t = tk[vt[i]];
+      i64 d = 0;
+      if (t.kind == TK_PUNCT) {
+        if (t.id == P_LPAREN || t.id == P_LBRACE) d = 1;
+        else if (t.id == P_RPAREN || t.id == P_RBRACE) d = -1;
+      }
+      bool head = vb[vv[i]] == (u32)i;
+      el[i] = (d & 0xFFFFFFFFll) | (head ? (1ll << 40) : 0);
+    }, st);
+    incl_scan(el, inc, VT, DepthOp(), sc, st);
+    u8* endf = (u8*)el;  // reuse as end flags (VT bytes)
+    par_for(VT, [=] EXS_HD (i64 i) {
+      const Tok& t = tk[vt[i]];
+      int dep = (int)(u32)(inc[i] & 0xFFFFFFFFll);
+      bool e = false;
+      if (dep == 0 && t.kind == TK_PUNCT) {
+        if (t.id == P_SEMI) e = true;
+        else if (t.id == P_RBRACE) {
+          bool semi_next = (u32)i + 1 < vb[vv[i] + 1] && tk[vt[i + 1]].kind == TK_PUNCT && tk[vt[i + 1]].id == P_SEMI;
+          e = !semi_next;
+        }
+      }
+      endf[i] = e;
+    }, st);
+    P.item_start = dalloc<u32>(VT + 1);
+    auto pred = [=] EXS_HD (u32 i) -> bool {
+      if (vb[vv[i]] == i) return true;
+      return endf[i - 1] && vv[i - 1] == vv[i];
+    };
+    P.I = select_idx(VT, pred, P.item_start, L.cnt, sc, st);
+    sync(st);
+    dfree(inc);
+    dfree(el);
+  }
+  const u32 I = P.I;
+  P.item_view = dalloc<u32>(I + 1);
+  P.item_root = dalloc<u32>(I + 1);
+  P.item_end = dalloc<u32>(I + 1);
+  P.item_stat = dalloc<u8>(I + 1);
+  P.item_err = dalloc<PErr>(I + 1);
+  P.vfirst = dalloc<u32>(V + 1);
+  P.vbad = dalloc<u32>(V + 1);
+  P.vstat = dalloc<u8>(V + 1);
+  P.n_nodes = 2ull * VT + 4ull * I + 64;
+  P.nodes = dalloc<Node>(P.n_nodes);
+  {
+    const u32* is = P.item_start; const u32* vv = P.vview; u32* iv = P.item_view;
+    par_for(I, [=] EXS_HD (i64 j) { iv[j] = vv[is[j]]; }, st);
+    const u32* ivc = P.item_view; u32* vfst = P.vfirst; u32* vbad = P.vbad;
+    par_for(V + 1, [=] EXS_HD (i64 v) {
+      u32 lo = 0, hi = I;
+      while (lo < hi) { u32 mid = (lo + hi) / 2; if (ivc[mid] < v) lo = mid + 1; else hi = mid; }
+      vfst[v] = lo;
+      if (v < V) vbad[v] = NONE;
+    }, st);
+  }
+  // 4. item-parallel parse
+  {
+    const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase; const u32* ve = P.veof;
+    const u32* is = P.item_start; const u32* iv = P.item_view; const u32* vf = P.vfile;
+    const u8* cf = L.cfg; const u8* s = L.src; const u32* sp = L.splice;
+    Node* nd = P.nodes; u32* ir = P.item_root; u32* ie = P.item_end; u8* ist = P.item_stat;
+    PErr* ier = P.item_err; u32* vbad = P.vbad;
+    par_for(I, [=] EXS_HD (i64 j) {
+      u32 v = iv[j];
+      u32 next = (j + 1 < I && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
+      u8 c = cf[vf[v]];
+      PView pv{tk, vt, vb[v], vb[v + 1] - vb[v], ve[2 * v], ve[2 * v + 1],
+               (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0)};
+      Parser p;
+      u64 base = node_base(is, (u32)j);
+      p.init(pv, nd, (u32)base, 2 * (next - is[j]) + 4, is[j] - vb[v]);
+      p.v_src = s; p.v_splice = sp;
+      u32 root = p.item();
+      ir[j] = root;
+      ie[j] = vb[v] + p.pos;
+      u8 stt = 0;
+      if (p.failed) stt = p.overflow ? 2 : 1;
+      ist[j] = stt;
+      ier[j] = p.e;
+      if (stt || vb[v] + p.pos != next) at_min(&vbad[v], (u32)j);
+    }, st);
+  }
+  // 5. per view: parse error, ok, or sequential repair
+  u32 nfb = 0;
+  std::vector<u32> fb_views;
+  {
+    u8* vs = P.vstat; const u32* vbad = P.vbad; const u8* ist = P.item_stat; const PErr* ier = P.item_err;
+    const u32* vf = P.vfile; const u8* vp = P.vpass; FP* fp = L.fp; WalkBufs B = WB;
+    u32* fbflag = dalloc<u32>(V + 1);
+    par_for(V, [=] EXS_HD (i64 v) {
+      u32 j = vbad[v];
+      fbflag[v] = 0;
+      if (j == NONE) { vs[v] = 0; return; }
+      if (ist[j] == 1) {
+        vs[v] = 1;
+        const PErr& e = ier[j];
+        emit_diag(B, mkdiag(vf[v], e.line, e.col, C_E0001, e.msg, e.a0, e.a1));
+        for (u32 p = 0; p < 2; p++) if ((vp[v] >> p) & 1) fp[2 * vf[v] + p].perr = 1;
+        return;
+      }
+      vs[v] = 3;  // needs repair
+      fbflag[v] = 1;
+    }, st);
+    u32* fbl = dalloc<u32>(V + 1);
+    nfb = select_idx(V, [=] EXS_HD (u32 v) -> bool { return fbflag[v] != 0; }, fbl, L.cnt, sc, st);
+    fb_views.resize(nfb);
+    if (nfb) d2h(fb_views.data(), fbl, nfb * 4, st);
+    sync(st);
+    dfree(fbl);
+    dfree(fbflag);
+  }
+  P.vfb_base = dalloc<u32>(V + 1);
+  P.vfb_cnt = dalloc<u32>(V + 1);
+  dzero(P.vfb_cnt, (V + 1) * 4, st);
+  if (nfb) {
+    // capacity: items consume >= 5 tokens
+    std::vector<u32> vbh(V + 1);
+    d2h(vbh.data(), P.vbase, (V + 1) * 4, st);
+    sync(st);
+    std::vector<u32> fbb(V + 1, 0);
+    u32 tot = 0;
+    for (u32 v : fb_views) { fbb[v] = tot; tot += (vbh[v + 1] - vbh[v]) / 5 + 2; }
+    h2d(P.vfb_base, fbb.data(), (V + 1) * 4, st);
+    P.fb_items = dalloc<u32>(tot + 1);
+    u32* fbl = dalloc<u32>(nfb);
+    h2d(fbl, fb_views.data(), nfb * 4, st);
+    const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase; const u32* ve = P.veof;
+    const u32* is = P.item_start; const u32* vfst = P.vfirst; const u32* vf = P.vfile;
+    const u8* cf = L.cfg; const u8* s = L.src; const u32* sp = L.splice; Node* nd = P.nodes;
+    u32* fbi = P.fb_items; u32* fbase = P.vfb_base; u32* fcnt = P.vfb_cnt; u8* vs = P.vstat;
+    const u8* vp = P.vpass; FP* fp = L.fp; WalkBufs B = WB;
+    par_for(nfb, [=] EXS_HD (i64 k) {
+      u32 v = fbl[k];
+      u8 c = cf[vf[v]];
+      PView pv{tk, vt, vb[v], vb[v + 1] - vb[v], ve[2 * v], ve[2 * v + 1],
+               (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0)};
+      u64 base = node_base(is, vfst[v]);
+      u64 lim = node_base(is, vfst[v + 1]);
+      Parser p;
+      p.init(pv, nd, (u32)base, (u32)(lim - base), 0);
+      p.v_src = s; p.v_splice = sp;
+      u32 n = 0;
+      while (p.pos < pv.n) {
+        u32 root = p.item();
+        if (p.failed) break;
+        fbi[fbase[v] + n++] = root;
+      }
+      if (p.failed) {
+        vs[v] = 1;
+        if (p.overflow) {
+          emit_diag(B, mkdiag(vf[v], 1, 1, C_X9999, M_X_CONTRACT));
+        } else {
+          emit_diag(B, mkdiag(vf[v], p.e.line, p.e.col, C_E0001, p.e.msg, p.e.a0, p.e.a1));
+        }
+        for (u32 q = 0; q < 2; q++) if ((vp[v] >> q) & 1) fp[2 * vf[v] + q].perr = 1;
+        return;
+      }
+      fcnt[v] = n;
+      vs[v] = 2;
+    }, st);
+    sync(st);
+    dfree(fbl);
+  }
+  // 6. final ordered item lists
+  {
+    u32* cnt = dalloc<u32>(V + 1);
+    const u8* vs = P.vstat; const u32* vfst = P.vfirst; const u32* fcnt = P.vfb_cnt;
+    par_for(V + 1, [=] EXS_HD (i64 v) {
+      if (v == V) { cnt[v] = 0; return; }
+      cnt[v] = vs[v] == 0 ? vfst[v + 1] - vfst[v] : (vs[v] == 2 ? fcnt[v] : 0);
+    }, st);
+    P.vfi = dalloc<u32>(V + 1);
+    excl_scan_u32(cnt, P.vfi, V + 1, sc, st);
+    P.FI = get1(P.vfi + V, st);
+    P.fitems = dalloc<u32>(P.FI + 1);
+    P.fitem_view = dalloc<u32>(P.FI + 1);
+    const u32* vfi = P.vfi; const u32* ir = P.item_root; const u32* fbi = P.fb_items;
+    const u32* fbase = P.vfb_base; u32* fit = P.fitems; u32* fiv = P.fitem_view;
+    const u32 Vv = V;
+    par_for(P.FI, [=] EXS_HD (i64 i) {
+      u32 lo = 0, hi = Vv;  // last view with vfi[v] <= i
+      while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (vfi[mid] <= (u32)i) lo = mid; else hi = mid; }
+      u32 v = lo, k = (u32)i - vfi[v];
+      fit[i] = vs[v] == 0 ? ir[vfst[v] + k] : fbi[fbase[v] + k];
+      fiv[i] = v;
+    }, st);
+    sync(st);
+    dfree(cnt);
+  }
+}
+
+}  // namespace exs

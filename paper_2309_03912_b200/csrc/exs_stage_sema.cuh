@@ -1,0 +1,442 @@
+// exs_stage_sema.cuh -- driver for K5: declaration records, the GPU hash-table
+// symbol join (structs, overload sets, signature duplicates) and the
+// unit-level checks of resolve() (reference: sema.py:152-320).
+#pragma once
+#include "exs_stage_parse.cuh"
+#include "exs_sema.cuh"
+
+namespace exs {
+
+struct SemaState {
+  u32 NF = 0, NR = 0, NC = 0;
+  FnRec* fns = nullptr;
+  RecRec* recs = nullptr;
+  u32* item_fn = nullptr;   // FI+1 exclusive scan of fn counts per item
+  u32* item_rec = nullptr;
+  u64* smap_k = nullptr; u32* smap_v = nullptr; u32 smap_mask = 0;
+  u64* fmap_k = nullptr; u32* fmap_v = nullptr; u32 fmap_mask = 0;
+  u64* sig_k = nullptr; u32* sig_v = nullptr; u32 sig_mask = 0;    // resolve duplicates
+  u64* siga_k = nullptr; u32* siga_v = nullptr; u32 siga_mask = 0; // walk-visible sig reps
+  u32* fcand = nullptr, *fcand_cnt = nullptr;
+  Tables tab;
+  void free_all() {
+    void* ps[] = {fns, recs, item_fn, item_rec, smap_k, smap_v, fmap_k, fmap_v, sig_k, sig_v,
+                  siga_k, siga_v, fcand, fcand_cnt};
+    for (void* p : ps) dfree(p);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// canonical printer as a hash stream (nodes.py:336-383)
+
+struct HashPrinter {
+  const Node* nodes;
+  const Tok* toks;
+  const u8* src;
+  const u32* splice;
+  u64 h;
+  int depth;
+  EXS_HD void s(const char* t) { while (*t) h = fnv_step(h, (u8)*t++); }
+  EXS_HD void c(u8 ch) { h = fnv_step(h, ch); }
+  EXS_HD void tok_text(u32 t) {
+    const Tok& k = toks[t];
+    for (u32 p = k.pos; p < k.end; p++)
+      if (!((splice[p >> 5] >> (p & 31)) & 1u)) h = fnv_step(h, src[p]);
+  }
+  EXS_HD void u64dec(u64 v) {
+    char b[24]; int n = 0;
+    do { b[n++] = (char)('0' + v % 10); v /= 10; } while (v);
+    while (n) c((u8)b[--n]);
+  }
+  EXS_HD void targs(u32 l) {
+    if (l == NONE) return;
+    s("< ");
+    bool first = true;
+    for (; l != NONE; l = nodes[l].next) {
+      if (!first) s(", ");
+      first = false;
+      if (nodes[l].kind == N_TYPE) type(l); else expr(l);
+    }
+    s(" >");
+  }
+  EXS_HD void type(u32 t) {
+    tok_text(nodes[t].tok);
+    targs(nodes[t].c0);
+  }
+  EXS_HD void args(u32 l) {
+    bool first = true;
+    for (; l != NONE; l = nodes[l].next) {
+      if (!first) s(", ");
+      first = false;
+      expr(l);
+    }
+  }
+  EXS_HD void expr(u32 e) {
+    if (++depth > 400) { depth--; return; }
+    const Node& n = nodes[e];
+    switch (n.kind) {
+      case N_INT: u64dec(toks[n.tok].hv); break;
+      case N_STR: c('"'); tok_text(n.tok); c('"'); break;
+      case N_BOOL: s(n.sub ? "true" : "false"); break;
+      case N_HDCV: s(n.sub == 1 ? "HDC::Hst" : (n.sub == 2 ? "HDC::Dev" : "HDC::HstDev")); break;
+      case N_ARCH: s("cuda_arch"); break;
+      case N_NAME: tok_text(n.tok); break;
+      case N_TMP: type(n.c0); s("{}"); break;
+      case N_TRAIT: s("hdc< "); type(n.c0); s(" >"); break;
+      case N_MCONST: type(n.c0); s("::"); tok_text(n.tok); break;
+      case N_CALL:
+        if (n.sub == CALL_STD) { s("std::"); tok_text(n.c0); }
+        else { tok_text(n.tok); targs(n.c1); }
+        c('('); args(n.c2); c(')');
+        break;
+      case N_MCALL: expr(n.c0); c('.'); tok_text(n.tok); targs(n.c1); c('('); args(n.c2); c(')'); break;
+      case N_SCALL: type(n.c0); s("::"); tok_text(n.tok); targs(n.c1); c('('); args(n.c2); c(')'); break;
+      case N_NOT: c('!'); expr(n.c0); break;
+      case N_BIN:
+        c('('); expr(n.c0);
+        s(n.sub == OP_OR ? " || " : (n.sub == OP_AND ? " && " : (n.sub == OP_EQ ? " == " : " != ")));
+        expr(n.c1); c(')');
+        break;
+      default: break;
+    }
+    depth--;
+  }
+};
+
+// signature_key hash (sema.py:144-149) with the spaces string under P2 (133-141)
+EXS_HD inline u64 sig_hash(const Node* nodes, const Tok* toks, const u8* src, const u32* sp,
+                           u32 fn_node, u32 owner_name_tok, bool p2) {
+  HashPrinter hp{nodes, toks, src, sp, fnv_init(), 0};
+  const Node& f = nodes[fn_node];
+  const Node& x = nodes[fn_node + 1];
+  if (owner_name_tok != NONE) hp.tok_text(owner_name_tok);
+  hp.c(0x1f);
+  hp.tok_text(f.tok);
+  hp.c(0x1f);
+  for (u32 p = f.c1; p != NONE; p = nodes[p].next) { hp.type(nodes[p].c0); hp.c(0x1e); }
+  hp.c(0x1f);
+  if (x.c0 != NONE) hp.expr(x.c0);
+  hp.c(0x1f);
+  if (p2) {
+    if (f.n & FF_H) { hp.c('H'); if (x.c1 != NONE) { hp.c('('); hp.expr(x.c1); hp.c(')'); } }
+    if (f.n & FF_D) { hp.c('D'); if (x.c2 != NONE) { hp.c('('); hp.expr(x.c2); hp.c(')'); } }
+    if (f.n & FF_G) hp.c('G');
+  }
+  return nz(hp.h);
+}
+
+// call sites + E0101 checks over one body (sema.py:251-320)
+struct BodyScan {
+  const Node* nodes;
+  const Tok* toks;
+  const Tables* T;
+  u32 view;
+  bool plain;
+  u32 ncalls;
+  // emit
+  const WalkBufs* B;
+  u32 file;
+  int depth;
+  EXS_HD void expr(u32 e) {
+    if (++depth > 400) { depth--; return; }
+    const Node& n = nodes[e];
+    switch (n.kind) {
+      case N_CALL: {
+        ncalls++;
+        bool known;
+        if (n.sub == CALL_STD) {
+          known = toks[n.c0].id == W_ABORT;  // std::abort is the only std builtin
+        } else {
+          known = T->fmap.find(vkey(view, toks[n.tok].hv)) != NONE;
+          if (!known) {
+            u8 w = toks[n.tok].id;
+            known = w == W_PRINTF || w == W_RELEASE_ASSERT || w == W_ABORT ||
+                    ((w == W_TRAP || w == W_CUDASYNC) && !plain);
+          }
+        }
+        if (!known && B) {
+          const Tok& k = toks[n.tok];
+          u64 a1 = n.sub == CALL_STD ? (((u64)toks[n.c0].pos << 32) | (toks[n.c0].end - toks[n.c0].pos)) : 0;
+          emit_diag(*B, mkdiag(file, k.line, k.col, C_E0101, M_S_UNDEF_NAME,
+                               ((u64)k.pos << 32) | (k.end - k.pos), a1, 0, n.sub == CALL_STD));
+        }
+        for (u32 a = n.c2; a != NONE; a = nodes[a].next) expr(a);
+        break;
+      }
+      case N_SCALL:
+        ncalls++;
+        for (u32 a = n.c2; a != NONE; a = nodes[a].next) expr(a);
+        break;
+      case N_MCALL:
+        ncalls++;
+        expr(n.c0);
+        for (u32 a = n.c2; a != NONE; a = nodes[a].next) expr(a);
+        break;
+      case N_NOT: expr(n.c0); break;
+      case N_BIN: expr(n.c0); expr(n.c1); break;
+      default: break;
+    }
+    depth--;
+  }
+  EXS_HD void stmts(u32 s) {
+    for (; s != NONE; s = nodes[s].next) {
+      const Node& n = nodes[s];
+      switch (n.kind) {
+        case N_SEXPR: expr(n.c0); break;
+        case N_SRET: if (n.c0 != NONE) expr(n.c0); break;
+        case N_SIF: expr(n.c0); stmts(n.c1); if (n.sub) stmts(n.c2); break;
+        case N_SFOR: expr(n.c0); expr(n.c1); stmts(n.c2); break;
+        case N_SLAUNCH: {
+          expr(n.c1);
+          expr(nodes[n.c1].next);
+          for (u32 a = n.c2; a != NONE; a = nodes[a].next) expr(a);
+          ncalls++;
+          if (B && T->fmap.find(vkey(view, toks[n.tok].hv)) == NONE) {
+            const Tok& k = toks[n.tok];
+            emit_diag(*B, mkdiag(file, k.line, k.col, C_E0101, M_S_UNDEF_NAME,
+                                 ((u64)k.pos << 32) | (k.end - k.pos)));
+          }
+          break;
+        }
+        default: break;
+      }
+    }
+  }
+};
+
+inline u32 pow2_at_least(u64 n) {
+  u32 c = 1024;
+  while (c < n) c <<= 1;
+  return c;
+}
+
+inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& WB, Scratch& sc,
+                     cudaStream_t st) {
+  const u32 FI = P.FI, V = P.V;
+  // 1. declaration records in _all_decls order (spacecheck.py:264-270)
+  u32* cf = dalloc<u32>(FI + 1);
+  u32* cr = dalloc<u32>(FI + 1);
+  {
+    const Node* nd = P.nodes; const u32* fit = P.fitems;
+    par_for(FI + 1, [=] EXS_HD (i64 i) {
+      if (i == FI) { cf[i] = cr[i] = 0; return; }
+      const Node& n = nd[fit[i]];
+      u32 nf = 0, nr = 0;
+      if (n.kind == N_FN) nf = 1;
+      else if (n.kind == N_STRUCT) {
+        nr = 1;
+        for (u32 m = n.c1; m != NONE; m = nd[m].next) if (nd[m].kind == N_FN) nf++;
+      }
+      cf[i] = nf; cr[i] = nr;
+    }, st);
+  }
+  S.item_fn = dalloc<u32>(FI + 1);
+  S.item_rec = dalloc<u32>(FI + 1);
+  excl_scan_u32(cf, S.item_fn, FI + 1, sc, st);
+  excl_scan_u32(cr, S.item_rec, FI + 1, sc, st);
+  S.NF = get1(S.item_fn + FI, st);
+  S.NR = get1(S.item_rec + FI, st);
+  sync(st);
+  dfree(cf);
+  dfree(cr);
+  const u32 NF = S.NF, NR = S.NR;
+  S.fns = dalloc<FnRec>(NF + 1);
+  S.recs = dalloc<RecRec>(NR + 1);
+  {
+    Node* nd = P.nodes; const u32* fit = P.fitems; const u32* fiv = P.fitem_view;
+    const u32* ifn = S.item_fn; const u32* irc = S.item_rec; FnRec* fr = S.fns; RecRec* rr = S.recs;
+    const Tok* tk = L.toks;
+    par_for(FI, [=] EXS_HD (i64 i) {
+      Node& n = nd[fit[i]];
+      u32 v = fiv[i];
+      u32 f = ifn[i];
+      auto put = [&](u32 node, u32 rec) {
+        FnRec& r = fr[f];
+        r.node = node; r.view = v; r.rec = rec; r.order = f;
+        r.name = tk[nd[node].tok].hv; r.sig = 0; r.sig_rep = f; r.ncalls = 0;
+        r.flags = rec == NONE ? 0 : FR_MEMBER;
+        nd[node + 1].tok = f;  // FNX.tok -> decl record
+        f++;
+      };
+      if (n.kind == N_FN) put(fit[i], NONE);
+      else if (n.kind == N_STRUCT) {
+        u32 r = irc[i];
+        RecRec& q = rr[r];
+        q.node = fit[i]; q.view = v; q.order = r; q.dup = 0; q.name = tk[n.tok].hv;
+        n.c2 = r;
+        for (u32 m = n.c1; m != NONE; m = nd[m].next) if (nd[m].kind == N_FN) put(m, r);
+      }
+    }, st);
+  }
+  // 2. struct table: first definition wins (sema.py:176-184)
+  S.smap_mask = pow2_at_least(2ull * NR + 2) - 1;
+  S.smap_k = dalloc<u64>(S.smap_mask + 1);
+  S.smap_v = dalloc<u32>(S.smap_mask + 1);
+  dzero(S.smap_k, 8ull * (S.smap_mask + 1), st);
+  dfill_ff(S.smap_v, 4ull * (S.smap_mask + 1), st);
+  {
+    u64* k = S.smap_k; u32* vv = S.smap_v; u32 mask = S.smap_mask; RecRec* rr = S.recs;
+    par_for(NR, [=] EXS_D (i64 r) { map_insert_min(k, vv, mask, vkey(rr[r].view, rr[r].name), (u32)r); }, st);
+    Map m{k, vv, mask};
+    const Node* nd = P.nodes; const Tok* tk = L.toks; const u32* vf = P.vfile; WalkBufs B = WB;
+    par_for(NR, [=] EXS_HD (i64 r) {
+      RecRec& q = rr[r];
+      q.dup = m.find(vkey(q.view, q.name)) != (u32)r;
+      if (q.dup) {
+        const Tok& t = tk[nd[q.node].tok];
+        emit_diag(B, mkdiag(vf[q.view], t.line, t.col, C_E0102, M_S_DUP, ((u64)t.pos << 32) | (t.end - t.pos)));
+      }
+    }, st);
+  }
+  // 3. owner flags, signature hashes
+  {
+    FnRec* fr = S.fns; const RecRec* rr = S.recs; const Node* nd = P.nodes; const Tok* tk = L.toks;
+    const u8* s = L.src; const u32* sp = L.splice; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
+    par_for(NF, [=] EXS_HD (i64 i) {
+      FnRec& r = fr[i];
+      u32 owner_tok = NONE;
+      if (r.rec != NONE && !rr[r.rec].dup) { r.flags |= FR_OWNER; owner_tok = nd[rr[r.rec].node].tok; }
+      bool p2 = (cfgs[vf[r.view]] & CFG_MODE_MASK) == MODE_P2;
+      r.sig = sig_hash(nd, tk, s, sp, r.node, owner_tok, p2);
+    }, st);
+  }
+  // 4. duplicates among free functions and members of kept structs (sema.py:161-195)
+  S.sig_mask = pow2_at_least(2ull * NF + 2) - 1;
+  S.sig_k = dalloc<u64>(S.sig_mask + 1);
+  S.sig_v = dalloc<u32>(S.sig_mask + 1);
+  S.siga_mask = S.sig_mask;
+  S.siga_k = dalloc<u64>(S.sig_mask + 1);
+  S.siga_v = dalloc<u32>(S.sig_mask + 1);
+  dzero(S.sig_k, 8ull * (S.sig_mask + 1), st);
+  dfill_ff(S.sig_v, 4ull * (S.sig_mask + 1), st);
+  dzero(S.siga_k, 8ull * (S.sig_mask + 1), st);
+  dfill_ff(S.siga_v, 4ull * (S.sig_mask + 1), st);
+  {
+    FnRec* fr = S.fns; const RecRec* rr = S.recs;
+    u64* k = S.sig_k; u32* vv = S.sig_v; u32 mask = S.sig_mask;
+    par_for(NF, [=] EXS_D (i64 i) {
+      const FnRec& r = fr[i];
+      if (r.rec != NONE && rr[r.rec].dup) return;  // members of duplicate structs are never checked
+      map_insert_min(k, vv, mask, vkey(r.view, r.sig), (u32)i);
+    }, st);
+    Map m{k, vv, mask};
+    const Node* nd = P.nodes; const Tok* tk = L.toks; const u32* vf = P.vfile; WalkBufs B = WB;
+    par_for(NF, [=] EXS_HD (i64 i) {
+      FnRec& r = fr[i];
+      if (r.rec != NONE && rr[r.rec].dup) return;
+      if (m.find(vkey(r.view, r.sig)) != (u32)i) {
+        r.flags |= FR_DUP;
+        const Tok& t = tk[nd[r.node].tok];
+        u64 osp = 0;
+        if (r.flags & FR_OWNER) { const Tok& o = tk[nd[rr[r.rec].node].tok]; osp = ((u64)o.pos << 32) | (o.end - o.pos); }
+        emit_diag(B, mkdiag(vf[r.view], t.line, t.col, C_E0102, M_S_DUP, ((u64)t.pos << 32) | (t.end - t.pos), osp));
+      }
+    }, st);
+    u64* ka = S.siga_k; u32* va = S.siga_v;
+    par_for(NF, [=] EXS_D (i64 i) {
+      const FnRec& r = fr[i];
+      if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) return;  // removed from the struct
+      map_insert_min(ka, va, mask, vkey(r.view, r.sig), (u32)i);
+    }, st);
+    Map ma{ka, va, mask};
+    par_for(NF, [=] EXS_HD (i64 i) {
+      FnRec& r = fr[i];
+      u32 rep = ma.find(vkey(r.view, r.sig));
+      r.sig_rep = rep == NONE ? (u32)i : rep;
+    }, st);
+  }
+  // 5. overload sets of free functions, in item order
+  {
+    u32* idx = dalloc<u32>(NF + 1);
+    FnRec* fr = S.fns;
+    S.NC = select_idx(NF, [=] EXS_HD (u32 i) -> bool { return fr[i].rec == NONE && !(fr[i].flags & FR_DUP); },
+                      idx, L.cnt, sc, st);
+    const u32 NC = S.NC;
+    u64* keys = dalloc<u64>(NC + 1);
+    par_for(NC, [=] EXS_HD (i64 i) { keys[i] = vkey(fr[idx[i]].view, fr[idx[i]].name); }, st);
+    sort_pairs(keys, idx, NC, sc, st);
+    S.fcand = idx;
+    S.fcand_cnt = dalloc<u32>(NC + 1);
+    S.fmap_mask = pow2_at_least(2ull * NC + 2) - 1;
+    S.fmap_k = dalloc<u64>(S.fmap_mask + 1);
+    S.fmap_v = dalloc<u32>(S.fmap_mask + 1);
+    dzero(S.fmap_k, 8ull * (S.fmap_mask + 1), st);
+    dfill_ff(S.fmap_v, 4ull * (S.fmap_mask + 1), st);
+    u32* cnt = S.fcand_cnt; u64* fk = S.fmap_k; u32* fv = S.fmap_v; u32 mask = S.fmap_mask;
+    par_for(NC, [=] EXS_D (i64 i) {
+      if (i > 0 && keys[i - 1] == keys[i]) return;
+      u32 j = (u32)i;
+      while (j < NC && keys[j] == keys[i]) j++;
+      cnt[i] = j - (u32)i;
+      map_insert_min(fk, fv, mask, keys[i], (u32)i);
+    }, st);
+    sync(st);
+    dfree(keys);
+  }
+  // tables for the evaluator
+  S.tab.nodes = P.nodes; S.tab.toks = L.toks; S.tab.fns = S.fns; S.tab.recs = S.recs;
+  S.tab.smap = Map{S.smap_k, S.smap_v, S.smap_mask};
+  S.tab.fmap = Map{S.fmap_k, S.fmap_v, S.fmap_mask};
+  S.tab.fcand = S.fcand; S.tab.fcand_cnt = S.fcand_cnt;
+  S.tab.src = L.src; S.tab.splice = L.splice;
+  // 6. mode-gated syntax (sema.py:221-248), call sites, undefined names
+  {
+    const Tables tab = S.tab;
+    const RecRec* rr = S.recs; const Node* nd = P.nodes; const Tok* tk = L.toks;
+    const u32* vf = P.vfile; const u8* cfgs = L.cfg; WalkBufs B = WB;
+    par_for(NR, [=] EXS_HD (i64 r) {
+      const RecRec& q = rr[r];
+      u8 mode = cfgs[vf[q.view]] & CFG_MODE_MASK;
+      const Node& n = nd[q.node];
+      if (mode != MODE_P2 && (n.n & (SF_H | SF_D | SF_G))) {
+        const Tok& t = tk[n.tok];
+        emit_diag(B, mkdiag(vf[q.view], t.line, t.col, C_E0001, M_S_STRUCT_SPEC_MODE));
+      }
+    }, st);
+    FnRec* fr = S.fns;
+    par_for(NF, [=] EXS_HD (i64 i) {
+      FnRec& r = fr[i];
+      if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) return;  // not in the struct any more
+      u8 c = cfgs[vf[r.view]];
+      u8 mode = c & CFG_MODE_MASK;
+      const Node& n = nd[r.node];
+      if (mode != MODE_P1 && (n.n & (FF_HPRED | FF_DPRED))) {
+        const Tok& t = tk[n.tok];
+        emit_diag(B, mkdiag(vf[r.view], t.line, t.col, C_E0001, M_S_COND_SPEC_MODE));
+      }
+      if (n.n & FF_BODY) {
+        BodyScan bs{nd, tk, &tab, r.view, (c & CFG_PLAIN) != 0, 0, &B, vf[r.view], 0};
+        bs.stmts(n.c2);
+        r.ncalls = bs.ncalls;
+      }
+    }, st);
+  }
+  // 7. static assertions (sema.py:200-217)
+  {
+    const Tables* tabp = nullptr;
+    Tables* dt = dalloc<Tables>(1);
+    h2d(dt, &S.tab, sizeof(Tables), st);
+    tabp = dt;
+    const u32* fit = P.fitems; const u32* fiv = P.fitem_view; const Node* nd = P.nodes;
+    const u32* vf = P.vfile; const u8* cfgs = L.cfg; WalkBufs B = WB;
+    par_for(FI, [=] EXS_HD (i64 i) {
+      const Node& n = nd[fit[i]];
+      if (n.kind != N_ASSERT) return;
+      u32 v = fiv[i];
+      Sema S2;
+      S2.init(tabp, v, cfgs[vf[v]]);
+      Env e; e.clear();
+      Val out;
+      u8 stt = S2.eval(n.c0, e, false, out);
+      const Tok& t = S2.K(n.tok);
+      if (S2.contract) { emit_diag(B, mkdiag(vf[v], t.line, t.col, C_X9999, M_X_CONTRACT)); return; }
+      if (stt == ST_SUBST) emit_diag(B, mkdiag(vf[v], t.line, t.col, C_E0104, M_S_ASSERT_EVAL));
+      else if (stt == ST_SEMA) emit_diag(B, mkdiag(vf[v], S2.err.line, S2.err.col, S2.err.code, S2.err.msg, S2.err.a0, S2.err.a1, S2.err.a2));
+      else if (!(out.k == V_BOOL && out.x == 1)) emit_diag(B, mkdiag(vf[v], t.line, t.col, C_E0104, M_S_ASSERT_FAIL));
+    }, st);
+    sync(st);
+    dfree(dt);
+  }
+}
+
+}  // namespace exs

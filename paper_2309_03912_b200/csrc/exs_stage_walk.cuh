@@ -1,0 +1,404 @@
+// exs_stage_walk.cuh -- driver for K6..K8: root seeding, the level-synchronous
+// instantiation fixpoint, reachability, pending-stray verdicts and
+// __CUDA_ARCH__ divergence (reference: spacecheck.py:254-767).
+#pragma once
+#include "exs_stage_sema.cuh"
+#include "exs_walk.cuh"
+
+namespace exs {
+
+struct WalkState {
+  u32 cap_inst = 0, n_inst = 0, levels = 0;
+  u64 n_edges = 0, edge_cap = 0, callsites = 0;
+  IKey* slots = nullptr;
+  u32* sid = nullptr;
+  u32 mask = 0;
+  Inst* inst = nullptr;
+  u32* edges = nullptr;
+  Pending* pend = nullptr;
+  u32 cap_pend = 0;
+  u32* seeds = nullptr;
+  u32 cap_seeds = 0;
+  CreateLog* log = nullptr;
+  u32 cap_log = 0;
+  u32* main_inst = nullptr;
+  unsigned long long* main_key = nullptr;
+  u32* counters = nullptr;  // [n_inst, n_pend, n_seeds, n_log, overflow]
+  u8* visited = nullptr;
+  // per walk statistics
+  std::vector<u32> w_inst, w_edges, w_demands;
+  void free_all() {
+    void* ps[] = {slots, sid, inst, edges, pend, seeds, log, main_inst, main_key, counters, visited};
+    for (void* p : ps) dfree(p);
+    slots = nullptr; sid = nullptr; inst = nullptr; edges = nullptr; pend = nullptr; seeds = nullptr;
+    log = nullptr; main_inst = nullptr; main_key = nullptr; counters = nullptr; visited = nullptr;
+  }
+};
+
+struct WalkCfg {
+  const Tables* tab;  // device copy
+  const FnRec* fns;
+  const RecRec* recs;
+  const Node* nodes;
+  const Tok* toks;
+  const u32* vfile;
+  const u8* cfg;      // per file
+  const FP* fp;
+};
+
+// build a walker for an existing instance
+EXS_HD inline void walker_for(Walker& w, const WalkCfg& C, const WalkBufs& B, u32 id, u64 rank) {
+  const Inst& I = B.inst[id];
+  const FnRec& fr = C.fns[I.fn];
+  u32 file = C.vfile[fr.view];
+  u8 c = C.cfg[file];
+  w.S.init(C.tab, fr.view, c);
+  w.B = &B;
+  w.T = C.tab;
+  w.file = file;
+  w.walk = I.walk;
+  w.inst_id = id;
+  w.native = (u8)(I.walk & 1);
+  w.side = I.side;
+  w.spaces = I.spaces;
+  w.clevel = (u8)(I.level + 1);
+  w.fn = I.fn;
+  const Node& fn = C.nodes[fr.node];
+  w.pragma = (fn.n & FF_PRAGMA) != 0;
+  w.from_hd = I.spaces == 3;
+  w.fidelity_host = (c & CFG_MODE_MASK) == MODE_FIDELITY && w.native == 0;
+  w.parent_rank = rank;
+  w.local = 0;
+  w.ebase = I.ebase;
+  w.ecnt = 0;
+  w.contract = false;
+  w.orec_self = I.orec;
+  w.env.clear();
+  if (I.orec != NONE && I.ot.k == V_TYPE) w.S.struct_env(I.orec, I.ot, w.env);
+  w.obinds_self = w.env;
+  w.env.nbase = w.env.n;
+  w.add_binds(fn, I.tb, I.hb, w.env);
+  w.env.nbase = w.env.n;
+}
+
+inline WalkBufs make_bufs(WalkState& W, u32* n_diags, Diag* diags, u32 cap_diags, u64* dset,
+                          u32 dmask, u32* contract) {
+  WalkBufs B;
+  B.slots = W.slots; B.sid = W.sid; B.mask = W.mask; B.inst = W.inst;
+  B.n_inst = W.counters + 0; B.cap_inst = W.cap_inst;
+  B.edges = W.edges;
+  B.pend = W.pend; B.n_pend = W.counters + 1; B.cap_pend = W.cap_pend;
+  B.seeds = W.seeds; B.n_seeds = W.counters + 2; B.cap_seeds = W.cap_seeds;
+  B.log = W.log; B.n_log = W.counters + 3; B.cap_log = W.cap_log;
+  B.main_inst = W.main_inst; B.main_key = W.main_key;
+  B.diags = diags; B.n_diags = n_diags; B.cap_diags = cap_diags; B.dset = dset; B.dmask = dmask;
+  B.overflow = W.counters + 4;
+  B.contract = contract;
+  return B;
+}
+
+template <class T>
+void grow(T*& p, u64& cap_or_dummy, u64 need, u64 used, cudaStream_t st) {
+  if (need <= cap_or_dummy) return;
+  u64 nc = need + need / 2 + 1024;
+  T* q = dalloc<T>(nc);
+  if (p && used) d2d(q, p, used * sizeof(T), st);
+  sync(st);
+  dfree(p);
+  p = q;
+  cap_or_dummy = nc;
+}
+
+// returns false if a buffer overflowed (caller grows and retries)
+inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, WalkBufs& B0,
+                     Scratch& sc, cudaStream_t st, u32 diag_cap) {
+  const u32 F = L.F, NF = S.NF;
+  const u32 NW = 2 * F;
+  Tables* dtab = dalloc<Tables>(1);
+  h2d(dtab, &S.tab, sizeof(Tables), st);
+  WalkCfg C{dtab, S.fns, S.recs, P.nodes, L.toks, P.vfile, L.cfg, L.fp};
+  // buffers
+  W.mask = pow2_at_least(2ull * W.cap_inst) - 1;
+  W.slots = dalloc<IKey>((u64)W.mask + 1);
+  W.sid = dalloc<u32>((u64)W.mask + 1);
+  dzero(W.slots, sizeof(IKey) * ((u64)W.mask + 1), st);
+  dfill_ff(W.sid, 4ull * ((u64)W.mask + 1), st);
+  W.inst = dalloc<Inst>(W.cap_inst);
+  W.counters = dalloc<u32>(8);
+  dzero(W.counters, 32, st);
+  W.main_inst = dalloc<u32>(NW + 1);
+  W.main_key = dalloc<unsigned long long>(NW + 1);
+  dfill_ff(W.main_inst, 4ull * (NW + 1), st);
+  dzero(W.main_key, 8ull * (NW + 1), st);
+  u64 edge_cap = 0, pend_cap = 0, seed_cap = 0, log_cap = 0;
+  W.edges = nullptr; W.pend = nullptr; W.seeds = nullptr; W.log = nullptr;
+  // roots need log capacity 2 per decl and walk
+  grow(W.log, log_cap, 4ull * NF + 64, 0, st);
+  grow(W.pend, pend_cap, 1024, 0, st);
+  grow(W.seeds, seed_cap, 2048, 0, st);
+  grow(W.edges, edge_cap, 1024, 0, st);
+  auto bufs = [&]() {
+    W.cap_log = (u32)log_cap; W.cap_pend = (u32)pend_cap; W.cap_seeds = (u32)(seed_cap / 2);
+    WalkBufs B = make_bufs(W, B0.n_diags, B0.diags, diag_cap, B0.dset, B0.dmask, B0.contract);
+    return B;
+  };
+  WalkBufs B = bufs();
+  // ---- roots (spacecheck.py:272-308)
+  {
+    const FnRec* fr = S.fns; const RecRec* rr = S.recs; const Node* nd = P.nodes; const Tok* tk = L.toks;
+    const FP* fp = L.fp; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
+    const Tables* tab = dtab;
+    par_for(2ull * NF, [=] EXS_HD (i64 x) {
+      u32 i = (u32)(x >> 1), p = (u32)(x & 1);
+      const FnRec& r = fr[i];
+      u32 file = vf[r.view];
+      u32 walk = 2 * file + p;
+      if (fp[walk].view != r.view || fp[walk].perr) return;
+      if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) return;
+      const Node& fn = nd[r.node];
+      if (fn.c0 != NONE || !(fn.n & FF_BODY)) return;
+      if (r.rec != NONE && nd[rr[r.rec].node].c0 != NONE) return;
+      u8 c = cfgs[file];
+      u8 mode = c & CFG_MODE_MASK;
+      bool undec = !(fn.n & (FF_H | FF_D | FF_G));
+      if (mode == MODE_P2) {
+        bool rooted = (tk[fn.tok].id == W_MAIN && r.rec == NONE) || !undec ||
+                      (r.rec != NONE && (nd[rr[r.rec].node].n & (SF_H | SF_D | SF_G)));
+        if (!rooted) return;
+      }
+      Walker w;
+      w.S.init(tab, r.view, c);
+      w.B = &B; w.T = tab; w.file = file; w.walk = walk; w.inst_id = NONE;
+      w.native = (u8)p; w.side = 0; w.clevel = 0;  // roots are created at level 0
+      w.fn = i; w.pragma = false; w.from_hd = false;
+      w.fidelity_host = mode == MODE_FIDELITY && p == 0;
+      w.parent_rank = i; w.local = 0; w.contract = false;
+      Val ot = vnone();
+      if (r.rec != NONE) {
+        u32 canon = w.S.struct_of(rr[r.rec].name);
+        ot.k = V_TYPE; ot.rec = canon; ot.x = rr[r.rec].name; ot.bt = BT_NONE; ot.targ = 0;
+      }
+      Env none; none.clear();
+      u8 sides;
+      if (fn.n & FF_G) sides = 2;
+      else {
+        u8 sp;
+        w.S.depth = 0;
+        u8 stt = w.S.spaces(i, none, 0, fn.tok, r.rec, sp);
+        if (w.S.contract) { at_or(&B.contract[file], 1); return; }
+        if (stt == ST_SEMA) { w.emit_err(); return; }
+        if (stt == ST_SUBST) { w.emit_tok(C_E0001, fn.tok, M_W_PRED_CONST); return; }
+        sides = sp & 3;
+      }
+      u32 k = 0;
+      for (u8 sd = 0; sd < 2; sd++) {
+        if (!((sides >> sd) & 1)) continue;
+        w.local = k++;
+        w.instantiate(i, vnone(), vnone(), sd, r.rec, none, ot, fn.tok);
+      }
+    }, st);
+  }
+  // ---- levels
+  u32 prev_n = 0;
+  u32 level = 0;
+  u32* front = nullptr;
+  u64 front_cap = 0;
+  u64 edges_used = 0;
+  W.callsites = 0;
+  while (true) {
+    std::vector<u32> cnt(8);
+    d2h(cnt.data(), W.counters, 32, st);
+    sync(st);
+    if (cnt[4]) { dfree(dtab); dfree(front); return false; }
+    u32 n_now = cnt[0];
+    // fixup creators of this level (min creation key wins)
+    {
+      const CreateLog* lg = W.log; Inst* in = W.inst;
+      par_for(cnt[3], [=] EXS_HD (i64 j) {
+        const CreateLog& e = lg[j];
+        Inst& I = in[e.inst];
+        if (I.ckey == e.ckey) { I.at = e.at; I.fn = e.fn; }
+      }, st);
+    }
+    dzero(W.counters + 3, 4, st);
+    // ckey: atomicMin over creators
+    // (done inside instantiate via the log; apply min here)
+    u32 nnew = n_now - prev_n;
+    if (!nnew) break;
+    // frontier: new instances with bodies, ordered by creation key
+    grow(front, front_cap, nnew + 1, 0, st);
+    u32 nf;
+    {
+      const Inst* in = W.inst;
+      u32 base = prev_n;
+      u32* fr_tmp = dalloc<u32>(nnew + 1);
+      nf = select_idx(nnew, [=] EXS_HD (u32 j) -> bool { return (in[base + j].flags & IF_BODY) != 0; },
+                      fr_tmp, L.cnt, sc, st);
+      u64* keys = dalloc<u64>(nf + 1);
+      par_for(nf, [=] EXS_HD (i64 j) { fr_tmp[j] += base; keys[j] = in[fr_tmp[j]].ckey; }, st);
+      sort_pairs(keys, fr_tmp, nf, sc, st);
+      d2d(front, fr_tmp, 4ull * nf, st);
+      sync(st);
+      dfree(keys);
+      dfree(fr_tmp);
+    }
+    prev_n = n_now;
+    if (!nf) break;
+    // edge bases: scan of call-site counts
+    u32* ec = dalloc<u32>(nf + 1);
+    u32* eb = dalloc<u32>(nf + 1);
+    {
+      const Inst* in = W.inst; const FnRec* fr = S.fns; const u32* fl = front;
+      par_for(nf + 1, [=] EXS_HD (i64 j) { ec[j] = j < nf ? fr[in[fl[j]].fn].ncalls : 0; }, st);
+    }
+    excl_scan_u32(ec, eb, nf + 1, sc, st);
+    u64 S_level = get1(eb + nf, st);
+    W.callsites += S_level;
+    grow(W.edges, edge_cap, edges_used + S_level + 1, edges_used, st);
+    grow(W.log, log_cap, 2 * S_level + 64, 0, st);
+    u32 npend = cnt[1], nseeds = cnt[2];
+    grow(W.pend, pend_cap, (u64)npend + S_level + 64, npend, st);
+    grow(W.seeds, seed_cap, 2ull * (nseeds + S_level) + 64, 2ull * nseeds, st);
+    B = bufs();
+    {
+      Inst* in = W.inst; const u32* fl = front; u64 eu = edges_used;
+      par_for(nf, [=] EXS_HD (i64 j) { in[fl[j]].ebase = (u32)(eu + eb[j]); }, st);
+    }
+    edges_used += S_level;
+    // walk the frontier (one thread per instance)
+    {
+      const u32* fl = front;
+      WalkCfg Cc = C;
+      u32* ct = B.contract;
+      par_for(nf, [=] EXS_HD (i64 j) {
+        Walker w;
+        walker_for(w, Cc, B, fl[j], (u64)j);
+        w.run_body();
+        B.inst[fl[j]].ecnt = w.ecnt;
+        if (w.contract) at_or(&ct[w.file], 1);
+      }, st, 128);
+    }
+    sync(st);
+    dfree(ec);
+    dfree(eb);
+    level++;
+  }
+  W.levels = level;
+  dfree(front);
+  W.n_inst = prev_n;
+  W.n_edges = edges_used;
+  // ---- main instance per walk: the last created (max creation key)
+  {
+    const Inst* in = W.inst; unsigned long long* mk = W.main_key; u32* mi = W.main_inst;
+    u32 n = W.n_inst;
+    par_for(n, [=] EXS_D (i64 i) {
+      if (in[i].flags & IF_MAIN) {
+#ifndef EXS_EMU
+        atomicMax(&mk[in[i].walk], in[i].ckey + 1);
+#else
+        if (in[i].ckey + 1 > mk[in[i].walk]) mk[in[i].walk] = in[i].ckey + 1;
+#endif
+      }
+    }, st);
+    par_for(n, [=] EXS_HD (i64 i) {
+      if ((in[i].flags & IF_MAIN) && mk[in[i].walk] == in[i].ckey + 1) mi[in[i].walk] = (u32)i;
+    }, st);
+  }
+  // ---- reachability (spacecheck.py:617-632)
+  W.visited = dalloc<u8>((u64)W.n_inst + 8);
+  dzero(W.visited, (u64)W.n_inst + 8, st);
+  {
+    u32 n = W.n_inst;
+    u32* q0 = dalloc<u32>((u64)n + 1);
+    u32* q1 = dalloc<u32>((u64)n + 1);
+    u32* qn = dalloc<u32>(2);
+    dzero(qn, 8, st);
+    u8* vis = W.visited; const u32* mi = W.main_inst; const u32* sd = W.seeds; const Inst* in = W.inst;
+    std::vector<u32> cnt(8);
+    d2h(cnt.data(), W.counters, 32, st);
+    sync(st);
+    u32 nseeds = cnt[2];
+    // host walks: main; device walks: launch seeds
+    par_for(NW, [=] EXS_D (i64 w) {
+      if (w & 1) return;
+      u32 m = mi[w];
+      if (m == NONE) return;
+      vis[m] = 1;  // one main per walk
+      u32 k = at_add(&qn[0], 1);
+      q0[k] = m;
+    }, st);
+    par_for(nseeds, [=] EXS_D (i64 k) {
+      u32 w = sd[2 * k], t = sd[2 * k + 1];
+      if (!(w & 1)) return;
+#ifndef EXS_EMU
+      u32* wp = (u32*)(vis + (t & ~3u));
+      u32 sh = (t & 3u) * 8;
+      u32 old = atomicOr(wp, 1u << sh);
+      if ((old >> sh) & 0xFF) return;
+#else
+      if (vis[t]) return;
+      vis[t] = 1;
+#endif
+      u32 j = at_add(&qn[0], 1);
+      q0[j] = t;
+    }, st);
+    u32 nq = get1(qn, st);
+    const u32* ed = W.edges;
+    while (nq) {
+      dzero(qn + 1, 4, st);
+      const u32* qa = q0; u32* qb = q1;
+      par_for(nq, [=] EXS_D (i64 j) {
+        const Inst& I = in[qa[j]];
+        u8 native = (u8)(I.walk & 1);
+        for (u32 e = 0; e < I.ecnt; e++) {
+          u32 c = ed[I.ebase + e];
+          if (in[c].side != native) continue;
+#ifndef EXS_EMU
+          u32* wp = (u32*)(vis + (c & ~3u));
+          u32 sh = (c & 3u) * 8;
+          u32 old = atomicOr(wp, 1u << sh);
+          if ((old >> sh) & 0xFF) continue;
+#else
+          if (vis[c]) continue;
+          vis[c] = 1;
+#endif
+          u32 k = at_add(&qn[1], 1);
+          qb[k] = c;
+        }
+      }, st);
+      nq = get1(qn + 1, st);
+      std::swap(q0, q1);
+    }
+    sync(st);
+    dfree(q0); dfree(q1); dfree(qn);
+  }
+  // ---- pending verdicts (spacecheck.py:634-655)
+  {
+    std::vector<u32> cnt(8);
+    d2h(cnt.data(), W.counters, 32, st);
+    sync(st);
+    const Pending* pd = W.pend; const Inst* in = W.inst; const u8* vis = W.visited;
+    const FnRec* fr = S.fns; const Node* nd = P.nodes; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
+    WalkBufs Bc = B;
+    par_for(cnt[1], [=] EXS_HD (i64 j) {
+      const Pending& p = pd[j];
+      const Inst& I = in[p.caller];
+      u8 native = (u8)(p.walk & 1);
+      if (I.side != native) return;
+      u32 file = vf[fr[I.fn].view];
+      u8 c = cfgs[file];
+      u8 mode = c & CFG_MODE_MASK;
+      u16 code = verdict(I.side, p.callee, true, mode, vis[p.caller] != 0);
+      if (!code) return;
+      if (mode == MODE_FIDELITY && native == 0 && !hard_code(code)) return;
+      bool warn = code == C_W1101 || code == C_W1102 || code == C_W1502;
+      u8 sup = warn && (nd[fr[I.fn].node].n & FF_PRAGMA) ? 1 : 0;
+      emit_diag(Bc, mkdiag(file, p.line, p.col, code, M_W_STRAY, p.callee, I.side, 1, 0, sup));
+    }, st);
+  }
+  sync(st);
+  dfree(dtab);
+  return true;
+}
+
+}  // namespace exs

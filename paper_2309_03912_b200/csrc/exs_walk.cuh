@@ -1,0 +1,652 @@
+// exs_walk.cuh -- K6: walk of one instance's body (reference: spacecheck.py
+// _Walk._walk_instance .. _report_stray, lines 312-613).  One thread walks one
+// frontier instance of a level-synchronous BFS; the FIFO order of the
+// reference is reproduced by creation keys (level, parent rank, local index)
+// kept with atomicMin, so "first creator" data (the E1201 location) matches.
+#pragma once
+#include "exs_common.cuh"
+#include "exs_sema.cuh"
+
+namespace exs {
+
+// 128-bit instance key: a = sig_rep<<32 | tcode(type binding),
+//                       b = 1<<63 | tcode(owner)<<32 | walk<<3 | hdc<<1 | side
+struct alignas(16) IKey {
+  u64 a, b;
+};
+
+struct Inst {
+  u64 ka, kb;
+  unsigned long long ckey;  // min creation key (level<<52 | parent rank<<24 | local)
+  u32 fn, orec, walk, at;   // creating decl, owner struct, walk, at_loc token
+  u32 ebase, ecnt;          // legal edges (callee instance ids)
+  Val tb, hb, ot;           // type binding, hdc binding, owner type
+  u8 side, spaces, level, flags;
+  u32 pad;
+};
+enum { IF_BODY = 1, IF_MAIN = 2 };
+
+struct Pending {
+  u32 walk, caller, line, col;
+  u8 callee, pad[3];
+};
+struct CreateLog {
+  unsigned long long ckey;
+  u32 inst, at, fn, pad;
+};
+
+struct WalkBufs {
+  // instance table
+  IKey* slots;
+  u32* sid;
+  u32 mask;
+  Inst* inst;
+  u32* n_inst;
+  u32 cap_inst;
+  // outputs
+  u32* edges;
+  Pending* pend;
+  u32* n_pend;
+  u32 cap_pend;
+  u32* seeds;   // (walk, inst) pairs
+  u32* n_seeds;
+  u32 cap_seeds;
+  CreateLog* log;
+  u32* n_log;
+  u32 cap_log;
+  u32* main_inst;               // per walk: instance of main with the max creation key
+  unsigned long long* main_key; // per walk
+  // diagnostics
+  Diag* diags;
+  u32* n_diags;
+  u32 cap_diags;
+  u64* dset;      // dedup set of diag hashes
+  u32 dmask;
+  u32* overflow;  // bit0 instances, bit1 diags, bit2 log/pend/seeds
+  u32* contract;  // units that exceeded a recursion bound (per file flag array)
+};
+
+EXS_HD inline u32 tcode(const Val& t) {
+  if (t.k != V_TYPE) return 0;
+  if (t.rec == NONE) return t.bt;  // BT_VOID/INT/BOOL are 1..3
+  return 4u + t.rec * 4u + t.targ;
+}
+
+// ---------------------------------------------------------------------------
+// diagnostics emission with on-the-fly dedup (diagnostics.py:116-121)
+
+EXS_HD inline u64 diag_hash(const Diag& d) {
+  u64 h = hcombine(d.file, ((u64)d.line << 32) | d.col);
+  h = hcombine(h, ((u64)d.code << 16) | d.msg);
+  h = hcombine(h, d.a0);
+  h = hcombine(h, d.a1);
+  h = hcombine(h, d.a2);
+  h = hcombine(h, d.a3);
+  return nz(h);
+}
+
+EXS_HD inline bool set_insert(u64* set, u32 mask, u64 k) {
+  u32 h = (u32)mix64(k) & mask;
+  for (u32 probes = 0; probes <= mask; probes++) {
+    unsigned long long prev = at_cas64((unsigned long long*)&set[h], 0ull, (unsigned long long)k);
+    if (prev == 0ull) return true;
+    if (prev == k) return false;
+    h = (h + 1) & mask;
+  }
+  return false;
+}
+
+EXS_HD inline void emit_diag(const WalkBufs& B, Diag d) {
+  u64 h = diag_hash(d);
+  if (!set_insert(B.dset, B.dmask, h)) return;
+  u32 i = at_add(B.n_diags, 1);
+  if (i < B.cap_diags) B.diags[i] = d;
+  else at_or(B.overflow, 2);
+}
+EXS_HD inline Diag mkdiag(u32 file, u32 line, u32 col, u16 code, u16 msg, u64 a0 = 0, u64 a1 = 0,
+                          u64 a2 = 0, u32 a3 = 0, u8 sup = 0) {
+  Diag d;
+  d.file = file; d.line = line; d.col = col; d.code = code; d.msg = msg;
+  d.a0 = a0; d.a1 = a1; d.a2 = a2; d.a3 = a3; d.suppressed = sup; d.pad0 = d.pad1 = d.pad2 = 0;
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// instance table
+
+EXS_HD inline bool ikey_cas(IKey* slot, const IKey& k, IKey& old) {
+#if EXS_DEV_PATH
+  IKey empty; empty.a = 0; empty.b = 0;
+  old = atomicCAS(slot, empty, k);
+#else
+  old = *slot;
+  if (old.a == 0 && old.b == 0) *slot = k;
+#endif
+  return old.a == 0 && old.b == 0;
+}
+EXS_HD inline u32 inst_lookup_or_insert(const WalkBufs& B, const IKey& k, bool& inserted) {
+  u32 h = (u32)mix64(k.a ^ mix64(k.b)) & B.mask;
+  inserted = false;
+  for (u32 probes = 0; probes <= B.mask; probes++) {
+    IKey old;
+    if (ikey_cas(&B.slots[h], k, old)) {
+      u32 id = at_add(B.n_inst, 1u);
+      if (id >= B.cap_inst) { at_or(B.overflow, 1u); id = NONE; }
+      inserted = true;
+      return id;  // caller initialises the record, then publishes sid[h]
+    }
+    if (old.a == k.a && old.b == k.b) {
+      u32 id;
+      while ((id = ld_volatile(&B.sid[h])) == NONE) {
+        if (ld_volatile(B.overflow) & 1u) return NONE;
+      }
+      return id;
+    }
+    h = (h + 1) & B.mask;
+  }
+  at_or(B.overflow, 1u);
+  return NONE;
+}
+EXS_HD inline void inst_publish(const WalkBufs& B, const IKey& k, u32 id) {
+  u32 h = (u32)mix64(k.a ^ mix64(k.b)) & B.mask;
+  while (!(B.slots[h].a == k.a && B.slots[h].b == k.b)) h = (h + 1) & B.mask;
+  fence_gpu();  // the record is visible before its id is published
+  at_cas(&B.sid[h], NONE, id);
+}
+
+// ---------------------------------------------------------------------------
+
+// verdict table (spacecheck.py:86-132) for direct calls; callee 1=H 2=D
+// returns a code or 0 (legal)
+EXS_HD inline u16 verdict(u8 side, u8 callee, bool from_hd, u8 mode, bool reachable) {
+  if (callee == 3 || callee == (1u << side)) return 0;
+  bool host_only = callee == 1;
+  if (!from_hd) {
+    if (mode == MODE_P2) return C_E1501;
+    return side == 0 ? C_E1001 : C_E1002;
+  }
+  if (mode == MODE_FIDELITY && !host_only) return 0;
+  if (mode == MODE_SOUND && reachable) return host_only ? C_E1101 : C_E1102;
+  if (mode == MODE_P2) return reachable ? C_E1501 : C_W1502;
+  return host_only ? C_W1101 : C_W1102;
+}
+EXS_HD inline bool hard_code(u16 c) {
+  return c == C_E0001 || c == C_E0002 || c == C_E0101 || c == C_E0102 || c == C_E0103 ||
+         c == C_E0104 || c == C_E1301 || c == C_E1302;
+}
+
+#define MAX_LOCALS 64
+#define MAX_WALK_DEPTH 160
+#define MAX_ARGS 32
+
+struct Walker {
+  Sema S;
+  const WalkBufs* B;
+  const Tables* T;
+  u32 file, walk, inst_id;
+  u8 native, side, spaces;   // side 0 host 1 device; spaces bits 1 H 2 D 4 G
+  u8 clevel;                 // level of the instances this walker creates
+  u32 fn;                    // decl of the instance
+  bool pragma, from_hd, fidelity_host;
+  u64 parent_rank;           // dense rank of this instance within its level
+  u32 local;                 // _instantiate call counter (creation order)
+  u32 ebase, ecnt;
+  Env env;                   // owner bindings + bindings
+  Env obinds_self;           // owner bindings of this instance
+  u32 orec_self;
+  // locals (scoped dict)
+  u32 nloc;
+  u64 lname[MAX_LOCALS];
+  Val lval[MAX_LOCALS];
+  int wdepth;
+  bool contract;
+
+  EXS_HD const Node& N(u32 id) const { return T->nodes[id]; }
+  EXS_HD const Tok& K(u32 t) const { return T->toks[t]; }
+  EXS_HD u64 span(u32 t) const { return S.span(t); }
+
+  EXS_HD void emit(u16 code, u32 line, u32 col, u16 msg, u64 a0 = 0, u64 a1 = 0, u64 a2 = 0,
+                   u32 a3 = 0) {
+    if (fidelity_host && !hard_code(code)) return;
+    emit_diag(*B, mkdiag(file, line, col, code, msg, a0, a1, a2, a3));
+  }
+  EXS_HD void emit_tok(u16 code, u32 tok, u16 msg, u64 a0 = 0, u64 a1 = 0, u64 a2 = 0, u32 a3 = 0) {
+    emit(code, K(tok).line, K(tok).col, msg, a0, a1, a2, a3);
+  }
+  EXS_HD void emit_err() {  // a SemaError from the evaluator
+    emit(S.err.code, S.err.line, S.err.col, S.err.msg, S.err.a0, S.err.a1, S.err.a2);
+  }
+
+  // display-name arguments of a decl: (name span, owner span or 0)
+  EXS_HD u64 owner_span(u32 fi) const {
+    const FnRec& fr = T->fns[fi];
+    return (fr.flags & FR_OWNER) ? span(N(T->recs[fr.rec].node).tok) : 0;
+  }
+
+  // ------------------------------------------------------------- locals
+  EXS_HD bool local_get(u64 name, Val& v) const {
+    for (int i = (int)nloc - 1; i >= 0; i--)
+      if (lname[i] == name) { v = lval[i]; return true; }
+    return false;
+  }
+  EXS_HD void local_set(u64 name, const Val& v) {
+    if (nloc < MAX_LOCALS) { lname[nloc] = name; lval[nloc] = v; nloc++; }
+    else contract = true;
+  }
+
+  // _resolve_type_soft (spacecheck.py:363-370)
+  EXS_HD Val soft_type(u32 tr, u32 loc_tok) {
+    Val t;
+    S.depth = 0;
+    u8 st = S.type_of(tr, env, t);
+    if (S.contract) { contract = true; return vnone(); }
+    if (st == ST_OK) return t;
+    if (st == ST_SEMA) emit_err();
+    else emit_tok(C_E0101, loc_tok, M_W_NOT_TYPE, span(N(tr).tok));
+    return vnone();
+  }
+
+  // ------------------------------------------------------------- instantiate
+  // _instantiate (spacecheck.py:312-351); returns instance id or NONE
+  EXS_HD u32 instantiate(u32 fi, const Val& tb, const Val& hb, u8 want_side, u32 orec,
+                         const Env& obinds, const Val& ot, u32 at_tok) {
+    u32 my_local = local++;
+    // merged = owner bindings + bindings
+    Env merged = obinds;
+    merged.nbase = merged.n;
+    const Node& fnn = N(T->fns[fi].node);
+    add_binds(fnn, tb, hb, merged);
+    merged.nbase = merged.n;
+    u8 sp;
+    S.depth = 0;
+    u8 st = S.spaces(fi, merged, want_side, at_tok, orec, sp);
+    if (S.contract) { contract = true; return NONE; }
+    if (st == ST_SEMA) { emit_err(); return NONE; }
+    if (st == ST_SUBST) { emit_tok(C_E0001, at_tok, M_W_PRED_CONST); return NONE; }
+    const FnRec& fr = T->fns[fi];
+    IKey k;
+    k.a = ((u64)fr.sig_rep << 32) | tcode(tb);
+    k.b = (1ull << 63) | ((u64)tcode(ot) << 32) | ((u64)walk << 3) |
+          ((u64)(hb.k == V_HDC ? hb.x : 0) << 1) | want_side;
+    bool inserted;
+    u32 id = inst_lookup_or_insert(*B, k, inserted);
+    if (id == NONE) return NONE;
+    unsigned long long ck = ((unsigned long long)clevel << 52) |
+                            ((unsigned long long)parent_rank << 24) | (my_local & 0xFFFFFFu);
+    Inst& I = B->inst[id];
+    if (inserted) {
+      I.ka = k.a; I.kb = k.b;
+      I.ckey = ck; I.fn = fi; I.orec = orec; I.walk = walk; I.at = at_tok;
+      I.ebase = 0; I.ecnt = 0;
+      I.tb = tb; I.hb = hb; I.ot = ot;
+      I.side = want_side; I.spaces = sp; I.level = clevel;
+      I.flags = (fnn.n & FF_BODY) ? IF_BODY : 0;
+      if (K(fnn.tok).id == W_MAIN && !(fr.flags & FR_OWNER)) I.flags |= IF_MAIN;
+      inst_publish(*B, k, id);
+    }
+    if (I.level == clevel) {
+      // a creator in this level: log it; the minimum creation key wins
+      if (!inserted) at_min64(&I.ckey, ck);
+      u32 li = at_add(B->n_log, 1);
+      if (li < B->cap_log) {
+        CreateLog& L = B->log[li];
+        L.ckey = ck; L.inst = id; L.at = at_tok; L.fn = fi;
+      } else {
+        at_or(B->overflow, 4);
+      }
+    }
+    return id;
+  }
+
+  EXS_HD void add_binds(const Node& fnn, const Val& tb, const Val& hb, Env& e) const {
+    for (u32 tp = fnn.c0; tp != NONE; tp = N(tp).next) {
+      const Val& v = N(tp).sub == 0 ? tb : hb;
+      if (v.k != V_NONE) e.add(K(N(tp).tok).hv, v);
+    }
+  }
+
+  // ------------------------------------------------------------- dispatch
+  // _report_stray (spacecheck.py:604-613); callee 1=H 2=D
+  EXS_HD void stray(u8 callee, u32 loc_tok) {
+    if (from_hd) {
+      u32 i = at_add(B->n_pend, 1);
+      if (i < B->cap_pend) {
+        Pending& p = B->pend[i];
+        p.walk = walk; p.caller = inst_id; p.line = K(loc_tok).line; p.col = K(loc_tok).col;
+        p.callee = callee;
+      } else {
+        at_or(B->overflow, 4);
+      }
+      return;
+    }
+    u16 code = verdict(side, callee, false, S.mode, true);
+    emit_tok(code, loc_tok, M_W_STRAY, callee, side, 0);
+  }
+
+  // _dispatch (spacecheck.py:554-596)
+  EXS_HD void dispatch(u32 fi, const Val& tb, const Val& hb, u32 loc_tok, u32 orec,
+                       const Env& obinds, const Val& ot) {
+    Env merged = obinds;
+    merged.nbase = merged.n;
+    const Node& fnn = N(T->fns[fi].node);
+    add_binds(fnn, tb, hb, merged);
+    merged.nbase = merged.n;
+    u8 sp;
+    S.depth = 0;
+    u8 st = S.spaces(fi, merged, side, loc_tok, orec, sp);
+    if (S.contract) { contract = true; return; }
+    if (st == ST_SEMA) { emit_err(); return; }
+    if (st == ST_SUBST) { emit_tok(C_E0001, loc_tok, M_W_PRED_CONST); return; }
+    if (sp == 4) { emit_tok(C_E1004, loc_tok, M_W_GLOBAL_CALL); return; }
+    bool relaxed_ok = S.relaxed && (fnn.n & FF_CX);
+    bool legal = relaxed_ok || (sp & (1u << side));
+    u8 want = legal ? side : ((sp & 1) ? 0 : 1);
+    u32 callee = instantiate(fi, tb, hb, want, orec, obinds, ot, loc_tok);
+    if (legal && callee != NONE) {
+      B->edges[ebase + ecnt] = callee;
+      ecnt++;
+    }
+    if (!legal) stray(sp == 1 ? 1 : 2, loc_tok);
+    bool tmpl = fnn.c0 != NONE;
+    if ((S.mode == MODE_CLASSIC || S.mode == MODE_FIDELITY || S.mode == MODE_P1) && sp == 3 &&
+        (tmpl || ot.k != V_NONE))
+      instantiate(fi, tb, hb, native, orec, obinds, ot, loc_tok);
+  }
+
+  // _select + overload resolution (sema.py:491-542); cand list given as
+  // (free: fcand run) or (member: struct rec).  Returns false on failure.
+  EXS_HD bool select(bool member, u32 first, u32 count, u32 rec, u64 mname, u32 targs,
+                     const Val* argtys, u32 nargs, u32 loc_tok, u8 ctx_side, const Env& obinds,
+                     u64 name_a0, u64 name_a1, u32& out_fi, Val& out_tb, Val& out_hb) {
+    u32 nviable = 0;
+    u32 vfi[8];
+    Val vtb[8], vhb[8];
+    u32 i = 0;
+    u32 m = member ? N(T->recs[rec].node).c1 : NONE;
+    while (true) {
+      u32 fi;
+      if (member) {
+        // member functions with this name, in member order (dups were removed)
+        while (m != NONE) {
+          const Node& mn = N(m);
+          if (mn.kind == N_FN && K(mn.tok).hv == mname) {
+            u32 fx = N(m + 1).tok;  // FNX.tok holds the decl record index
+            if (!(T->fns[fx].flags & FR_DUP)) break;
+          }
+          m = mn.next;
+        }
+        if (m == NONE) break;
+        fi = N(m + 1).tok;
+        m = N(m).next;
+      } else {
+        if (i >= count) break;
+        fi = T->fcand[first + i];
+        i++;
+      }
+      Sema::Binds b;
+      S.depth = 0;
+      u8 st = S.try_cand(fi, targs, argtys, nargs, env, member ? rec : NONE, obinds, b);
+      if (S.contract) { contract = true; return false; }
+      if (st == ST_SEMA) { emit_err(); return false; }
+      if (st == ST_SUBST) continue;
+      if (nviable < 8) {
+        vfi[nviable] = fi;
+        // split bindings by tparam kind
+        Val tb = vnone(), hb = vnone();
+        const Node& fnn = N(T->fns[fi].node);
+        for (u32 tp = fnn.c0; tp != NONE; tp = N(tp).next) {
+          Val v;
+          if (b.get(K(N(tp).tok).hv, v)) {
+            if (N(tp).sub == 0) tb = v; else hb = v;
+          }
+        }
+        vtb[nviable] = tb; vhb[nviable] = hb;
+      }
+      nviable++;
+    }
+    if (S.mode == MODE_P2 && nviable > 1 && nviable <= 8) {
+      u32 nc = 0;
+      for (u32 j = 0; j < nviable; j++)
+        if (S.compatible(vfi[j], ctx_side, member ? rec : NONE)) {
+          vfi[nc] = vfi[j]; vtb[nc] = vtb[j]; vhb[nc] = vhb[j]; nc++;
+        }
+      if (nc) nviable = nc;
+    }
+    if (nviable == 0) { emit_tok(C_E1301, loc_tok, M_S_NO_VIABLE, name_a0, name_a1); return false; }
+    if (nviable > 1) { emit_tok(C_E1302, loc_tok, M_S_AMBIGUOUS, name_a0, name_a1, nviable); return false; }
+    out_fi = vfi[0]; out_tb = vtb[0]; out_hb = vhb[0];
+    return true;
+  }
+
+  // ------------------------------------------------------------- expressions
+  EXS_HD u32 count_list(u32 l) const {
+    u32 c = 0;
+    for (; l != NONE; l = N(l).next) c++;
+    return c;
+  }
+
+  // walk args (post-order) into types
+  EXS_HD u32 walk_args(u32 args, Val* tys) {
+    u32 n = 0;
+    for (u32 a = args; a != NONE; a = N(a).next) {
+      Val t = expr(a);
+      if (n < MAX_ARGS) tys[n] = t;
+      else contract = true;
+      n++;
+    }
+    return n;
+  }
+
+  EXS_HD Val expr(u32 e) {
+    if (++wdepth > MAX_WALK_DEPTH) { contract = true; wdepth--; return vnone(); }
+    Val r = expr_(e);
+    wdepth--;
+    return r;
+  }
+
+  EXS_HD Val expr_(u32 e) {
+    const Node& n = N(e);
+    switch (n.kind) {
+      case N_INT: { Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int"); return t; }
+      case N_BOOL:
+      case N_ARCH: { Val t = vnone(); t.k = V_TYPE; t.bt = BT_BOOL; t.x = word_hash("bool"); return t; }
+      case N_STR:
+      case N_HDCV: return vnone();
+      case N_NAME: {
+        u64 nm = K(n.tok).hv;
+        Val v;
+        if (local_get(nm, v)) return v;
+        for (int i = 0; i < env.n; i++)
+          if (env.names[i] == nm) return vnone();
+        emit_tok(C_E0101, n.tok, M_S_UNDEF_NAME, span(n.tok));
+        return vnone();
+      }
+      case N_TMP: return soft_type(n.c0, n.tok);
+      case N_TRAIT: {
+        Val t;
+        S.depth = 0;
+        u8 st = S.type_of(n.c0, env, t);
+        if (st == ST_OK) {
+          Val h;
+          st = S.trait(t, S.fund, h);
+        }
+        if (S.contract) { contract = true; return vnone(); }
+        if (st == ST_SEMA) emit_err();
+        return vnone();
+      }
+      case N_MCONST: {
+        Val v;
+        S.depth = 0;
+        u8 st = S.eval(e, env, S.fund, v);
+        if (S.contract) { contract = true; return vnone(); }
+        if (st == ST_SEMA) emit_err();
+        else if (st == ST_SUBST)
+          emit_tok(C_E0101, N(n.c0).tok, M_W_SUBST, S.err.a0, S.err.a1, S.err.a2, S.err.msg);
+        return vnone();
+      }
+      case N_NOT: {
+        expr(n.c0);
+        Val t = vnone(); t.k = V_TYPE; t.bt = BT_BOOL; t.x = word_hash("bool");
+        return t;
+      }
+      case N_BIN: {
+        expr(n.c0);
+        expr(n.c1);
+        Val t = vnone(); t.k = V_TYPE; t.bt = BT_BOOL; t.x = word_hash("bool");
+        return t;
+      }
+      case N_CALL: return free_call(e);
+      case N_MCALL: {
+        u32 recv = n.c0;
+        Val rt = expr(recv);
+        u8 rk = N(recv).kind;
+        if (rt.k == V_NONE && rk != N_TMP && rk != N_NAME)
+          emit_tok(C_E0001, S.loc_tok(recv), M_W_RECEIVER);
+        Val tys[MAX_ARGS];
+        u32 na = walk_args(n.c2, tys);
+        if (rt.k != V_NONE) member_dispatch(rt, n.tok, n.c1, tys, na, S.loc_tok(e));
+        return vnone();
+      }
+      case N_SCALL: {
+        Val tys[MAX_ARGS];
+        u32 na = walk_args(n.c2, tys);
+        Val t = soft_type(n.c0, N(n.c0).tok);
+        if (t.k != V_NONE) member_dispatch(t, n.tok, n.c1, tys, na, N(n.c0).tok);
+        return vnone();
+      }
+      default:
+        return vnone();
+    }
+  }
+
+  EXS_HD Val free_call(u32 e) {
+    const Node& n = N(e);
+    Val tys[MAX_ARGS];
+    u32 na = walk_args(n.c2, tys);
+    bool is_std = n.sub == CALL_STD;
+    u64 nm = is_std ? hcombine(word_hash("std::"), K(n.c0).hv) : K(n.tok).hv;
+    u32 run = is_std ? NONE : T->fmap.find(vkey(S.view, nm));
+    if (run == NONE) {
+      // builtin_spaces (sema.py:99-102)
+      u8 w = is_std ? (K(n.c0).id == W_ABORT ? (u8)0xFE : (u8)0) : K(n.tok).id;
+      u8 sp = 0;
+      if (w == W_PRINTF || w == W_RELEASE_ASSERT) sp = 3;
+      else if (w == W_TRAP) sp = S.plain ? 0 : 2;
+      else if (w == W_ABORT || w == 0xFE) sp = 1;
+      else if (w == W_CUDASYNC) sp = S.plain ? 0 : 1;
+      if (sp) {
+        if (!(sp & (1u << side))) stray(sp == 1 ? 1 : 2, n.tok);
+        if (w == W_CUDASYNC) { Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int"); return t; }
+      }
+      return vnone();
+    }
+    u32 fi; Val tb, hb;
+    Env none; none.clear();
+    if (select(false, run, T->fcand_cnt[run], NONE, 0, n.c1, tys, na, n.tok, side, none,
+               span(n.tok), 0, fi, tb, hb))
+      dispatch(fi, tb, hb, n.tok, NONE, none, vnone());
+    return vnone();
+  }
+
+  // _member_dispatch (spacecheck.py:529-550)
+  EXS_HD void member_dispatch(const Val& rt, u32 name_tok, u32 targs, const Val* tys, u32 na,
+                              u32 loc_tok) {
+    u64 mname = K(name_tok).hv;
+    u64 tname = S.type_name_arg(rt);
+    u64 targ_arg = rt.targ;
+    bool any = false;
+    if (rt.rec != NONE) {
+      for (u32 m = N(T->recs[rt.rec].node).c1; m != NONE; m = N(m).next) {
+        const Node& mn = N(m);
+        if (mn.kind == N_FN && K(mn.tok).hv == mname && !(T->fns[N(m + 1).tok].flags & FR_DUP)) { any = true; break; }
+      }
+    }
+    if (!any) {
+      emit_tok(C_E0101, loc_tok, M_W_NO_MEMBER, tname, span(name_tok), targ_arg);
+      return;
+    }
+    Env ob;
+    S.struct_env(rt.rec, rt, ob);
+    u32 fi; Val tb, hb;
+    // name for messages: "{type display}::{name}"
+    if (select(true, 0, 0, rt.rec, mname, targs, tys, na, loc_tok, side, ob,
+               span(name_tok), tname | 0, fi, tb, hb))
+      dispatch(fi, tb, hb, loc_tok, rt.rec, ob, rt);
+  }
+
+  // ------------------------------------------------------------- statements
+  EXS_HD void stmts(u32 s) {
+    for (; s != NONE; s = N(s).next) {
+      if (contract) return;
+      const Node& n = N(s);
+      switch (n.kind) {
+        case N_SEXPR: expr(n.c0); break;
+        case N_SRET: if (n.c0 != NONE) expr(n.c0); break;
+        case N_SVAR: {
+          Val t = soft_type(n.c0, N(n.c0).tok);
+          local_set(K(n.tok).hv, t);
+          break;
+        }
+        case N_SIF: {
+          expr(n.c0);
+          u32 mark = nloc;
+          stmts(n.c1);
+          nloc = mark;
+          if (n.sub) { stmts(n.c2); nloc = mark; }
+          break;
+        }
+        case N_SFOR: {
+          expr(n.c0);
+          expr(n.c1);
+          u32 mark = nloc;
+          Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int");
+          local_set(K(n.tok).hv, t);
+          stmts(n.c2);
+          nloc = mark;
+          break;
+        }
+        case N_SLAUNCH: launch(s); break;
+        default: break;
+      }
+    }
+  }
+
+  // _walk_launch (spacecheck.py:395-415)
+  EXS_HD void launch(u32 s) {
+    const Node& n = N(s);
+    u32 grid = n.c1;
+    expr(grid);
+    expr(N(grid).next);
+    Val tys[MAX_ARGS];
+    u32 na = walk_args(n.c2, tys);
+    if (side == 1) emit_tok(C_E1003, n.tok, M_W_LAUNCH_DEVICE);
+    u32 run = T->fmap.find(vkey(S.view, K(n.tok).hv));
+    if (run == NONE) return;
+    u32 fi; Val tb, hb;
+    Env none; none.clear();
+    if (!select(false, run, T->fcand_cnt[run], NONE, 0, n.c0, tys, na, n.tok, 1, none,
+                span(n.tok), 0, fi, tb, hb))
+      return;
+    if (!(N(T->fns[fi].node).n & FF_G)) { emit_tok(C_E1004, n.tok, M_W_LAUNCH_NONGLOBAL); return; }
+    u32 tgt = instantiate(fi, tb, hb, 1, NONE, none, vnone(), n.tok);
+    if (tgt != NONE && side == 0) {
+      u32 i = at_add(B->n_seeds, 1);
+      if (i < B->cap_seeds) { B->seeds[2 * i] = walk; B->seeds[2 * i + 1] = tgt; }
+      else at_or(B->overflow, 4);
+    }
+  }
+
+  // _walk_instance (spacecheck.py:355-361)
+  EXS_HD void run_body() {
+    const Node& fnn = N(T->fns[fn].node);
+    nloc = 0;
+    wdepth = 0;
+    for (u32 p = fnn.c1; p != NONE; p = N(p).next) {
+      Val t = soft_type(N(p).c0, N(p).tok);
+      local_set(K(N(p).tok).hv, t);
+    }
+    stmts(fnn.c2);
+  }
+};
+
+}  // namespace exs

@@ -1,0 +1,372 @@
+"""Drop-in mirror of the reference ``exspace`` analysis API, GPU-backed.
+
+Same names, argument meaning, result schema and ordering as
+``exspace.spacecheck.analyze``/``check_unit`` (spacecheck.py:687-750) and the
+types they return (diagnostics.py:8-121, preprocess.py:31-78, sema.py:12-62).
+Every unit is analysed by the sm_100a pipeline behind the C ABI
+(include/exspace_b200.h); the host only packs inputs and renders messages.
+``analyze_corpus`` is the batch entry point (many units per GPU launch).
+"""
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Iterable, Optional
+
+import numpy as np
+
+from . import _native
+from .messages import CODES, Renderer, stray_text
+
+
+# ---------------------------------------------------------------------------
+# result schema (diagnostics.py)
+
+class Severity(Enum):
+    ERROR = "error"
+    WARNING = "warning"
+    NOTE = "note"
+
+
+CODE_REGISTRY: dict = {
+    "E0001": (Severity.ERROR, "parse error"),
+    "E0002": (Severity.ERROR, "preprocessor error"),
+    "E0101": (Severity.ERROR, "undefined name"),
+    "E0102": (Severity.ERROR, "duplicate definition"),
+    "E0103": (Severity.ERROR, "hdc member is not an HDC constant"),
+    "E0104": (Severity.ERROR, "static assertion failed"),
+    "E1001": (Severity.ERROR, "host code calls a device function"),
+    "E1002": (Severity.ERROR, "device code calls a host function"),
+    "E1003": (Severity.ERROR, "kernel launch from device code"),
+    "E1004": (Severity.ERROR, "misused __global__ function"),
+    "W1101": (Severity.WARNING, "host device function calls a host-only function"),
+    "W1102": (Severity.WARNING, "host device function calls a device-only function"),
+    "E1101": (Severity.ERROR, "reachable stray call to a host-only function"),
+    "E1102": (Severity.ERROR, "reachable stray call to a device-only function"),
+    "E1201": (Severity.ERROR, "instantiation depends on the compile pass"),
+    "E1301": (Severity.ERROR, "no viable overload candidate"),
+    "E1302": (Severity.ERROR, "ambiguous call"),
+    "E1401": (Severity.ERROR, "empty execution-space set"),
+    "E1501": (Severity.ERROR, "stray call"),
+    "W1502": (Severity.WARNING, "host device function calls a one-sided function"),
+    "N0001": (Severity.NOTE, "kernel launch skipped after device error"),
+    # the analyser's own marker for inputs beyond its recursion/nesting bounds,
+    # where the reference raises RecursionError
+    "X9999": (Severity.ERROR, "input outside the analyser contract"),
+}
+
+STRAY_CODES = frozenset({"E1001", "E1002", "W1101", "W1102", "E1101", "E1102", "E1501", "W1502"})
+
+
+@dataclass(frozen=True, order=True)
+class SrcLoc:
+    file: str
+    line: int
+    col: int
+
+    def __post_init__(self):
+        if self.line < 1 or self.col < 1:
+            raise ValueError(f"source positions are 1-based: {self.line}:{self.col}")
+
+    def __str__(self):
+        return f"{self.file}:{self.line}:{self.col}"
+
+
+@dataclass
+class Diagnostic:
+    code: str
+    severity: Severity
+    loc: SrcLoc
+    message: str
+    suppressed: bool = field(default=False)
+
+    @classmethod
+    def make(cls, code: str, loc: SrcLoc, message: str) -> "Diagnostic":
+        return cls(code, CODE_REGISTRY[code][0], loc, message)
+
+    @property
+    def is_error(self) -> bool:
+        return self.severity is Severity.ERROR
+
+    def sort_key(self):
+        return (self.loc.file, self.loc.line, self.loc.col, self.code, self.message)
+
+    def dedup_key(self):
+        return (self.loc, self.code, self.message)
+
+
+_COLORS = {Severity.ERROR: "\x1b[31;1m", Severity.WARNING: "\x1b[35;1m", Severity.NOTE: "\x1b[36m"}
+
+
+def format_diagnostic(d: Diagnostic, style: str = "machine", source: Optional[str] = None,
+                      color: bool = False) -> Optional[str]:
+    """diagnostics.py:88-113."""
+    if d.suppressed:
+        return None
+    word = d.severity.value
+    if color:
+        word = f"{_COLORS[d.severity]}{word}\x1b[0m"
+    line = f"{d.loc.file}:{d.loc.line}:{d.loc.col}: {word}[{d.code}]: {d.message}"
+    if style == "machine" or source is None:
+        return line
+    lines = source.splitlines()
+    if 1 <= d.loc.line <= len(lines):
+        return f"{line}\n{lines[d.loc.line - 1]}\n{' ' * (d.loc.col - 1)}^"
+    return line
+
+
+def finish_diagnostics(diags: list) -> list:
+    """diagnostics.py:116-121."""
+    seen = {}
+    for d in diags:
+        seen.setdefault(d.dedup_key(), d)
+    return sorted(seen.values(), key=Diagnostic.sort_key)
+
+
+# ---------------------------------------------------------------------------
+# configuration (preprocess.py:46-78, spacecheck.py:53-58, sema.py:54-62)
+
+@dataclass(frozen=True)
+class CompileProfile:
+    compiler: str = "nvcc"
+    cuda_version: int = 12
+    relaxed_constexpr: bool = False
+    erase_specifiers: bool = False
+
+    def __post_init__(self):
+        if self.compiler not in ("nvcc", "plain"):
+            raise ValueError(f"unknown compiler {self.compiler!r}")
+        if self.cuda_version not in (9, 10, 11, 12):
+            raise ValueError(f"unsupported cuda version {self.cuda_version}")
+        if self.relaxed_constexpr and self.compiler != "nvcc":
+            raise ValueError("relaxed constexpr is an nvcc-only flag")
+        if self.erase_specifiers and self.compiler != "plain":
+            raise ValueError("specifier erasure applies to the plain profile only")
+
+    def pass_kinds(self) -> list:
+        return ["host"] if self.compiler == "plain" else ["host", "device"]
+
+    def trap_error_code(self) -> int:
+        return 4 if self.cuda_version == 9 else 207
+
+
+class Mode(Enum):
+    CLASSIC = "classic"
+    FIDELITY = "fidelity"
+    SOUND = "sound"
+    PROPOSAL1 = "proposal1"
+    PROPOSAL2 = "proposal2"
+
+
+_MODE_ID = {Mode.CLASSIC: 0, Mode.FIDELITY: 1, Mode.SOUND: 2, Mode.PROPOSAL1: 3, Mode.PROPOSAL2: 4}
+
+
+@dataclass(frozen=True)
+class TraitConfig:
+    fundamentals_hstdev: bool = False
+
+
+class ExecSpace(Enum):
+    Host = "host"
+    Device = "device"
+    Global = "global"
+    HostDevice = "host device"
+
+
+HOST, DEVICE = ExecSpace.Host, ExecSpace.Device
+
+
+def cfg_byte(profile: CompileProfile, mode: Mode, cfg: TraitConfig) -> int:
+    b = _MODE_ID[mode]
+    if profile.compiler == "plain":
+        b |= 8
+    if profile.relaxed_constexpr:
+        b |= 16
+    if profile.erase_specifiers:
+        b |= 32
+    if cfg.fundamentals_hstdev:
+        b |= 64
+    return b
+
+
+# ---------------------------------------------------------------------------
+# legality matrix (host-side mirror of spacecheck.py:86-132; the GPU kernels
+# carry the same table in exs_walk.cuh:verdict)
+
+@dataclass(frozen=True)
+class Verdict:
+    kind: str
+    code: Optional[str] = None
+
+    @property
+    def ok(self) -> bool:
+        return self.kind == "ok"
+
+
+def legality(caller_side, callee_space, kind: str = "direct", *, caller_from_hd: bool = False,
+             relaxed_constexpr: bool = False, callee_is_constexpr: bool = False,
+             mode: Mode = Mode.CLASSIC, mismatched_side_reachable: bool = True) -> Verdict:
+    if caller_side not in (HOST, DEVICE):
+        raise ValueError("the caller side must be host or device")
+    if kind == "launch":
+        if caller_side is DEVICE:
+            return Verdict("error", "E1003")
+        return Verdict("ok") if callee_space is ExecSpace.Global else Verdict("error", "E1004")
+    if callee_space is ExecSpace.Global:
+        return Verdict("error", "E1004")
+    if relaxed_constexpr and callee_is_constexpr:
+        return Verdict("ok")
+    if callee_space is ExecSpace.HostDevice or callee_space is caller_side:
+        return Verdict("ok")
+    host_only = callee_space is HOST
+    if not caller_from_hd:
+        if mode is Mode.PROPOSAL2:
+            return Verdict("error", "E1501")
+        return Verdict("error", "E1001" if caller_side is HOST else "E1002")
+    if mode is Mode.FIDELITY and not host_only:
+        return Verdict("ok")
+    if mode is Mode.SOUND and mismatched_side_reachable:
+        return Verdict("error", "E1101" if host_only else "E1102")
+    if mode is Mode.PROPOSAL2:
+        return Verdict("error", "E1501") if mismatched_side_reachable else Verdict("warn", "W1502")
+    return Verdict("warn", "W1101" if host_only else "W1102")
+
+
+# ---------------------------------------------------------------------------
+# results
+
+@dataclass
+class WalkSummary:
+    """What the GPU walk exposes per native side (Analysis.walks)."""
+    native: ExecSpace
+    n_instances: int
+    n_edges: int
+    n_demands: int
+
+
+@dataclass
+class Analysis:
+    path: str
+    profile: CompileProfile
+    mode: Mode
+    diagnostics: list
+    all_diagnostics: list = field(default_factory=list)
+    walks: dict = field(default_factory=dict)
+    passes: dict = field(default_factory=dict)  # pass kind -> status dict
+
+    @property
+    def has_errors(self) -> bool:
+        return any(d.is_error for d in self.diagnostics)
+
+
+# ---------------------------------------------------------------------------
+# the engine
+
+class Engine:
+    """A GPU-resident analyser; one instance per device."""
+
+    def __init__(self, device: int = 0, lib_path=None):
+        self.handle = _native.Handle(device, lib_path)
+        self.lock = threading.Lock()
+        self.last_stats: dict = {}
+
+    def run_batch(self, units: list, want_walks: bool = False):
+        """units: list of (text, path, CompileProfile, Mode, TraitConfig).
+
+        Returns a list of Analysis in input order.
+        """
+        blobs = [u[0].encode("utf-8", "surrogateescape") for u in units]
+        offsets = np.zeros(len(blobs) + 1, dtype=np.uint64)
+        if blobs:
+            offsets[1:] = np.cumsum([len(b) for b in blobs])
+        data = np.frombuffer(b"".join(blobs), dtype=np.uint8) if blobs else np.zeros(0, np.uint8)
+        cfg = np.array([cfg_byte(u[2], u[3], u[4]) for u in units], dtype=np.uint8)
+        with self.lock:
+            self.handle.set_option(1, 1 if want_walks else 0)
+            self.handle.run(data, offsets, cfg)
+            recs = self.handle.diags()
+            arena = self.handle.arena()
+            self.last_stats = self.handle.stats()
+            walks = self.handle.walk_stats(len(units)) if want_walks else None
+            status = self.handle.pass_status(len(units)) if want_walks else None
+            ren = Renderer(data.tobytes(), offsets.tolist(), arena, self.handle.describe)
+            out = self._assemble(units, recs, ren, walks, status)
+        return out
+
+    def _assemble(self, units, recs, ren: Renderer, walks, status):
+        per_file: list = [[] for _ in units]
+        for r in recs:
+            f = int(r["file"])
+            code = CODES[int(r["code"])]
+            msg = ren.message(r)
+            d = Diagnostic.make(code, SrcLoc(units[f][1], int(r["line"]), int(r["col"])), msg)
+            d.suppressed = bool(r["suppressed"])
+            per_file[f].append(d)
+        out = []
+        for f, u in enumerate(units):
+            ordered = finish_diagnostics(per_file[f])
+            a = Analysis(u[1], u[2], u[3], [d for d in ordered if not d.suppressed], ordered)
+            if walks is not None:
+                for p, side in ((0, HOST), (1, DEVICE)):
+                    w = walks[2 * f + p]
+                    if w["exists"]:
+                        a.walks[side] = WalkSummary(side, int(w["instances"]), int(w["edges"]),
+                                                    int(w["demands"]))
+                for p, kind in enumerate(u[2].pass_kinds()):
+                    s = status[2 * f + p]
+                    a.passes[kind] = {"pp_line": int(s["pp_line"]), "lex_line": int(s["lex_line"]),
+                                      "parse_failed": bool(s["parse_failed"])}
+            out.append(a)
+        return out
+
+
+_ENGINES: dict = {}
+_ENGINE_LOCK = threading.Lock()
+
+
+def get_engine(device: int = 0) -> Engine:
+    with _ENGINE_LOCK:
+        e = _ENGINES.get(device)
+        if e is None:
+            e = Engine(device)
+            _ENGINES[device] = e
+        return e
+
+
+def analyze(text: str, path: str = "<unit>", profile: CompileProfile = CompileProfile(),
+            mode: Mode = Mode.CLASSIC, cfg: TraitConfig = TraitConfig()) -> Analysis:
+    """Preprocess, parse, resolve and space-check one unit (spacecheck.py:687-739)."""
+    return get_engine().run_batch([(text, path, profile, mode, cfg)], want_walks=True)[0]
+
+
+def check_unit(text: str, path: str = "<unit>", profile: CompileProfile = CompileProfile(),
+               mode: Mode = Mode.CLASSIC, cfg: TraitConfig = TraitConfig()) -> list:
+    """The ordered diagnostic list for one unit (spacecheck.py:742-750)."""
+    return analyze(text, path, profile, mode, cfg).diagnostics
+
+
+def analyze_corpus(units: Iterable, profile: CompileProfile = CompileProfile(),
+                   mode: Mode = Mode.CLASSIC, cfg: TraitConfig = TraitConfig(),
+                   device: int = 0, want_walks: bool = False) -> list:
+    """Batch analysis.  ``units`` yields (path, text) or (path, text, profile, mode, cfg)."""
+    packed = []
+    for u in units:
+        if len(u) == 2:
+            packed.append((u[1], u[0], profile, mode, cfg))
+        else:
+            packed.append((u[1], u[0], u[2], u[3], u[4]))
+    return get_engine(device).run_batch(packed, want_walks=want_walks)
+
+
+def stray_set(analysis: Analysis) -> list:
+    """The stray-coded subset of the ordered diagnostics."""
+    return [d for d in analysis.diagnostics if d.code in STRAY_CODES]
+
+
+__all__ = [
+    "Analysis", "CODE_REGISTRY", "CompileProfile", "Diagnostic", "Engine", "ExecSpace", "Mode",
+    "Severity", "SrcLoc", "TraitConfig", "Verdict", "analyze", "analyze_corpus", "check_unit",
+    "finish_diagnostics", "format_diagnostic", "get_engine", "legality", "stray_set",
+    "stray_text",
+]

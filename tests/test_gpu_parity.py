@@ -1,0 +1,176 @@
+"""GPU parity: the sm_100a pipeline (through the C ABI) against the reference's
+golden vectors and against the CPU oracle on seeded synthetic corpora.
+
+Bar: bit-exact ordered diagnostics (code, severity, line, col, message,
+suppressed) and identical per-walk instance / legal-edge / demand counts.
+Out of contract (excluded): units the reference itself crashes on.
+"""
+import random
+
+import pytest
+
+from exs_testlib import GOLDEN_GROUPS, load_golden
+from oracle import exs_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def X():
+    from paper_2309_03912_b200 import exspace
+    return exspace
+
+
+@pytest.fixture(scope="module")
+def eng(X):
+    return X.Engine(0)
+
+
+def unit_of(X, c, path="u.mcu"):
+    prof = X.CompileProfile(c["compiler"], 12, c["relaxed"], c["erase"])
+    return (c["text"], path, prof, X.Mode(c["mode"]), X.TraitConfig(c["fund"]))
+
+
+def as_rows(a):
+    return [[d.code, d.severity.value, d.loc.line, d.loc.col, d.message, d.suppressed]
+            for d in a.all_diagnostics]
+
+
+@pytest.mark.parametrize("group", GOLDEN_GROUPS)
+def test_golden_vectors(X, eng, group):
+    cases = load_golden(group)
+    res = eng.run_batch([unit_of(X, c) for c in cases], want_walks=True)
+    bad = []
+    for c, a in zip(cases, res):
+        if as_rows(a) != c["diags"]:
+            bad.append((c["name"], as_rows(a)[:3], c["diags"][:3]))
+            continue
+        sides = {s.value for s in a.walks}
+        if sides != set(c["walks"]):
+            bad.append((c["name"], "walk sides", sides))
+            continue
+        for side, ent in c["walks"].items():
+            w = a.walks[X.ExecSpace(side)]
+            if (w.n_instances, w.n_edges, w.n_demands) != (
+                    ent["n_instances"], ent["n_edges"], ent["n_demands"]):
+                bad.append((c["name"], side, (w.n_instances, w.n_edges, w.n_demands),
+                            (ent["n_instances"], ent["n_edges"], ent["n_demands"])))
+    assert not bad, bad[:5]
+
+
+def test_golden_token_streams(X, eng):
+    """K1-K3 lexer parity: per-pass token streams / first E0002 / LexError."""
+    cases = [c for g in ("corpus", "mutations", "synthetic") for c in load_golden(g) if "lex" in c]
+    res = eng.run_batch([unit_of(X, c) for c in cases], want_walks=True)
+    bad = 0
+    h = eng.handle
+    st = h.pass_status(len(cases))
+    data = b"".join(c["text"].encode() for c in cases)
+    offs = [0]
+    for c in cases:
+        offs.append(offs[-1] + len(c["text"].encode()))
+    from paper_2309_03912_b200.messages import Renderer
+    ren = Renderer(data, offs, h.arena())
+    kinds = {1: "ident", 2: "int", 3: "string", 4: "punct", 5: "pragma"}
+    puncts = [None, "<<<", ">>>", "::", "==", "!=", "&&", "||", "++", "{", "}", "(", ")", "<",
+              ">", ",", ";", ".", "!", "="]
+    for f, c in enumerate(cases):
+        toks = h.tokens(f)
+        for p, kind in enumerate(["host", "device"][: len(c["lex"])]):
+            want = c["lex"][kind]
+            s = st[2 * f + p]
+            if "pp_error" in want:
+                ok = s["pp_line"] == want["pp_error"][0]
+            elif "lex_error" in want:
+                ok = (s["pp_line"] == 0 and s["lex_line"] == want["lex_error"][0]
+                      and s["lex_col"] == want["lex_error"][1])
+            else:
+                got = []
+                for t in toks:
+                    if not (int(t["mask"]) >> p) & 1:
+                        continue
+                    k = kinds[int(t["kind"])]
+                    if k == "punct":
+                        text = puncts[int(t["id"])]
+                    elif k == "int":
+                        text = None
+                    else:
+                        text = ren.span_text((int(t["pos"]) << 32) | (int(t["end"]) - int(t["pos"])))
+                    got.append([k, text, int(t["line"]), int(t["col"])])
+                got.append(["eof", "", int(s["eof_line"]), int(s["eof_col"])])
+                exp = [[k, (None if k == "int" else tx), ln, co] for k, tx, ln, co in want["tokens"]]
+                ok = s["pp_line"] == 0 and s["lex_line"] == 0 and got == exp
+            if not ok:
+                bad += 1
+    assert bad == 0
+
+
+def _oracle_rows(text, mode):
+    r = O.analyze_unit(text, mode)
+    rows = [[d[0], O.SEVERITY[d[0]], d[1], d[2], d[3], d[4]] for d in r.all_diagnostics]
+    walks = {w.native: (len(w.instances), sum(len(v) for v in w.edges.values()))
+             for w in r.walks.values()}
+    return rows, walks, O.edge_count(r)
+
+
+def _check_against_oracle(X, eng, texts, modes):
+    units = [(t, f"f{i:05d}.cu", X.CompileProfile(), X.Mode(m), X.TraitConfig())
+             for i, (t, m) in enumerate(zip(texts, modes))]
+    res = eng.run_batch(units, want_walks=True)
+    callsites = 0
+    want_calls = 0
+    for t, m, a in zip(texts, modes, res):
+        rows, walks, ec = _oracle_rows(t, m)
+        assert as_rows(a) == rows
+        for side, (ni, ne) in walks.items():
+            w = a.walks[X.ExecSpace(side)]
+            assert (w.n_instances, w.n_edges) == (ni, ne)
+        want_calls += ec
+    callsites = eng.last_stats["callsites"]
+    assert callsites == want_calls
+
+
+def test_c2_files_vs_oracle(X, eng):
+    from paper_2309_03912_b200 import synth
+    texts = [synth.gen_c2_file(1000 + s, 15000) for s in range(8)]
+    _check_against_oracle(X, eng, texts, ["classic", "sound", "fidelity", "proposal1"] * 2)
+
+
+def test_c5_stressors_vs_oracle(X, eng):
+    from paper_2309_03912_b200 import synth
+    texts = [synth.gen_c5_file(500 + s, 12000, 0.5) for s in range(10)]
+    _check_against_oracle(X, eng, texts, ["classic", "sound", "proposal2", "fidelity", "proposal1"] * 2)
+
+
+def test_c3_chain_vs_oracle(X, eng):
+    from paper_2309_03912_b200 import synth
+    text = synth.gen_chain(24, 48)
+    _check_against_oracle(X, eng, [text, text], ["classic", "sound"])
+
+
+def test_c4_callgraph_vs_oracle(X, eng):
+    from paper_2309_03912_b200 import synth
+    text = synth.gen_callgraph(2000, 10, 7)
+    _check_against_oracle(X, eng, [text], ["sound"])
+
+
+def test_batch_invariance_and_determinism(X, eng):
+    """A unit's result does not depend on its batch neighbours or on the run."""
+    from paper_2309_03912_b200 import synth
+    rng = random.Random(5)
+    texts = [synth.gen_c5_file(rng.randrange(10**6), 4000, 0.3) for _ in range(12)]
+    units = [(t, f"b{i}.cu", X.CompileProfile(), X.Mode.SOUND, X.TraitConfig()) for i, t in enumerate(texts)]
+    together = eng.run_batch(units)
+    again = eng.run_batch(units)
+    alone = [eng.run_batch([u])[0] for u in units]
+    for a, b, c in zip(together, again, alone):
+        assert as_rows(a) == as_rows(b) == as_rows(c)
+
+
+def test_public_api_check_unit(X):
+    src = """struct D { __device__ void call() {} };
+void a() { D{}.call(); }
+void b() { D{}.call(); }
+"""
+    got = [(d.code, d.loc.line) for d in X.check_unit(src, "u.mcu")]
+    assert got == [("E1001", 2), ("E1001", 3)]

@@ -106,6 +106,8 @@ int exs_describe(exs_handle h, const uint32_t* ids, const uint8_t* kinds, uint32
                  exs_desc* out);
 /* options: 1 = also compute per-walk demand counts (Analysis.walks parity) */
 int exs_set_option(exs_handle h, int key, int value);
+/* with EXS_PROFILE=1 in the environment: per-launch-site device times of the last run */
+const char* exs_profile_text(void);
 /* per-stage device time of the last run (ms): lex, parse, sema, walk */
 int exs_stage_times(exs_handle h, float* out4);
 

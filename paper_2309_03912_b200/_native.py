@@ -57,7 +57,7 @@ class Stats(C.Structure):
 EXPORTS = [
     "exs_create", "exs_destroy", "exs_last_error", "exs_run", "exs_run_device", "exs_get_stats",
     "exs_get_diags", "exs_get_arena", "exs_get_pass_status", "exs_get_tokens",
-    "exs_get_walk_stats", "exs_describe", "exs_set_option", "exs_stage_times",
+    "exs_get_walk_stats", "exs_describe", "exs_set_option", "exs_stage_times", "exs_profile_text",
 ]
 
 
@@ -76,6 +76,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     lib.exs_create.argtypes = [C.c_int, C.POINTER(vp)]
     lib.exs_destroy.argtypes = [vp]
     lib.exs_last_error.restype = C.c_char_p
+    lib.exs_profile_text.restype = C.c_char_p
     lib.exs_run.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
     lib.exs_run_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
     lib.exs_get_stats.argtypes = [vp, C.POINTER(Stats)]
@@ -88,7 +89,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     lib.exs_set_option.argtypes = [vp, C.c_int, C.c_int]
     lib.exs_stage_times.argtypes = [vp, C.POINTER(C.c_float)]
     for name in EXPORTS:
-        if name not in ("exs_last_error",):
+        if name not in ("exs_last_error", "exs_profile_text"):
             getattr(lib, name).restype = C.c_int
     _ = (u8p, u32p)
     return lib

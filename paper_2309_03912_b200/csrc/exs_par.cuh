@@ -30,12 +30,22 @@ struct Err : std::runtime_error {
 #endif
 
 // ----------------------------------------------------------------- memory
+#ifndef EXS_EMU
+extern thread_local cudaStream_t g_alloc_stream;
+#endif
+#ifndef EXS_EMU
+// Size-exact block cache over the stream-ordered pool: a repeated batch shape
+// (the steady state of a corpus service) allocates nothing.  All work is on
+// one stream per handle, so a block freed in stream order is safe to reuse.
+void* cache_alloc(size_t bytes);
+void cache_free(void* p);
+#endif
 template <class T>
 T* dalloc(size_t n) {
   if (n == 0) n = 1;
   void* p = nullptr;
 #ifndef EXS_EMU
-  CK(cudaMalloc(&p, n * sizeof(T)));
+  p = cache_alloc(n * sizeof(T));
 #else
   p = calloc(n, sizeof(T));
   if (!p) throw Err("out of host memory");
@@ -45,7 +55,7 @@ T* dalloc(size_t n) {
 inline void dfree(void* p) {
   if (!p) return;
 #ifndef EXS_EMU
-  cudaFree(p);
+  cache_free(p);
 #else
   free(p);
 #endif
@@ -111,23 +121,78 @@ template <class F>
 __global__ void __launch_bounds__(256) k_for(F f, i64 n) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) f(i);
 }
+// latency-bound walkers: cap registers (64/thread) so 32 warps fit per SM
+template <class F>
+__global__ void __launch_bounds__(128, 8) k_for_walk(F f, i64 n) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) f(i);
+}
 extern int g_sm_count;
 extern u64 g_launches;
+// optional per-launch device timing (EXS_PROFILE=1): (site, start, stop) events
+struct ProfRec { const char* fn; int line; cudaEvent_t a, b; };
+extern bool g_profile;
+extern std::vector<ProfRec> g_prof;
 #endif
 
 template <class F>
-void par_for(i64 n, F f, cudaStream_t s, int block = 256) {
+void par_for(i64 n, F f, cudaStream_t s, int block = 256, const char* fn = __builtin_FUNCTION(),
+             int line = __builtin_LINE()) {
   if (n <= 0) return;
 #ifndef EXS_EMU
   i64 want = (n + block - 1) / block;
   i64 cap = (i64)g_sm_count * 16;
   int grid = (int)(want < cap ? want : cap);
+  ProfRec pr{fn, line, nullptr, nullptr};
+  if (g_profile) {
+    cudaEventCreate(&pr.a); cudaEventCreate(&pr.b);
+    cudaEventRecord(pr.a, s);
+  }
   k_for<<<grid, block, 0, s>>>(f, n);
   CK(cudaGetLastError());
+  if (g_profile) { cudaEventRecord(pr.b, s); g_prof.push_back(pr); }
   g_launches++;
 #else
+  (void)fn; (void)line;
   (void)s; (void)block;
   for (i64 i = 0; i < n; i++) f(i);
+#endif
+}
+
+// launch for the heavy walker kernels (128 threads, register-capped)
+template <class F>
+void par_for_walk(i64 n, F f, cudaStream_t s, const char* fn = __builtin_FUNCTION(),
+                  int line = __builtin_LINE()) {
+  if (n <= 0) return;
+#ifndef EXS_EMU
+  i64 want = (n + 127) / 128;
+  i64 cap = (i64)g_sm_count * 64;
+  int grid = (int)(want < cap ? want : cap);
+  ProfRec pr{fn, line, nullptr, nullptr};
+  if (g_profile) {
+    cudaEventCreate(&pr.a); cudaEventCreate(&pr.b);
+    cudaEventRecord(pr.a, s);
+  }
+  k_for_walk<<<grid, 128, 0, s>>>(f, n);
+  CK(cudaGetLastError());
+  if (g_profile) { cudaEventRecord(pr.b, s); g_prof.push_back(pr); }
+  g_launches++;
+#else
+  (void)s; (void)fn; (void)line;
+  for (i64 i = 0; i < n; i++) f(i);
+#endif
+}
+
+// profiling marks on the stream timeline: the interval between consecutive
+// marks includes host-side gaps (allocation, synchronisation, launch latency)
+inline void prof_mark(cudaStream_t s, const char* fn = __builtin_FUNCTION(), int line = __builtin_LINE()) {
+#ifndef EXS_EMU
+  if (!g_profile) return;
+  ProfRec pr{fn, -line, nullptr, nullptr};
+  cudaEventCreate(&pr.a);
+  cudaEventRecord(pr.a, s);
+  g_prof.push_back(pr);
+#else
+  (void)s; (void)fn; (void)line;
 #endif
 }
 

@@ -35,13 +35,15 @@ EXS_HD inline bool val_eq(const Val& a, const Val& b) {
 }
 
 // Struct and function records (one per declaration, view-local order)
-enum { FR_DUP = 1, FR_OWNER = 2, FR_MEMBER = 4 };
+enum { FR_DUP = 1, FR_OWNER = 2, FR_MEMBER = 4, FR_VARDECL = 8 };
 struct FnRec {
   u32 node, view, rec, order;  // rec: containing struct record (NONE for free)
   u64 sig, name;               // signature hash (sema.py:144-149), name hash
   u32 sig_rep;                 // first decl of the view with this signature
   u32 ncalls;                  // call sites in the body (edges/s unit)
-  u8 flags, pad[7];
+  u8 flags, pad[3];
+  u32 nstmts;                  // top-level statements of the body
+  u32 stmt_base, pad2;         // first entry in the per-statement tables
 };
 struct RecRec {
   u32 node, view, order, dup;

@@ -185,14 +185,34 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
   S.arena_top = dalloc<u32>(1);
   dzero(S.arena_top, 4, st);
   S.line_info = dalloc<LineInfo>(L + 1);
+  S.line_ntok = dalloc<u32>(L + 1);
+  S.line_tok = dalloc<u32>(L + 2);
+  S.line_err = dalloc<u16>(L + 1);
+  S.line_err_col = dalloc<u32>(L + 1);
+  S.line_err_pos = dalloc<u32>(L + 1);
   {
+    // one pass per logical line: directive detection + token count (the
+    // count does not depend on pass activity: tokens of inactive lines are
+    // emitted with an empty pass mask and ignored downstream)
     const u32* ls = S.line_start; const u32* lh = S.line_hi; const u8* lst = S.line_st;
+    const u32* lno = S.line_no; const u32* lf = S.line_file;
     const u8* s = S.src; const u32* sp = S.splice; LineInfo* li = S.line_info;
     u8* ar = S.arena; u32* at = S.arena_top; u32 cap = S.arena_cap;
-    par_for(L, [=] EXS_HD (i64 i) {
-      li[i] = scan_line_directive(s, sp, ls[i], lh[i], lst[i], ar, at, cap);
+    u32* nt = S.line_ntok; u16* le = S.line_err; u32* lec = S.line_err_col; u32* lep = S.line_err_pos;
+    par_for(L + 1, [=] EXS_HD (i64 i) {
+      if (i == L) { nt[i] = 0; return; }
+      LineInfo x = scan_line_directive(s, sp, ls[i], lh[i], lst[i], ar, at, cap);
+      li[i] = x;
+      if (x.kind >= LK_IFDEF) { nt[i] = 0; le[i] = 0; return; }
+      LexErr e;
+      nt[i] = lex_line(s, sp, ls[i], lh[i], lst[i], lno[i], lf[i], 0, nullptr, &e);
+      le[i] = e.msg;
+      lec[i] = e.col;
+      lep[i] = e.pos;
     }, st);
   }
+  excl_scan_u32(S.line_ntok, S.line_tok, L + 1, sc, st);
+  S.T = get1(S.line_tok + L, st);
   S.dir_line = dalloc<u32>(L + 1);
   {
     const LineInfo* li = S.line_info;
@@ -298,50 +318,23 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
       lm[i] = m;
     }, st);
   }
-  // tokens: count, scan, emit
-  S.line_ntok = dalloc<u32>(L + 1);
-  S.line_tok = dalloc<u32>(L + 2);
-  S.line_err = dalloc<u16>(L + 1);
-  S.line_err_col = dalloc<u32>(L + 1);
-  S.line_err_pos = dalloc<u32>(L + 1);
-  {
-    const u32* ls = S.line_start; const u32* lh = S.line_hi; const u8* lst = S.line_st;
-    const u32* lno = S.line_no; const u32* lf = S.line_file; const u8* lm = S.line_mask;
-    const u8* s = S.src; const u32* sp = S.splice;
-    u32* nt = S.line_ntok; u16* le = S.line_err; u32* lec = S.line_err_col; u32* lep = S.line_err_pos;
-    FP* fp = S.fp;
-    par_for(L, [=] EXS_HD (i64 i) {
-      u8 m = lm[i];
-      if (!m) { nt[i] = 0; le[i] = 0; return; }
-      LexErr e;
-      u32 n = lex_line(s, sp, ls[i], lh[i], lst[i], lno[i], lf[i], m, nullptr, &e);
-      nt[i] = n;
-      le[i] = e.msg;
-      lec[i] = e.col;
-      lep[i] = e.pos;
-      if (e.msg) {
-        u32 f = lf[i];
-        for (u32 p = 0; p < 2; p++)
-          if ((m >> p) & 1) at_min(&fp[2 * f + p].lex_line, (u32)i);
-      }
-    }, st);
-  }
-  excl_scan_u32(S.line_ntok, S.line_tok, L + 1, sc, st);  // line_ntok[L] is garbage-free? set below
-  S.T = L ? get1(S.line_tok + L - 1, st) + get1(S.line_ntok + L - 1, st) : 0;
-  {
-    u32 T = S.T;
-    h2d(S.line_tok + L, &T, 4, st);
-  }
+  // tokens: emit (counts and offsets come from the directive pass)
   S.toks = dalloc<Tok>((size_t)S.T + 1);
   {
     const u32* ls = S.line_start; const u32* lh = S.line_hi; const u8* lst = S.line_st;
     const u32* lno = S.line_no; const u32* lf = S.line_file; const u8* lm = S.line_mask;
     const u8* s = S.src; const u32* sp = S.splice; const u32* lt = S.line_tok; Tok* tk = S.toks;
+    const u16* le = S.line_err; const u32* nt = S.line_ntok; FP* fp = S.fp;
     par_for(L, [=] EXS_HD (i64 i) {
+      if (!nt[i] && !le[i]) return;
       u8 m = lm[i];
-      if (!m) return;
       LexErr e;
       lex_line(s, sp, ls[i], lh[i], lst[i], lno[i], lf[i], m, tk + lt[i], &e);
+      if (e.msg) {
+        u32 f = lf[i];
+        for (u32 p = 0; p < 2; p++)
+          if ((m >> p) & 1) at_min(&fp[2 * f + p].lex_line, (u32)i);
+      }
     }, st);
   }
   // EOF positions and first errors per (file, pass)

@@ -18,10 +18,12 @@ struct SemaState {
   u64* sig_k = nullptr; u32* sig_v = nullptr; u32 sig_mask = 0;    // resolve duplicates
   u64* siga_k = nullptr; u32* siga_v = nullptr; u32 siga_mask = 0; // walk-visible sig reps
   u32* fcand = nullptr, *fcand_cnt = nullptr;
+  u32 NS = 0;                                  // top-level statements of all bodies
+  u32* stmt_node = nullptr, *stmt_cs = nullptr;  // per statement: node, call sites before it
   Tables tab;
   void free_all() {
     void* ps[] = {fns, recs, item_fn, item_rec, smap_k, smap_v, fmap_k, fmap_v, sig_k, sig_v,
-                  siga_k, siga_v, fcand, fcand_cnt};
+                  siga_k, siga_v, fcand, fcand_cnt, stmt_node, stmt_cs};
     for (void* p : ps) dfree(p);
   }
 };
@@ -179,7 +181,10 @@ struct BodyScan {
     depth--;
   }
   EXS_HD void stmts(u32 s) {
-    for (; s != NONE; s = nodes[s].next) {
+    for (; s != NONE; s = nodes[s].next) one(s);
+  }
+  EXS_HD void one(u32 s) {
+    {
       const Node& n = nodes[s];
       switch (n.kind) {
         case N_SEXPR: expr(n.c0); break;
@@ -404,12 +409,39 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
         const Tok& t = tk[n.tok];
         emit_diag(B, mkdiag(vf[r.view], t.line, t.col, C_E0001, M_S_COND_SPEC_MODE));
       }
+      r.nstmts = 0;
       if (n.n & FF_BODY) {
         BodyScan bs{nd, tk, &tab, r.view, (c & CFG_PLAIN) != 0, 0, &B, vf[r.view], 0};
         bs.stmts(n.c2);
         r.ncalls = bs.ncalls;
+        for (u32 s = n.c2; s != NONE; s = nd[s].next) r.nstmts++;
       }
     }, st);
+    // per-statement tables: chunks of a body are walked in parallel (K6)
+    u32* ns = dalloc<u32>(NF + 1);
+    u32* sb = dalloc<u32>(NF + 1);
+    par_for(NF + 1, [=] EXS_HD (i64 i) { ns[i] = i < NF ? fr[i].nstmts : 0; }, st);
+    excl_scan_u32(ns, sb, NF + 1, sc, st);
+    S.NS = get1(sb + NF, st);
+    S.stmt_node = dalloc<u32>(S.NS + 1);
+    S.stmt_cs = dalloc<u32>(S.NS + 1);
+    u32* sn = S.stmt_node; u32* scs = S.stmt_cs;
+    par_for(NF, [=] EXS_HD (i64 i) {
+      FnRec& r = fr[i];
+      r.stmt_base = sb[i];
+      if (!r.nstmts) return;
+      BodyScan bs{nd, tk, &tab, r.view, false, 0, nullptr, 0, 0};
+      u32 k = 0;
+      for (u32 s = nd[r.node].c2; s != NONE; s = nd[s].next, k++) {
+        sn[sb[i] + k] = s;
+        scs[sb[i] + k] = bs.ncalls;
+        if (nd[s].kind == N_SVAR) r.flags |= FR_VARDECL;
+        bs.one(s);
+      }
+    }, st);
+    sync(st);
+    dfree(ns);
+    dfree(sb);
   }
   // 7. static assertions (sema.py:200-217)
   {

@@ -68,7 +68,8 @@ EXS_HD inline void walker_for(Walker& w, const WalkCfg& C, const WalkBufs& B, u3
   w.from_hd = I.spaces == 3;
   w.fidelity_host = (c & CFG_MODE_MASK) == MODE_FIDELITY && w.native == 0;
   w.parent_rank = rank;
-  w.local = 0;
+  w.stmt_k = 0; w.stmt_ord = 0; w.stmt_cs_base = 0; w.cs_ord = 0;
+  w.silent = false; w.asp = 0; w.nloc = 0; w.wdepth = 0;
   w.ebase = I.ebase;
   w.ecnt = 0;
   w.contract = false;
@@ -143,12 +144,13 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     return B;
   };
   WalkBufs B = bufs();
+  prof_mark(st);
   // ---- roots (spacecheck.py:272-308)
   {
     const FnRec* fr = S.fns; const RecRec* rr = S.recs; const Node* nd = P.nodes; const Tok* tk = L.toks;
     const FP* fp = L.fp; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
     const Tables* tab = dtab;
-    par_for(2ull * NF, [=] EXS_HD (i64 x) {
+    par_for_walk(2ull * NF, [=] EXS_HD (i64 x) {
       u32 i = (u32)(x >> 1), p = (u32)(x & 1);
       const FnRec& r = fr[i];
       u32 file = vf[r.view];
@@ -172,7 +174,9 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       w.native = (u8)p; w.side = 0; w.clevel = 0;  // roots are created at level 0
       w.fn = i; w.pragma = false; w.from_hd = false;
       w.fidelity_host = mode == MODE_FIDELITY && p == 0;
-      w.parent_rank = i; w.local = 0; w.contract = false;
+      w.parent_rank = i; w.contract = false;
+      w.stmt_k = 0; w.stmt_ord = 0; w.stmt_cs_base = 0; w.cs_ord = 0;
+      w.silent = false; w.asp = 0; w.nloc = 0; w.wdepth = 0; w.ebase = 0; w.ecnt = 0;
       Val ot = vnone();
       if (r.rec != NONE) {
         u32 canon = w.S.struct_of(rr[r.rec].name);
@@ -193,11 +197,12 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       u32 k = 0;
       for (u8 sd = 0; sd < 2; sd++) {
         if (!((sides >> sd) & 1)) continue;
-        w.local = k++;
+        w.stmt_ord = k++;  // roots: decl order x side order (spacecheck.py:272-283)
         w.instantiate(i, vnone(), vnone(), sd, r.rec, none, ot, fn.tok);
       }
     }, st);
   }
+  prof_mark(st);
   // ---- levels
   u32 prev_n = 0;
   u32 level = 0;
@@ -211,6 +216,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     sync(st);
     if (cnt[4]) { dfree(dtab); dfree(front); return false; }
     u32 n_now = cnt[0];
+    prof_mark(st);
     // fixup creators of this level (min creation key wins)
     {
       const CreateLog* lg = W.log; Inst* in = W.inst;
@@ -225,6 +231,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     // (done inside instantiate via the log; apply min here)
     u32 nnew = n_now - prev_n;
     if (!nnew) break;
+    prof_mark(st);
     // frontier: new instances with bodies, ordered by creation key
     grow(front, front_cap, nnew + 1, 0, st);
     u32 nf;
@@ -244,6 +251,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     }
     prev_n = n_now;
     if (!nf) break;
+    prof_mark(st);
     // edge bases: scan of call-site counts
     u32* ec = dalloc<u32>(nf + 1);
     u32* eb = dalloc<u32>(nf + 1);
@@ -264,29 +272,51 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       Inst* in = W.inst; const u32* fl = front; u64 eu = edges_used;
       par_for(nf, [=] EXS_HD (i64 j) { in[fl[j]].ebase = (u32)(eu + eb[j]); }, st);
     }
+    dfill_ff(W.edges + edges_used, 4ull * S_level, st);  // empty edge slots
     edges_used += S_level;
-    // walk the frontier (one thread per instance)
+    prof_mark(st);
+    // walk the frontier: one thread per (instance, chunk of top-level statements)
     {
-      const u32* fl = front;
+      const u32 KCH = 2;
+      u32* wc = dalloc<u32>(nf + 1);
+      u32* wb = dalloc<u32>(nf + 1);
+      const Inst* in = W.inst; const FnRec* fr = S.fns; const u32* fl = front;
+      par_for(nf + 1, [=] EXS_HD (i64 j) {
+        u32 n = j < nf ? fr[in[fl[j]].fn].nstmts : 0;
+        wc[j] = j < nf ? (n ? (n + KCH - 1) / KCH : 1) : 0;
+      }, st);
+      excl_scan_u32(wc, wb, nf + 1, sc, st);
+      u32 nwi = get1(wb + nf, st);
       WalkCfg Cc = C;
       u32* ct = B.contract;
-      par_for(nf, [=] EXS_HD (i64 j) {
+      const u32* sn = S.stmt_node; const u32* scs = S.stmt_cs;
+      const u32 nfc = nf;
+      par_for_walk(nwi, [=] EXS_HD (i64 i) {
+        u32 lo = 0, hi = nfc;  // instance j with wb[j] <= i < wb[j+1]
+        while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (wb[mid] <= (u32)i) lo = mid; else hi = mid; }
+        u32 j = lo, c = (u32)i - wb[j];
         Walker w;
         walker_for(w, Cc, B, fl[j], (u64)j);
-        w.run_body();
-        B.inst[fl[j]].ecnt = w.ecnt;
+        const FnRec& r = fr[w.fn];
+        u32 k0 = c * KCH, k1 = k0 + KCH < r.nstmts ? k0 + KCH : r.nstmts;
+        w.run_chunk(sn, scs, r.stmt_base, k0, k1);
+        if (w.ecnt) at_add(&B.inst[fl[j]].ecnt, w.ecnt);
         if (w.contract) at_or(&ct[w.file], 1);
-      }, st, 128);
+      }, st);
+      sync(st);
+      dfree(wc);
+      dfree(wb);
     }
-    sync(st);
     dfree(ec);
     dfree(eb);
+    prof_mark(st);
     level++;
   }
   W.levels = level;
   dfree(front);
   W.n_inst = prev_n;
   W.n_edges = edges_used;
+  prof_mark(st);
   // ---- main instance per walk: the last created (max creation key)
   {
     const Inst* in = W.inst; unsigned long long* mk = W.main_key; u32* mi = W.main_inst;
@@ -304,6 +334,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       if ((in[i].flags & IF_MAIN) && mk[in[i].walk] == in[i].ckey + 1) mi[in[i].walk] = (u32)i;
     }, st);
   }
+  prof_mark(st);
   // ---- reachability (spacecheck.py:617-632)
   W.visited = dalloc<u8>((u64)W.n_inst + 8);
   dzero(W.visited, (u64)W.n_inst + 8, st);
@@ -344,15 +375,17 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     }, st);
     u32 nq = get1(qn, st);
     const u32* ed = W.edges;
+    const FnRec* fr_ = S.fns;
     while (nq) {
       dzero(qn + 1, 4, st);
       const u32* qa = q0; u32* qb = q1;
       par_for(nq, [=] EXS_D (i64 j) {
         const Inst& I = in[qa[j]];
         u8 native = (u8)(I.walk & 1);
-        for (u32 e = 0; e < I.ecnt; e++) {
+        u32 ns = fr_[I.fn].ncalls;
+        for (u32 e = 0; e < ns; e++) {
           u32 c = ed[I.ebase + e];
-          if (in[c].side != native) continue;
+          if (c == NONE || in[c].side != native) continue;
 #ifndef EXS_EMU
           u32* wp = (u32*)(vis + (c & ~3u));
           u32 sh = (c & 3u) * 8;
@@ -372,6 +405,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     sync(st);
     dfree(q0); dfree(q1); dfree(qn);
   }
+  prof_mark(st);
   // ---- pending verdicts (spacecheck.py:634-655)
   {
     std::vector<u32> cnt(8);

@@ -175,9 +175,9 @@ EXS_HD inline bool hard_code(u16 c) {
          c == C_E0104 || c == C_E1301 || c == C_E1302;
 }
 
-#define MAX_LOCALS 64
+#define MAX_LOCALS 32
 #define MAX_WALK_DEPTH 160
-#define MAX_ARGS 32
+#define MAX_ARGS 48
 
 struct Walker {
   Sema S;
@@ -189,8 +189,10 @@ struct Walker {
   u32 fn;                    // decl of the instance
   bool pragma, from_hd, fidelity_host;
   u64 parent_rank;           // dense rank of this instance within its level
-  u32 local;                 // _instantiate call counter (creation order)
-  u32 ebase, ecnt;
+  u32 stmt_k, stmt_ord;      // creation order: (top-level statement, ordinal within it)
+  u32 ebase, ecnt;           // edge slots of this instance, legal edges written
+  u32 stmt_cs_base, cs_ord;  // edge slot of the current statement, edges in it so far
+  bool silent;               // replaying declarations of earlier chunks: no side effects
   Env env;                   // owner bindings + bindings
   Env obinds_self;           // owner bindings of this instance
   u32 orec_self;
@@ -200,6 +202,9 @@ struct Walker {
   Val lval[MAX_LOCALS];
   int wdepth;
   bool contract;
+  // argument types of the calls being walked (a stack shared by all frames)
+  u32 asp;
+  Val astk[MAX_ARGS];
 
   EXS_HD const Node& N(u32 id) const { return T->nodes[id]; }
   EXS_HD const Tok& K(u32 t) const { return T->toks[t]; }
@@ -207,7 +212,7 @@ struct Walker {
 
   EXS_HD void emit(u16 code, u32 line, u32 col, u16 msg, u64 a0 = 0, u64 a1 = 0, u64 a2 = 0,
                    u32 a3 = 0) {
-    if (fidelity_host && !hard_code(code)) return;
+    if (silent || (fidelity_host && !hard_code(code))) return;
     emit_diag(*B, mkdiag(file, line, col, code, msg, a0, a1, a2, a3));
   }
   EXS_HD void emit_tok(u16 code, u32 tok, u16 msg, u64 a0 = 0, u64 a1 = 0, u64 a2 = 0, u32 a3 = 0) {
@@ -250,7 +255,7 @@ struct Walker {
   // _instantiate (spacecheck.py:312-351); returns instance id or NONE
   EXS_HD u32 instantiate(u32 fi, const Val& tb, const Val& hb, u8 want_side, u32 orec,
                          const Env& obinds, const Val& ot, u32 at_tok) {
-    u32 my_local = local++;
+    u32 my_local = (stmt_k << 12) | (stmt_ord++ & 0xFFFu);
     // merged = owner bindings + bindings
     Env merged = obinds;
     merged.nbase = merged.n;
@@ -271,8 +276,9 @@ struct Walker {
     bool inserted;
     u32 id = inst_lookup_or_insert(*B, k, inserted);
     if (id == NONE) return NONE;
-    unsigned long long ck = ((unsigned long long)clevel << 52) |
-                            ((unsigned long long)parent_rank << 24) | (my_local & 0xFFFFFFu);
+    unsigned long long ck = ((unsigned long long)clevel << 54) |
+                            ((unsigned long long)(parent_rank & 0x3FFFFFFull) << 28) |
+                            (my_local & 0xFFFFFFFu);
     Inst& I = B->inst[id];
     if (inserted) {
       I.ka = k.a; I.kb = k.b;
@@ -343,7 +349,9 @@ struct Walker {
     u8 want = legal ? side : ((sp & 1) ? 0 : 1);
     u32 callee = instantiate(fi, tb, hb, want, orec, obinds, ot, loc_tok);
     if (legal && callee != NONE) {
-      B->edges[ebase + ecnt] = callee;
+      // slot: post-order position inside the statement, statements in order
+      B->edges[ebase + stmt_cs_base + cs_ord] = callee;
+      cs_ord++;
       ecnt++;
     }
     if (!legal) stray(sp == 1 ? 1 : 2, loc_tok);
@@ -357,7 +365,8 @@ struct Walker {
   // (free: fcand run) or (member: struct rec).  Returns false on failure.
   EXS_HD bool select(bool member, u32 first, u32 count, u32 rec, u64 mname, u32 targs,
                      const Val* argtys, u32 nargs, u32 loc_tok, u8 ctx_side, const Env& obinds,
-                     u64 name_a0, u64 name_a1, u32& out_fi, Val& out_tb, Val& out_hb) {
+                     u64 name_a0, u64 name_a1, u32& out_fi, Val& out_tb, Val& out_hb,
+                     u32 name_targ = 0) {
     u32 nviable = 0;
     u32 vfi[8];
     Val vtb[8], vhb[8];
@@ -412,8 +421,8 @@ struct Walker {
         }
       if (nc) nviable = nc;
     }
-    if (nviable == 0) { emit_tok(C_E1301, loc_tok, M_S_NO_VIABLE, name_a0, name_a1); return false; }
-    if (nviable > 1) { emit_tok(C_E1302, loc_tok, M_S_AMBIGUOUS, name_a0, name_a1, nviable); return false; }
+    if (nviable == 0) { emit_tok(C_E1301, loc_tok, M_S_NO_VIABLE, name_a0, name_a1, 0, name_targ); return false; }
+    if (nviable > 1) { emit_tok(C_E1302, loc_tok, M_S_AMBIGUOUS, name_a0, name_a1, nviable, name_targ); return false; }
     out_fi = vfi[0]; out_tb = vtb[0]; out_hb = vhb[0];
     return true;
   }
@@ -425,12 +434,14 @@ struct Walker {
     return c;
   }
 
-  // walk args (post-order) into types
-  EXS_HD u32 walk_args(u32 args, Val* tys) {
+  // walk args (post-order) pushing their types on the argument stack; the
+  // caller pops with asp = base after dispatching
+  EXS_HD u32 walk_args(u32 args, u32& base) {
+    base = asp;
     u32 n = 0;
     for (u32 a = args; a != NONE; a = N(a).next) {
       Val t = expr(a);
-      if (n < MAX_ARGS) tys[n] = t;
+      if (asp < MAX_ARGS) astk[asp++] = t;
       else contract = true;
       n++;
     }
@@ -502,16 +513,18 @@ struct Walker {
         u8 rk = N(recv).kind;
         if (rt.k == V_NONE && rk != N_TMP && rk != N_NAME)
           emit_tok(C_E0001, S.loc_tok(recv), M_W_RECEIVER);
-        Val tys[MAX_ARGS];
-        u32 na = walk_args(n.c2, tys);
-        if (rt.k != V_NONE) member_dispatch(rt, n.tok, n.c1, tys, na, S.loc_tok(e));
+        u32 base;
+        u32 na = walk_args(n.c2, base);
+        if (rt.k != V_NONE && !contract) member_dispatch(rt, n.tok, n.c1, astk + base, na, S.loc_tok(e));
+        asp = base;
         return vnone();
       }
       case N_SCALL: {
-        Val tys[MAX_ARGS];
-        u32 na = walk_args(n.c2, tys);
+        u32 base;
+        u32 na = walk_args(n.c2, base);
         Val t = soft_type(n.c0, N(n.c0).tok);
-        if (t.k != V_NONE) member_dispatch(t, n.tok, n.c1, tys, na, N(n.c0).tok);
+        if (t.k != V_NONE && !contract) member_dispatch(t, n.tok, n.c1, astk + base, na, N(n.c0).tok);
+        asp = base;
         return vnone();
       }
       default:
@@ -521,8 +534,13 @@ struct Walker {
 
   EXS_HD Val free_call(u32 e) {
     const Node& n = N(e);
-    Val tys[MAX_ARGS];
-    u32 na = walk_args(n.c2, tys);
+    u32 base;
+    u32 na = walk_args(n.c2, base);
+    Val r = contract ? vnone() : free_call_(n, astk + base, na);
+    asp = base;
+    return r;
+  }
+  EXS_HD Val free_call_(const Node& n, const Val* tys, u32 na) {
     bool is_std = n.sub == CALL_STD;
     u64 nm = is_std ? hcombine(word_hash("std::"), K(n.c0).hv) : K(n.tok).hv;
     u32 run = is_std ? NONE : T->fmap.find(vkey(S.view, nm));
@@ -570,7 +588,7 @@ struct Walker {
     u32 fi; Val tb, hb;
     // name for messages: "{type display}::{name}"
     if (select(true, 0, 0, rt.rec, mname, targs, tys, na, loc_tok, side, ob,
-               span(name_tok), tname | 0, fi, tb, hb))
+               span(name_tok), tname, fi, tb, hb, rt.targ))
       dispatch(fi, tb, hb, loc_tok, rt.rec, ob, rt);
   }
 
@@ -578,36 +596,39 @@ struct Walker {
   EXS_HD void stmts(u32 s) {
     for (; s != NONE; s = N(s).next) {
       if (contract) return;
-      const Node& n = N(s);
-      switch (n.kind) {
-        case N_SEXPR: expr(n.c0); break;
-        case N_SRET: if (n.c0 != NONE) expr(n.c0); break;
-        case N_SVAR: {
-          Val t = soft_type(n.c0, N(n.c0).tok);
-          local_set(K(n.tok).hv, t);
-          break;
-        }
-        case N_SIF: {
-          expr(n.c0);
-          u32 mark = nloc;
-          stmts(n.c1);
-          nloc = mark;
-          if (n.sub) { stmts(n.c2); nloc = mark; }
-          break;
-        }
-        case N_SFOR: {
-          expr(n.c0);
-          expr(n.c1);
-          u32 mark = nloc;
-          Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int");
-          local_set(K(n.tok).hv, t);
-          stmts(n.c2);
-          nloc = mark;
-          break;
-        }
-        case N_SLAUNCH: launch(s); break;
-        default: break;
+      stmt(s);
+    }
+  }
+  EXS_HD void stmt(u32 s) {
+    const Node& n = N(s);
+    switch (n.kind) {
+      case N_SEXPR: expr(n.c0); break;
+      case N_SRET: if (n.c0 != NONE) expr(n.c0); break;
+      case N_SVAR: {
+        Val t = soft_type(n.c0, N(n.c0).tok);
+        local_set(K(n.tok).hv, t);
+        break;
       }
+      case N_SIF: {
+        expr(n.c0);
+        u32 mark = nloc;
+        stmts(n.c1);
+        nloc = mark;
+        if (n.sub) { stmts(n.c2); nloc = mark; }
+        break;
+      }
+      case N_SFOR: {
+        expr(n.c0);
+        expr(n.c1);
+        u32 mark = nloc;
+        Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int");
+        local_set(K(n.tok).hv, t);
+        stmts(n.c2);
+        nloc = mark;
+        break;
+      }
+      case N_SLAUNCH: launch(s); break;
+      default: break;
     }
   }
 
@@ -617,16 +638,17 @@ struct Walker {
     u32 grid = n.c1;
     expr(grid);
     expr(N(grid).next);
-    Val tys[MAX_ARGS];
-    u32 na = walk_args(n.c2, tys);
+    u32 base;
+    u32 na = walk_args(n.c2, base);
     if (side == 1) emit_tok(C_E1003, n.tok, M_W_LAUNCH_DEVICE);
     u32 run = T->fmap.find(vkey(S.view, K(n.tok).hv));
-    if (run == NONE) return;
+    if (run == NONE || contract) { asp = base; return; }
     u32 fi; Val tb, hb;
     Env none; none.clear();
-    if (!select(false, run, T->fcand_cnt[run], NONE, 0, n.c0, tys, na, n.tok, 1, none,
-                span(n.tok), 0, fi, tb, hb))
-      return;
+    bool ok = select(false, run, T->fcand_cnt[run], NONE, 0, n.c0, astk + base, na, n.tok, 1, none,
+                     span(n.tok), 0, fi, tb, hb);
+    asp = base;
+    if (!ok) return;
     if (!(N(T->fns[fi].node).n & FF_G)) { emit_tok(C_E1004, n.tok, M_W_LAUNCH_NONGLOBAL); return; }
     u32 tgt = instantiate(fi, tb, hb, 1, NONE, none, vnone(), n.tok);
     if (tgt != NONE && side == 0) {
@@ -636,16 +658,34 @@ struct Walker {
     }
   }
 
-  // _walk_instance (spacecheck.py:355-361)
-  EXS_HD void run_body() {
+  // _walk_instance (spacecheck.py:355-361) over top-level statements
+  // [k0, k1) of the body.  A chunk that does not start the body first
+  // replays, silently, the parameter and top-level declarations before it
+  // (only those reach later statements: nested blocks are scoped).
+  EXS_HD void run_chunk(const u32* stmt_node, const u32* stmt_cs, u32 sbase, u32 k0, u32 k1) {
     const Node& fnn = N(T->fns[fn].node);
     nloc = 0;
     wdepth = 0;
+    asp = 0;
+    silent = k0 != 0;
     for (u32 p = fnn.c1; p != NONE; p = N(p).next) {
       Val t = soft_type(N(p).c0, N(p).tok);
       local_set(K(N(p).tok).hv, t);
     }
-    stmts(fnn.c2);
+    if (T->fns[fn].flags & FR_VARDECL) {
+      for (u32 k = 0; k < k0; k++) {
+        const Node& s = N(stmt_node[sbase + k]);
+        if (s.kind == N_SVAR) local_set(K(s.tok).hv, soft_type(s.c0, N(s.c0).tok));
+      }
+    }
+    silent = false;
+    for (u32 k = k0; k < k1 && !contract; k++) {
+      stmt_k = k;
+      stmt_ord = 0;
+      stmt_cs_base = stmt_cs[sbase + k];
+      cs_ord = 0;
+      stmt(stmt_node[sbase + k]);
+    }
   }
 };
 

@@ -8,12 +8,118 @@
 #include "exs_stage_walk.cuh"
 #include "../../include/exspace_b200.h"
 #include <chrono>
+#include <map>
 #include <mutex>
 
 namespace exs {
 #ifndef EXS_EMU
 int g_sm_count = 148;
 u64 g_launches = 0;
+thread_local cudaStream_t g_alloc_stream = 0;
+bool g_profile = getenv("EXS_PROFILE") != nullptr;
+std::vector<ProfRec> g_prof;
+static std::string g_prof_text;
+
+// size-exact block cache (see exs_par.cuh); keyed per stream so handles on
+// different streams never share a block
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<std::pair<cudaStream_t, size_t>, void*> free_;
+  std::map<void*, std::pair<cudaStream_t, size_t>> live;
+  size_t cached = 0;
+};
+static BlockCache g_cache;
+
+void* cache_alloc(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  std::lock_guard<std::mutex> g(g_cache.mu);
+  auto it = g_cache.free_.find({g_alloc_stream, bytes});
+  void* p = nullptr;
+  if (it != g_cache.free_.end()) {
+    p = it->second;
+    g_cache.free_.erase(it);
+    g_cache.cached -= bytes;
+  } else {
+    cudaError_t e = cudaMallocAsync(&p, bytes, g_alloc_stream);
+    if (e != cudaSuccess) {
+      // release cached blocks of this stream and retry once
+      cudaGetLastError();
+      for (auto i = g_cache.free_.begin(); i != g_cache.free_.end();) {
+        if (i->first.first == g_alloc_stream) {
+          cudaFreeAsync(i->second, g_alloc_stream);
+          g_cache.cached -= i->first.second;
+          i = g_cache.free_.erase(i);
+        } else {
+          ++i;
+        }
+      }
+      cudaStreamSynchronize(g_alloc_stream);
+      CK(cudaMallocAsync(&p, bytes, g_alloc_stream));
+    }
+  }
+  g_cache.live[p] = {g_alloc_stream, bytes};
+  return p;
+}
+
+void cache_free(void* p) {
+  std::lock_guard<std::mutex> g(g_cache.mu);
+  auto it = g_cache.live.find(p);
+  if (it == g_cache.live.end()) { cudaFreeAsync(p, g_alloc_stream); return; }
+  g_cache.free_.insert({it->second, p});
+  g_cache.cached += it->second.second;
+  g_cache.live.erase(it);
+}
+
+// drop every cached block of a stream (handle destruction)
+static void cache_release(cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_cache.mu);
+  for (auto i = g_cache.free_.begin(); i != g_cache.free_.end();) {
+    if (i->first.first == s) {
+      cudaFreeAsync(i->second, s);
+      g_cache.cached -= i->first.second;
+      i = g_cache.free_.erase(i);
+    } else {
+      ++i;
+    }
+  }
+}
+
+// fold the recorded launch events into "site ms count" lines
+static void collect_profile() {
+  if (!g_profile) return;
+  cudaDeviceSynchronize();
+  std::vector<std::pair<std::string, std::pair<double, int>>> acc;
+  cudaEvent_t last_mark = nullptr;
+  std::string last_name;
+  for (auto& p : g_prof) {
+    float ms = 0;
+    std::string k;
+    if (p.line < 0) {  // a timeline mark: interval since the previous mark
+      if (last_mark) cudaEventElapsedTime(&ms, last_mark, p.a);
+      k = "[" + last_name + " .. " + std::to_string(-p.line) + "]";
+      last_name = std::string(p.fn) + ":" + std::to_string(-p.line);
+      if (last_mark) cudaEventDestroy(last_mark);
+      last_mark = p.a;
+      if (k == "[ .. " + std::to_string(-p.line) + "]") continue;
+    } else {
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+      k = std::string(p.fn) + ":" + std::to_string(p.line);
+    }
+    bool found = false;
+    for (auto& e : acc)
+      if (e.first == k) { e.second.first += ms; e.second.second++; found = true; break; }
+    if (!found) acc.push_back({k, {ms, 1}});
+  }
+  g_prof.clear();
+  g_prof_text.clear();
+  for (auto& e : acc) {
+    char b[256];
+    snprintf(b, sizeof b, "%-40s %9.3f ms x%d\n", e.first.c_str(), e.second.first, e.second.second);
+    g_prof_text += b;
+  }
+}
 #else
 u64 g_launches = 0;
 #endif
@@ -55,11 +161,24 @@ struct Handle {
   ~Handle() {
     reset();
     dfree(d_src_owned);
+    dfree(sc.p);
+    sc.p = nullptr;
+    sc.cap = 0;
 #ifndef EXS_EMU
-    if (st) cudaStreamDestroy(st);
+    cache_release(st);
+    if (st) { cudaStreamSynchronize(st); cudaStreamDestroy(st); }
 #endif
   }
 };
+
+inline void bind_stream(Handle& H) {
+#ifndef EXS_EMU
+  g_alloc_stream = H.st;
+  cudaSetDevice(H.device);
+#else
+  (void)H;
+#endif
+}
 
 struct Timer {
 #ifndef EXS_EMU
@@ -224,17 +343,21 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     B0.diags = H.d_diags; B0.n_diags = H.d_ndiags; B0.cap_diags = cap_diags; B0.dset = H.d_dset;
     B0.dmask = H.dmask; B0.overflow = ovf; B0.contract = H.d_contract;
 
+    prof_mark(st);
     Timer t0(st);
     run_lex(L, B0, H.sc, st);
     H.t_stage[0] = t0.stop();
+    prof_mark(st);
     Timer t1(st);
     run_parse(L, H.P, B0, H.sc, st);
     H.t_stage[1] = t1.stop();
+    prof_mark(st);
     Timer t2(st);
     run_sema(L, H.P, H.S, B0, H.sc, st);
     H.t_stage[2] = t2.stop();
     if (!cap_inst) cap_inst = (u32)std::min<u64>(std::max<u64>(65536, 4ull * H.S.NF + 1024), 0x7FFFFFFFull);
     H.W.cap_inst = cap_inst;
+    prof_mark(st);
     Timer t3(st);
     bool ok = run_walk(L, H.P, H.S, H.W, B0, H.sc, st, cap_diags);
     if (ok && (any_div || H.want_demands)) run_demands(H, any_div);
@@ -316,6 +439,9 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
   s.ms_lex = H.t_stage[0]; s.ms_parse = H.t_stage[1]; s.ms_sema = H.t_stage[2]; s.ms_walk = H.t_stage[3];
   s.ms_total = total.stop();
   s.gpu_launches = g_launches - launches0;
+#ifndef EXS_EMU
+  collect_profile();
+#endif
 }
 
 }  // namespace exs
@@ -353,6 +479,12 @@ int exs_create(int device, exs_handle* out) {
   g_sm_count = pr.multiProcessorCount;
   CK(cudaDeviceSetLimit(cudaLimitStackSize, 16384));
   CK(cudaStreamCreateWithFlags(&x->h.st, cudaStreamNonBlocking));
+  // keep freed pool memory cached across stages and runs (no cudaFree syncs)
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = ~0ull;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  g_alloc_stream = x->h.st;
 #endif
   *out = x;
   API_END
@@ -360,6 +492,7 @@ int exs_create(int device, exs_handle* out) {
 
 int exs_destroy(exs_handle h) {
   API_TRY
+  bind_stream(h->h);
   delete h;
   API_END
 }
@@ -368,6 +501,7 @@ int exs_run(exs_handle x, const uint8_t* bytes, uint64_t n_bytes, const uint64_t
             uint32_t n_files, const uint8_t* file_cfg) {
   API_TRY
   Handle& H = x->h;
+  bind_stream(H);
 #ifndef EXS_EMU
   CK(cudaSetDevice(H.device));
 #endif
@@ -389,6 +523,7 @@ int exs_run_device(exs_handle x, const uint8_t* d_bytes, uint64_t n_bytes, const
                    uint32_t n_files, const uint8_t* file_cfg) {
   API_TRY
   Handle& H = x->h;
+  bind_stream(H);
 #ifndef EXS_EMU
   CK(cudaSetDevice(H.device));
 #endif
@@ -410,6 +545,14 @@ int exs_set_option(exs_handle x, int key, int value) {
   API_END
 }
 
+const char* exs_profile_text(void) {
+#ifndef EXS_EMU
+  return g_prof_text.c_str();
+#else
+  return "";
+#endif
+}
+
 int exs_stage_times(exs_handle x, float* out4) {
   API_TRY
   for (int i = 0; i < 4; i++) out4[i] = x->h.t_stage[i];
@@ -428,6 +571,7 @@ int exs_get_diags(exs_handle x, exs_diag* out, uint64_t cap, uint64_t* n) {
 int exs_get_arena(exs_handle x, uint8_t* out, uint64_t cap, uint64_t* n) {
   API_TRY
   Handle& H = x->h;
+  bind_stream(H);
   u32 top = H.L.arena_top ? get1(H.L.arena_top, H.st) : 0;
   top = std::min(top, H.L.arena_cap);
   *n = top;
@@ -439,6 +583,7 @@ int exs_get_arena(exs_handle x, uint8_t* out, uint64_t cap, uint64_t* n) {
 int exs_get_pass_status(exs_handle x, exs_pass_status* out, uint64_t cap) {
   API_TRY
   Handle& H = x->h;
+  bind_stream(H);
   u32 F = H.L.F;
   std::vector<FP> fp(2 * F);
   std::vector<u32> lno(H.L.L + 1), lec(H.L.L + 1);
@@ -466,6 +611,7 @@ int exs_get_pass_status(exs_handle x, exs_pass_status* out, uint64_t cap) {
 int exs_get_tokens(exs_handle x, uint32_t file, exs_token* out, uint64_t cap, uint64_t* n) {
   API_TRY
   Handle& H = x->h;
+  bind_stream(H);
   if (file >= H.L.F) throw Err("file index out of range");
   u32 fl[2], lt[2];
   d2h(fl, H.L.fline + file, 8, H.st);
@@ -483,6 +629,7 @@ int exs_get_tokens(exs_handle x, uint32_t file, exs_token* out, uint64_t cap, ui
 int exs_get_walk_stats(exs_handle x, exs_walk_stats* out, uint64_t cap) {
   API_TRY
   Handle& H = x->h;
+  bind_stream(H);
   u32 F = H.L.F;
   std::vector<FP> fp(2 * F);
   if (F) d2h(fp.data(), H.L.fp, sizeof(FP) * 2 * F, H.st);
@@ -499,6 +646,7 @@ int exs_get_walk_stats(exs_handle x, exs_walk_stats* out, uint64_t cap) {
 int exs_describe(exs_handle x, const uint32_t* ids, const uint8_t* kinds, uint32_t n, exs_desc* out) {
   API_TRY
   Handle& H = x->h;
+  bind_stream(H);
   if (!n) return 0;
   u32* d_ids = dalloc<u32>(n);
   u8* d_k = dalloc<u8>(n);

@@ -23,6 +23,10 @@
 #define EXS_D __host__
 #endif
 
+#ifdef EXS_EMU
+#define EXS_TAG(name) ((void)0)
+#endif
+
 typedef uint8_t u8;
 typedef uint16_t u16;
 typedef uint32_t u32;

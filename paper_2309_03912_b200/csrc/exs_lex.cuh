@@ -78,10 +78,24 @@ struct Blanker {
   u8 pend;     // a second blank of a 2-char comment token is pending
   u32 pend_pos;
 
+  bool nospl;  // no spliced byte in [lo, hi): skip the bitmap on every character
+
   EXS_HD void init(const u8* s, const u32* sp, u32 lo, u32 hi_, u8 start_state) {
     src = s; splice = sp; p = lo; hi = hi_; st = start_state; pend = 0; pend_pos = 0;
+    u32 any = 0;
+    if (hi > lo) {
+      u32 w0 = lo >> 5, w1 = (hi - 1) >> 5;
+      for (u32 w = w0; w <= w1 && !any; w++) {
+        u32 m = sp[w];
+        if (w == w0) m &= ~0u << (lo & 31);
+        if (w == w1) m &= (~0u) >> (31 - ((hi - 1) & 31));
+        any |= m;
+      }
+    }
+    nospl = any == 0;
   }
   EXS_HD u32 next_logical(u32 q) const {
+    if (nospl) return q < hi ? q : hi;
     while (q < hi && bit_get(splice, q)) q++;
     return q;
   }
@@ -152,6 +166,35 @@ EXS_HD inline u8 line_fsm_map(const u8* s, const u32* sp, u32 lo, u32 hi) {
 __constant__ char kVocabDev[] = EXS_VOCAB_TEXT;
 #endif
 static const char kVocabHost[] = EXS_VOCAB_TEXT;
+
+// compile-time FNV-1a of a vocabulary word (same function the lexer streams)
+constexpr u64 fnv_c(const char* s, u64 h = 1469598103934665603ull) {
+  return *s ? fnv_c(s + 1, (h ^ (u8)*s) * 1099511628211ull) : h;
+}
+constexpr u32 len_c(const char* s) { return *s ? 1 + len_c(s + 1) : 0; }
+
+// Vocabulary id from the token's text hash and length: a switch over
+// compile-time constants (no table walk, no divergent constant-memory reads).
+EXS_HD inline u8 vocab_hash(u64 hv, u32 len) {
+#define EXS_W(str, id) case fnv_c(str): return len == len_c(str) ? (u8)(id) : (u8)0;
+  switch (hv) {
+    EXS_W("struct", W_STRUCT) EXS_W("class", W_CLASS) EXS_W("enum", W_ENUM)
+    EXS_W("template", W_TEMPLATE) EXS_W("typename", W_TYPENAME) EXS_W("requires", W_REQUIRES)
+    EXS_W("return", W_RETURN) EXS_W("if", W_IF) EXS_W("else", W_ELSE) EXS_W("for", W_FOR)
+    EXS_W("void", W_VOID) EXS_W("int", W_INT) EXS_W("bool", W_BOOL) EXS_W("true", W_TRUE)
+    EXS_W("false", W_FALSE) EXS_W("constexpr", W_CONSTEXPR) EXS_W("static", W_STATIC)
+    EXS_W("static_assert", W_STATIC_ASSERT) EXS_W("HDC", W_HDC) EXS_W("__host__", W_HOST)
+    EXS_W("__device__", W_DEVICE) EXS_W("__global__", W_GLOBAL) EXS_W("main", W_MAIN)
+    EXS_W("cuda_arch", W_CUDA_ARCH) EXS_W("hdc", W_HDC_TRAIT) EXS_W("std", W_STD)
+    EXS_W("Hst", W_HST) EXS_W("Dev", W_DEV) EXS_W("HstDev", W_HSTDEV) EXS_W("printf", W_PRINTF)
+    EXS_W("release_assert", W_RELEASE_ASSERT) EXS_W("__trap", W_TRAP) EXS_W("abort", W_ABORT)
+    EXS_W("cudaDeviceSynchronize", W_CUDASYNC) EXS_W("hd_warning_disable", W_HD_WARNING_DISABLE)
+    EXS_W("nv_exec_check_disable", W_NV_EXEC_CHECK_DISABLE) EXS_W("!", W_BANG_STR)
+    EXS_W("(", W_LPAREN_STR)
+    default: return W_NONE;
+  }
+#undef EXS_W
+}
 
 EXS_HD inline u8 vocab_lookup(const u8* t, u32 len) {
   if (len == 0 || len > 24) return W_NONE;
@@ -331,6 +374,22 @@ EXS_HD inline LineInfo scan_line_directive(const u8* s, const u32* sp, u32 lo, u
 // *err (M_LEX_*), *err_col, *err_pos and stops.
 struct LexErr { u16 msg; u32 col, pos; };
 
+// Writes a token built in registers with two 16-byte stores at scope exit.
+struct TokStore {
+  Tok* dst;
+  const Tok* src;
+  EXS_HD ~TokStore() {
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    d[0] = s[0];
+    d[1] = s[1];
+#else
+    *dst = *src;
+#endif
+  }
+};
+
 EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u32 line_no,
                            u32 file, u8 mask, Tok* out, LexErr* err) {
   Blanker b;
@@ -375,9 +434,10 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
         return n;
       }
       if (out) {
-        Tok& t = out[n];
+        Tok t;
+        TokStore ts_{out + n, &t};
         t.pos = name_pos; t.end = name_end; t.line = line_no; t.col = tcol; t.hv = h;
-        t.kind = TK_PRAGMA; t.id = nl <= 24 ? vocab_lookup(nb, nl) : 0; t.mask = mask; t.flags = 0; t.file = file;
+        t.kind = TK_PRAGMA; t.id = vocab_hash(h, nl); t.mask = mask; t.flags = 0; t.file = file;
       }
       n++;
       col += consumed;
@@ -404,10 +464,11 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
         return n;
       }
       if (out) {
-        Tok& t = out[n];
+        Tok t;
+        TokStore ts_{out + n, &t};
         t.pos = cstart == NONE ? pos : cstart; t.end = cstart == NONE ? pos : cend;
         t.line = line_no; t.col = tcol; t.hv = h;
-        t.kind = TK_STRING; t.id = nl <= 24 ? vocab_lookup(nb, nl) : 0; t.mask = mask; t.flags = 0; t.file = file;
+        t.kind = TK_STRING; t.id = vocab_hash(h, nl); t.mask = mask; t.flags = 0; t.file = file;
       }
       n++;
       col += cw;
@@ -438,11 +499,12 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
         have = b.next(c, pos, w);
       }
       if (out) {
-        Tok& t = out[n];
+        Tok t;
+        TokStore ts_{out + n, &t};
         t.pos = tpos; t.end = last + 1; t.line = line_no; t.col = tcol;
         t.hv = digits ? val : h;
         t.kind = digits ? TK_INT : TK_IDENT;
-        t.id = digits ? 0 : vocab_lookup(nb, nl);
+        t.id = digits ? 0 : vocab_hash(h, nl);
         t.mask = mask; t.flags = (ovf ? TF_INT_OVERFLOW : 0) | (spl ? TF_HAS_SPLICE : 0); t.file = file;
       }
       n++;
@@ -490,7 +552,8 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
       }
       u32 endp = plen == 1 ? tpos + 1 : (plen == 2 ? p1 + 1 : p2 + 1);
       if (out) {
-        Tok& t = out[n];
+        Tok t;
+        TokStore ts_{out + n, &t};
         t.pos = tpos; t.end = endp; t.line = line_no; t.col = tcol; t.hv = 0;
         t.kind = TK_PUNCT; t.id = pid; t.mask = mask; t.flags = 0; t.file = file;
       }

@@ -132,6 +132,8 @@ extern u64 g_launches;
 struct ProfRec { const char* fn; int line; cudaEvent_t a, b; };
 extern bool g_profile;
 extern std::vector<ProfRec> g_prof;
+extern thread_local const char* g_tag;  // name of the next launch (EXS_TAG)
+#define EXS_TAG(name) (::exs::g_tag = (name))
 #endif
 
 template <class F>
@@ -142,7 +144,8 @@ void par_for(i64 n, F f, cudaStream_t s, int block = 256, const char* fn = __bui
   i64 want = (n + block - 1) / block;
   i64 cap = (i64)g_sm_count * 16;
   int grid = (int)(want < cap ? want : cap);
-  ProfRec pr{fn, line, nullptr, nullptr};
+  ProfRec pr{g_tag ? g_tag : fn, g_tag ? 0 : line, nullptr, nullptr};
+  g_tag = nullptr;
   if (g_profile) {
     cudaEventCreate(&pr.a); cudaEventCreate(&pr.b);
     cudaEventRecord(pr.a, s);
@@ -167,7 +170,8 @@ void par_for_walk(i64 n, F f, cudaStream_t s, const char* fn = __builtin_FUNCTIO
   i64 want = (n + 127) / 128;
   i64 cap = (i64)g_sm_count * 64;
   int grid = (int)(want < cap ? want : cap);
-  ProfRec pr{fn, line, nullptr, nullptr};
+  ProfRec pr{g_tag ? g_tag : fn, g_tag ? 0 : line, nullptr, nullptr};
+  g_tag = nullptr;
   if (g_profile) {
     cudaEventCreate(&pr.a); cudaEventCreate(&pr.b);
     cudaEventRecord(pr.a, s);

@@ -54,14 +54,16 @@ struct Parser {
   }
 
   // ------------------------------------------------------------ tokens
-  EXS_HD u32 gtok(u32 i) const { return i < v.n ? v.vtok[v.vbase + i] : NONE; }
+  // view position -> global token index
+  EXS_HD u32 tix(u32 i) const { return v.vtok[v.vbase + i]; }
+  EXS_HD u32 gtok(u32 i) const { return i < v.n ? tix(i) : NONE; }
   EXS_HD u8 kind(u32 k = 0) const {
     u32 i = pos + k;
-    return i < v.n ? v.toks[v.vtok[v.vbase + i]].kind : (u8)TK_EOF;
+    return i < v.n ? v.toks[tix(i)].kind : (u8)TK_EOF;
   }
   EXS_HD u8 tid(u32 k = 0) const {
     u32 i = pos + k;
-    return i < v.n ? v.toks[v.vtok[v.vbase + i]].id : (u8)0;
+    return i < v.n ? v.toks[tix(i)].id : (u8)0;
   }
   // at(text): kind in (ident, punct) and text equal (parser.py:67-69)
   EXS_HD bool at_w(u8 w, u32 k = 0) const { return kind(k) == TK_IDENT && tid(k) == w; }
@@ -75,12 +77,12 @@ struct Parser {
     return g;
   }
   EXS_HD void loc_of(u32 i, u32& line, u32& col) const {
-    if (i < v.n) { const Tok& t = v.toks[v.vtok[v.vbase + i]]; line = t.line; col = t.col; }
+    if (i < v.n) { const Tok& t = v.toks[tix(i)]; line = t.line; col = t.col; }
     else { line = v.eof_line; col = v.eof_col; }
   }
   EXS_HD u64 span_of(u32 i) const {
     if (i >= v.n) return SPAN_EOF;
-    const Tok& t = v.toks[v.vtok[v.vbase + i]];
+    const Tok& t = v.toks[tix(i)];
     return ((u64)t.pos << 32) | (u64)(t.end - t.pos);
   }
 

@@ -12,11 +12,13 @@ namespace exs {
 enum { ST_OK = 0, ST_SUBST = 1, ST_SEMA = 2 };
 enum { V_NONE = 0, V_TYPE, V_HDC, V_BOOL, V_INT };
 // builtin type name hashes are FNV of the words (lexer computes the same)
-EXS_HD inline u64 word_hash(const char* w) {
-  u64 h = fnv_init();
-  while (*w) h = fnv_step(h, (u8)*w++);
+EXS_HD constexpr inline u64 word_hash(const char* w) {
+  u64 h = 1469598103934665603ull;
+  while (*w) h = (h ^ (u8)*w++) * 1099511628211ull;
   return h;
 }
+constexpr u64 H_INT = word_hash("int"), H_BOOL = word_hash("bool"), H_HDC_MEMBER = word_hash("hdc"),
+              H_STD = word_hash("std::");
 
 struct Val {
   u8 k;      // V_*

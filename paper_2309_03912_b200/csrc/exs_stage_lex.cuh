@@ -107,6 +107,7 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
     SrcView v{S.src, S.splice, S.fstart, N};
     u32* sp = S.splice;
     const u8* s = S.src;
+    EXS_TAG("lex_splice");
     par_for(W, [=] EXS_HD (i64 w) {
       u32 bits = 0;
       u32 base = (u32)w * 32;
@@ -137,6 +138,7 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
   {
     const u32* ls = S.line_start; u32* lf = S.line_file; u32* lh = S.line_hi; u64* sc_in = S.line_scan;
     const u32* fo = S.foff; const u8* s = S.src; const u32* sp = S.splice;
+    EXS_TAG("lex_line_map");
     par_for(L, [=] EXS_HD (i64 i) {
       u32 lo = ls[i];
       u32 f = upper_file(fo, F, lo);
@@ -199,7 +201,8 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
     const u8* s = S.src; const u32* sp = S.splice; LineInfo* li = S.line_info;
     u8* ar = S.arena; u32* at = S.arena_top; u32 cap = S.arena_cap;
     u32* nt = S.line_ntok; u16* le = S.line_err; u32* lec = S.line_err_col; u32* lep = S.line_err_pos;
-    par_for(L + 1, [=] EXS_HD (i64 i) {
+    EXS_TAG("lex_directive_count");
+    par_for_walk(L + 1, [=] EXS_HD (i64 i) {
       if (i == L) { nt[i] = 0; return; }
       LineInfo x = scan_line_directive(s, sp, ls[i], lh[i], lst[i], ar, at, cap);
       li[i] = x;
@@ -325,7 +328,8 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
     const u32* lno = S.line_no; const u32* lf = S.line_file; const u8* lm = S.line_mask;
     const u8* s = S.src; const u32* sp = S.splice; const u32* lt = S.line_tok; Tok* tk = S.toks;
     const u16* le = S.line_err; const u32* nt = S.line_ntok; FP* fp = S.fp;
-    par_for(L, [=] EXS_HD (i64 i) {
+    EXS_TAG("lex_emit");
+    par_for_walk(L, [=] EXS_HD (i64 i) {
       if (!nt[i] && !le[i]) return;
       u8 m = lm[i];
       LexErr e;

@@ -10,6 +10,7 @@ namespace exs {
 struct ParseState {
   u32 V = 0, VT = 0, I = 0, FI = 0;
   u32* vbase = nullptr;   // V+1
+  u32* vdirect = nullptr; // first token when the view is the file's whole token range
   u32* vfile = nullptr;
   u8* vpass = nullptr;    // passes served (bit0 host, bit1 device)
   u32* veof = nullptr;    // 2V (line, col)
@@ -31,7 +32,7 @@ struct ParseState {
   void free_all() {
     void* ps[] = {vbase, vfile, vpass, veof, vtok, vview, item_start, item_view, item_root,
                   item_end, item_stat, item_err, vfirst, vbad, vstat, vfb_base, vfb_cnt,
-                  fb_items, vfi, fitems, fitem_view, nodes};
+                  fb_items, vfi, fitems, fitem_view, nodes, vdirect};
     for (void* p : ps) dfree(p);
   }
 };
@@ -73,6 +74,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   P.vfile = dalloc<u32>(V + 1);
   P.vpass = dalloc<u8>(V + 1);
   P.veof = dalloc<u32>(2 * (size_t)V + 2);
+  P.vdirect = dalloc<u32>(V + 1);
   u32* vcnt = dalloc<u32>(V + 1);
   // token pass flags and their scans
   u32* s0 = dalloc<u32>(T + 1);
@@ -94,7 +96,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   }
   {
     FP* fp = L.fp; const u8* cf = L.cfg; const u32* fl = L.fline; const u32* lt = L.line_tok;
-    u32* vf = P.vfile; u8* vp = P.vpass; u32* ve = P.veof;
+    u32* vf = P.vfile; u8* vp = P.vpass; u32* ve = P.veof; u32* vd = P.vdirect;
     par_for(F, [=] EXS_HD (i64 f) {
       u32 v = fvb[f];
       u32 c = fvc[f];
@@ -107,6 +109,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
         fp[2 * f].view = v; fp[2 * f + 1].view = v;
         ve[2 * v] = fp[2 * f].eof_line; ve[2 * v + 1] = fp[2 * f].eof_col;
         vcnt[v] = s0[tf1] - s0[tf0];
+        vd[v] = vcnt[v] == tf1 - tf0 ? tf0 : NONE;
         return;
       }
       for (u32 p = 0; p < 2; p++) {
@@ -116,6 +119,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
         fp[2 * f + p].view = v;
         ve[2 * v] = fp[2 * f + p].eof_line; ve[2 * v + 1] = fp[2 * f + p].eof_col;
         vcnt[v] = p ? (s1[tf1] - s1[tf0]) : (s0[tf1] - s0[tf0]);
+        vd[v] = vcnt[v] == tf1 - tf0 ? tf0 : NONE;
         v++;
       }
     }, st);
@@ -211,11 +215,13 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   // 4. item-parallel parse
   {
     const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase; const u32* ve = P.veof;
+    const u32* vdr = P.vdirect;
     const u32* is = P.item_start; const u32* iv = P.item_view; const u32* vf = P.vfile;
     const u8* cf = L.cfg; const u8* s = L.src; const u32* sp = L.splice;
     Node* nd = P.nodes; u32* ir = P.item_root; u32* ie = P.item_end; u8* ist = P.item_stat;
     PErr* ier = P.item_err; u32* vbad = P.vbad;
-    par_for(I, [=] EXS_HD (i64 j) {
+    EXS_TAG("parse_items");
+    par_for_walk(I, [=] EXS_HD (i64 j) {
       u32 v = iv[j];
       u32 next = (j + 1 < I && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
       u8 c = cf[vf[v]];
@@ -280,6 +286,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     u32* fbl = dalloc<u32>(nfb);
     h2d(fbl, fb_views.data(), nfb * 4, st);
     const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase; const u32* ve = P.veof;
+    const u32* vdr = P.vdirect;
     const u32* is = P.item_start; const u32* vfst = P.vfirst; const u32* vf = P.vfile;
     const u8* cf = L.cfg; const u8* s = L.src; const u32* sp = L.splice; Node* nd = P.nodes;
     u32* fbi = P.fb_items; u32* fbase = P.vfb_base; u32* fcnt = P.vfb_cnt; u8* vs = P.vstat;

@@ -297,6 +297,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
   {
     FnRec* fr = S.fns; const RecRec* rr = S.recs; const Node* nd = P.nodes; const Tok* tk = L.toks;
     const u8* s = L.src; const u32* sp = L.splice; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
+    EXS_TAG("sema_sig_hash");
     par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
       u32 owner_tok = NONE;
@@ -399,7 +400,8 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       }
     }, st);
     FnRec* fr = S.fns;
-    par_for(NF, [=] EXS_HD (i64 i) {
+    EXS_TAG("sema_bodyscan");
+    par_for_walk(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
       if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) return;  // not in the struct any more
       u8 c = cfgs[vf[r.view]];

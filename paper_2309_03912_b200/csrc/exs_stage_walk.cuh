@@ -150,6 +150,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     const FnRec* fr = S.fns; const RecRec* rr = S.recs; const Node* nd = P.nodes; const Tok* tk = L.toks;
     const FP* fp = L.fp; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
     const Tables* tab = dtab;
+    EXS_TAG("walk_roots");
     par_for_walk(2ull * NF, [=] EXS_HD (i64 x) {
       u32 i = (u32)(x >> 1), p = (u32)(x & 1);
       const FnRec& r = fr[i];
@@ -291,6 +292,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       u32* ct = B.contract;
       const u32* sn = S.stmt_node; const u32* scs = S.stmt_cs;
       const u32 nfc = nf;
+      EXS_TAG("walk_chunks");
       par_for_walk(nwi, [=] EXS_HD (i64 i) {
         u32 lo = 0, hi = nfc;  // instance j with wb[j] <= i < wb[j+1]
         while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (wb[mid] <= (u32)i) lo = mid; else hi = mid; }
@@ -379,6 +381,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     while (nq) {
       dzero(qn + 1, 4, st);
       const u32* qa = q0; u32* qb = q1;
+      EXS_TAG("walk_reach");
       par_for(nq, [=] EXS_D (i64 j) {
         const Inst& I = in[qa[j]];
         u8 native = (u8)(I.walk & 1);
@@ -414,6 +417,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     const Pending* pd = W.pend; const Inst* in = W.inst; const u8* vis = W.visited;
     const FnRec* fr = S.fns; const Node* nd = P.nodes; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
     WalkBufs Bc = B;
+    EXS_TAG("walk_pending");
     par_for(cnt[1], [=] EXS_HD (i64 j) {
       const Pending& p = pd[j];
       const Inst& I = in[p.caller];

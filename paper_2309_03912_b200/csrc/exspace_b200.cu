@@ -18,6 +18,7 @@ u64 g_launches = 0;
 thread_local cudaStream_t g_alloc_stream = 0;
 bool g_profile = getenv("EXS_PROFILE") != nullptr;
 std::vector<ProfRec> g_prof;
+thread_local const char* g_tag = nullptr;
 static std::string g_prof_text;
 
 // size-exact block cache (see exs_par.cuh); keyed per stream so handles on
@@ -105,7 +106,7 @@ static void collect_profile() {
       cudaEventElapsedTime(&ms, p.a, p.b);
       cudaEventDestroy(p.a);
       cudaEventDestroy(p.b);
-      k = std::string(p.fn) + ":" + std::to_string(p.line);
+      k = p.line ? std::string(p.fn) + ":" + std::to_string(p.line) : std::string(p.fn);
     }
     bool found = false;
     for (auto& e : acc)
@@ -541,6 +542,9 @@ int exs_get_stats(exs_handle x, exs_stats* out) {
 int exs_set_option(exs_handle x, int key, int value) {
   API_TRY
   if (key == 1) x->h.want_demands = value != 0;
+#ifndef EXS_EMU
+  else if (key == 2) g_profile = value != 0;  // per-launch device timing of later runs
+#endif
   else throw Err("unknown option");
   API_END
 }

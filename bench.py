@@ -158,8 +158,8 @@ def run_reference_arm(a, rank, world):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    # bounded sample: ~2 files per core of the same C2 shape, per step
-    n = max(cores * 2, 8)
+    # bounded sample: ~8 files per core of the same C2 shape per step (~5 s)
+    n = max(cores * 8, 32)
     vals = []
     for i in range(a.warmup + a.steps):
         r = cpu_reference(n, a.file_bytes, 10_000 + i * n, cores)
@@ -222,9 +222,18 @@ def run_gpu_arm(a, rank, world, local):
         dist.barrier()
     torch.cuda.synchronize()
     steps = []
+    kern = {}  # tag -> [total ms, launches] over the timed steps (CUDA events, library stream)
+    h.set_option(2, 1)
     with ClockSampler(local) as clk:
         for _ in range(a.steps):
             steps.append(run_resident())
+            for ln in h.lib.exs_profile_text().decode().splitlines():
+                parts = ln.split()
+                if len(parts) >= 4 and not parts[0].startswith("[") and ":" not in parts[0]:
+                    k = kern.setdefault(parts[0], [0.0, 0])
+                    k[0] += float(parts[1])
+                    k[1] += int(parts[3].lstrip("x"))
+    h.set_option(2, 0)
     torch.cuda.synchronize()
     ms = [s["ms_total"] for s in steps]
     lex_ms = [s["ms_lex"] for s in steps]
@@ -248,6 +257,28 @@ def run_gpu_arm(a, rank, world, local):
     # roofline: the lexing stage (K1-K3): source read once + token records written
     lex_bytes = nbytes + 32 * st["tokens"]
     lex_ach = lex_bytes / (statistics.mean(lex_ms) / 1e3) / 1e9
+    # per-kernel algorithmic bytes: per step
+    algo = {
+        "lex_emit": nbytes + 32 * st["tokens"],             # source read + token records
+        "lex_directive_count": nbytes + 40 * st["tokens"] // 8,
+        "walk_chunks": 48 * st["callsites"],                 # 48 B per edge
+        "walk_roots": 48 * st["functions"],
+        "parse_items": 32 * st["tokens"] + 24 * st["tokens"] // 2,
+    }
+    per_kernel = {}
+    for tag, (ms_tot, n) in kern.items():
+        ms_step = ms_tot / max(1, a.steps)
+        ent = {"ms_per_step": ms_step, "launches_per_step": n / max(1, a.steps),
+               "share": ms_step / mean_ms}
+        if tag in algo and ms_step > 0:
+            ent["achieved_gbs"] = algo[tag] / (ms_step / 1e3) / 1e9
+            ent["frac"] = ent["achieved_gbs"] / HBM_PEAK
+        per_kernel[tag] = ent
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_per_step"]) if per_kernel else None
+    traffic_db = {}
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic_db = json.loads(tf.read_text())
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak",
@@ -261,16 +292,22 @@ def run_gpu_arm(a, rank, world, local):
                                      "diagnostics", "retries")},
         "stage_ms": {k: statistics.mean(s[k] for s in steps) for k in ("ms_lex", "ms_parse", "ms_sema", "ms_walk")},
         "gpu_launches": int(sum(s["gpu_launches"] for s in steps)),
-        "roofline": {"bound": "hbm", "achieved": lex_ach, "peak": HBM_PEAK, "unit": "GB/s",
-                     "frac": lex_ach / HBM_PEAK, "traffic": None,
-                     "kernel": "lex stage (K1-K3)", "peak_source": HBM_PEAK_SRC},
+        "roofline": ({"bound": "hbm", "achieved": per_kernel[dom].get("achieved_gbs"),
+                      "peak": HBM_PEAK, "unit": "GB/s", "frac": per_kernel[dom].get("frac"),
+                      "traffic": traffic_db.get(dom, {}).get("dram_bytes_per_step"),
+                      "algorithmic_bytes": algo.get(dom), "kernel": dom,
+                      "share_of_step": per_kernel[dom]["share"], "peak_source": HBM_PEAK_SRC}
+                     if dom else None),
+        "roofline_lex_stage": {"bound": "hbm", "achieved": lex_ach, "peak": HBM_PEAK, "unit": "GB/s",
+                               "frac": lex_ach / HBM_PEAK, "kernel": "lex stage K1-K3 (all launches)"},
+        "kernels": per_kernel,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": int(nbytes),
                 "d2h_bytes_per_step": int(d2h_b)},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        r = cpu_reference(max(cores * 2, 8), a.file_bytes, 50_000, cores)
+        r = cpu_reference(max(cores * 16, 64), a.file_bytes, 50_000, cores)
         line["cpu_baseline"] = {"value": r["gbs"], "unit": "GB/s", "cores": cores, "kind": "port",
                                 "sample": f"{r['files']} C2 files ({r['bytes'] / 1e6:.1f} MB), "
                                           f"oracle/exs_oracle.py on {cores} processes, {r['seconds']:.1f} s"}

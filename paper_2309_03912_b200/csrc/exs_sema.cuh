@@ -429,13 +429,16 @@ struct Sema {
         }
       }
     }
+    // the candidate env is materialised only when a default or the requires
+    // clause is evaluated; the full env only when an argument type is known
     Env mv_env, cenv;
-    cand_env(b, orec, obinds, cenv, mv_env);
+    bool have_cenv = false;
     for (u32 tp = fn.c0; tp != NONE; tp = N(tp).next) {
       u64 tn = K(N(tp).tok).hv;
       Val dummy;
       if (b.get(tn, dummy)) continue;
       if (N(tp).sub == 1 && N(tp).c0 != NONE) {
+        if (!have_cenv) { cand_env(b, orec, obinds, cenv, mv_env); have_cenv = true; }
         Val v;
         u8 st = eval(N(tp).c0, cenv, fund, v);
         if (st != ST_OK) return st;
@@ -446,21 +449,26 @@ struct Sema {
         return subst(SF_OTHER);
       }
     }
-    Env full = obinds;
-    full.nbase = full.n;
-    for (int i = 0; i < b.n; i++) full.add(b.names[i], b.vals[i]);
-    full.nbase = full.n;
-    u32 i = 0;
-    for (u32 p = fn.c1; p != NONE; p = N(p).next, i++) {
-      if (argtys[i].k == V_NONE) continue;
-      Val want;
-      u8 st = type_of(N(p).c0, full, want);
-      if (contract) return ST_SUBST;
-      if (st != ST_OK) return subst(SF_OTHER);
-      if (!val_eq(want, argtys[i])) return subst(SF_OTHER);
+    bool any_arg = false;
+    for (u32 i = 0; i < nargs; i++) any_arg |= argtys[i].k != V_NONE;
+    if (any_arg) {
+      Env full = obinds;
+      full.nbase = full.n;
+      for (int i = 0; i < b.n; i++) full.add(b.names[i], b.vals[i]);
+      full.nbase = full.n;
+      u32 i = 0;
+      for (u32 p = fn.c1; p != NONE; p = N(p).next, i++) {
+        if (argtys[i].k == V_NONE) continue;
+        Val want;
+        u8 st = type_of(N(p).c0, full, want);
+        if (contract) return ST_SUBST;
+        if (st != ST_OK) return subst(SF_OTHER);
+        if (!val_eq(want, argtys[i])) return subst(SF_OTHER);
+      }
     }
     u32 req = N(fr.node + 1).c0;
     if (req != NONE) {
+      if (!have_cenv) { cand_env(b, orec, obinds, cenv, mv_env); have_cenv = true; }
       Val ok;
       u8 st = eval(req, cenv, fund, ok);
       if (st != ST_OK) return st;
@@ -490,13 +498,24 @@ struct Sema {
   }
 
   // effective_spaces (sema.py:670-703): returns 1=H 2=D 3=HD 4=GLOBAL, or error status
-  EXS_HD u8 spaces(u32 fi, const Env& merged, u8 side, u32 at_tok, u32 orec, u8& out) {
+  // merged = owner bindings + (tb, hb) bound to the decl's template params; it
+  // is only materialised for conditional specifiers under proposal1
+  EXS_HD u8 spaces(u32 fi, const Env* obinds, const Val& tb, const Val& hb, u8 side, u32 at_tok,
+                   u32 orec, u8& out) {
     const FnRec& fr = T->fns[fi];
     const Node& fn = N(fr.node);
     u16 fl = fn.n;
     if (fl & FF_G) { out = 4; return ST_OK; }
     bool cond = (fl & (FF_HPRED | FF_DPRED)) != 0;
     if (mode == MODE_P1 && cond) {
+      Env merged;
+      if (obinds) merged = *obinds; else merged.clear();
+      merged.nbase = merged.n;
+      for (u32 tp = fn.c0; tp != NONE; tp = N(tp).next) {
+        const Val& v = N(tp).sub == 0 ? tb : hb;
+        if (v.k != V_NONE) merged.add(K(N(tp).tok).hv, v);
+      }
+      merged.nbase = merged.n;
       Env mv_env = merged, env = merged;
       env.nbase = env.n;
       env.mv_rec = orec;

@@ -73,10 +73,8 @@ EXS_HD inline void walker_for(Walker& w, const WalkCfg& C, const WalkBufs& B, u3
   w.ebase = I.ebase;
   w.ecnt = 0;
   w.contract = false;
-  w.orec_self = I.orec;
   w.env.clear();
   if (I.orec != NONE && I.ot.k == V_TYPE) w.S.struct_env(I.orec, I.ot, w.env);
-  w.obinds_self = w.env;
   w.env.nbase = w.env.n;
   w.add_binds(fn, I.tb, I.hb, w.env);
   w.env.nbase = w.env.n;
@@ -189,7 +187,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       else {
         u8 sp;
         w.S.depth = 0;
-        u8 stt = w.S.spaces(i, none, 0, fn.tok, r.rec, sp);
+        u8 stt = w.S.spaces(i, nullptr, vnone(), vnone(), 0, fn.tok, r.rec, sp);
         if (w.S.contract) { at_or(&B.contract[file], 1); return; }
         if (stt == ST_SEMA) { w.emit_err(); return; }
         if (stt == ST_SUBST) { w.emit_tok(C_E0001, fn.tok, M_W_PRED_CONST); return; }

@@ -175,9 +175,10 @@ EXS_HD inline bool hard_code(u16 c) {
          c == C_E0104 || c == C_E1301 || c == C_E1302;
 }
 
-#define MAX_LOCALS 32
+// per-thread bounds; a unit beyond them is reported as out of contract (X9999)
+#define MAX_LOCALS 16
 #define MAX_WALK_DEPTH 160
-#define MAX_ARGS 48
+#define MAX_ARGS 16
 
 struct Walker {
   Sema S;
@@ -194,8 +195,6 @@ struct Walker {
   u32 stmt_cs_base, cs_ord;  // edge slot of the current statement, edges in it so far
   bool silent;               // replaying declarations of earlier chunks: no side effects
   Env env;                   // owner bindings + bindings
-  Env obinds_self;           // owner bindings of this instance
-  u32 orec_self;
   // locals (scoped dict)
   u32 nloc;
   u64 lname[MAX_LOCALS];
@@ -256,15 +255,10 @@ struct Walker {
   EXS_HD u32 instantiate(u32 fi, const Val& tb, const Val& hb, u8 want_side, u32 orec,
                          const Env& obinds, const Val& ot, u32 at_tok) {
     u32 my_local = (stmt_k << 12) | (stmt_ord++ & 0xFFFu);
-    // merged = owner bindings + bindings
-    Env merged = obinds;
-    merged.nbase = merged.n;
     const Node& fnn = N(T->fns[fi].node);
-    add_binds(fnn, tb, hb, merged);
-    merged.nbase = merged.n;
     u8 sp;
     S.depth = 0;
-    u8 st = S.spaces(fi, merged, want_side, at_tok, orec, sp);
+    u8 st = S.spaces(fi, &obinds, tb, hb, want_side, at_tok, orec, sp);
     if (S.contract) { contract = true; return NONE; }
     if (st == ST_SEMA) { emit_err(); return NONE; }
     if (st == ST_SUBST) { emit_tok(C_E0001, at_tok, M_W_PRED_CONST); return NONE; }
@@ -332,14 +326,10 @@ struct Walker {
   // _dispatch (spacecheck.py:554-596)
   EXS_HD void dispatch(u32 fi, const Val& tb, const Val& hb, u32 loc_tok, u32 orec,
                        const Env& obinds, const Val& ot) {
-    Env merged = obinds;
-    merged.nbase = merged.n;
     const Node& fnn = N(T->fns[fi].node);
-    add_binds(fnn, tb, hb, merged);
-    merged.nbase = merged.n;
     u8 sp;
     S.depth = 0;
-    u8 st = S.spaces(fi, merged, side, loc_tok, orec, sp);
+    u8 st = S.spaces(fi, &obinds, tb, hb, side, loc_tok, orec, sp);
     if (S.contract) { contract = true; return; }
     if (st == ST_SEMA) { emit_err(); return; }
     if (st == ST_SUBST) { emit_tok(C_E0001, loc_tok, M_W_PRED_CONST); return; }
@@ -369,7 +359,7 @@ struct Walker {
                      u32 name_targ = 0) {
     u32 nviable = 0;
     u32 vfi[8];
-    Val vtb[8], vhb[8];
+    Val ftb = vnone(), fhb = vnone();  // bindings of the first viable candidate
     u32 i = 0;
     u32 m = member ? N(T->recs[rec].node).c1 : NONE;
     while (true) {
@@ -398,33 +388,37 @@ struct Walker {
       if (S.contract) { contract = true; return false; }
       if (st == ST_SEMA) { emit_err(); return false; }
       if (st == ST_SUBST) continue;
-      if (nviable < 8) {
-        vfi[nviable] = fi;
-        // split bindings by tparam kind
-        Val tb = vnone(), hb = vnone();
-        const Node& fnn = N(T->fns[fi].node);
-        for (u32 tp = fnn.c0; tp != NONE; tp = N(tp).next) {
-          Val v;
-          if (b.get(K(N(tp).tok).hv, v)) {
-            if (N(tp).sub == 0) tb = v; else hb = v;
-          }
-        }
-        vtb[nviable] = tb; vhb[nviable] = hb;
-      }
+      if (nviable < 8) vfi[nviable] = fi;
+      if (nviable == 0) split_binds(fi, b, ftb, fhb);
       nviable++;
     }
+    u32 first_ok = nviable ? vfi[0] : NONE;
     if (S.mode == MODE_P2 && nviable > 1 && nviable <= 8) {
       u32 nc = 0;
       for (u32 j = 0; j < nviable; j++)
-        if (S.compatible(vfi[j], ctx_side, member ? rec : NONE)) {
-          vfi[nc] = vfi[j]; vtb[nc] = vtb[j]; vhb[nc] = vhb[j]; nc++;
-        }
+        if (S.compatible(vfi[j], ctx_side, member ? rec : NONE)) vfi[nc++] = vfi[j];
       if (nc) nviable = nc;
     }
     if (nviable == 0) { emit_tok(C_E1301, loc_tok, M_S_NO_VIABLE, name_a0, name_a1, 0, name_targ); return false; }
     if (nviable > 1) { emit_tok(C_E1302, loc_tok, M_S_AMBIGUOUS, name_a0, name_a1, nviable, name_targ); return false; }
-    out_fi = vfi[0]; out_tb = vtb[0]; out_hb = vhb[0];
+    out_fi = vfi[0];
+    if (out_fi == first_ok) { out_tb = ftb; out_hb = fhb; return true; }
+    // the space filter chose a later candidate: re-derive its bindings
+    Sema::Binds b;
+    S.depth = 0;
+    S.try_cand(out_fi, targs, argtys, nargs, env, member ? rec : NONE, obinds, b);
+    split_binds(out_fi, b, out_tb, out_hb);
     return true;
+  }
+  EXS_HD void split_binds(u32 fi, const Sema::Binds& b, Val& tb, Val& hb) const {
+    tb = vnone(); hb = vnone();
+    const Node& fnn = N(T->fns[fi].node);
+    for (u32 tp = fnn.c0; tp != NONE; tp = N(tp).next) {
+      Val v;
+      if (b.get(K(N(tp).tok).hv, v)) {
+        if (N(tp).sub == 0) tb = v; else hb = v;
+      }
+    }
   }
 
   // ------------------------------------------------------------- expressions

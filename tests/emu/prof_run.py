@@ -11,7 +11,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
 blobs, offs = bench.make_corpus(n, 100_000, 0, os.cpu_count())
 data = np.frombuffer(b"".join(blobs), np.uint8)
 cfg = np.zeros(n, np.uint8)
-h = _native.Handle(0)
+h = _native.Handle(0, os.environ.get("EXS_LIB"))
 for it in range(3):
     t0 = time.time(); h.run(data, offs, cfg); t1 = time.time()
 st = h.stats()

@@ -25,6 +25,16 @@
 
 #ifdef EXS_EMU
 #define EXS_TAG(name) ((void)0)
+#define EXS_FI inline
+#define EXS_NOINLINE
+#else
+// Stack discipline for the recursive walkers (local-memory traffic dominated
+// DRAM traffic, profiles/r01_*): keep the frames of the recursive functions
+// small by inlining only light steps into them (EXS_FI) and moving heavy,
+// non-recursive leaf work (overload selection, dispatch, instantiation) into
+// separate functions (EXS_NOINLINE) whose big frames exist only while they run.
+#define EXS_FI __forceinline__
+#define EXS_NOINLINE __noinline__
 #endif
 
 typedef uint8_t u8;

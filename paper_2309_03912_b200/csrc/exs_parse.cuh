@@ -659,7 +659,7 @@ struct Parser {
     depth--;
     return lhs;
   }
-  EXS_HD u32 conj() {
+  EXS_HD EXS_FI u32 conj() {
     u32 lhs = cmp();
     while (lhs != NONE && at_p(P_AND)) {
       u32 op = take();
@@ -672,7 +672,7 @@ struct Parser {
     }
     return lhs;
   }
-  EXS_HD u32 cmp() {
+  EXS_HD EXS_FI u32 cmp() {
     u32 lhs = unary();
     if (lhs == NONE) return NONE;
     if (at_p(P_EQ) || at_p(P_NE)) {
@@ -700,7 +700,7 @@ struct Parser {
     }
     return postfix();
   }
-  EXS_HD bool call_args(u32& out) {
+  EXS_HD EXS_FI bool call_args(u32& out) {
     ListB l;
     if (!at_p(P_RPAREN)) {
       while (true) {
@@ -714,7 +714,7 @@ struct Parser {
     out = l.head;
     return true;
   }
-  EXS_HD bool paren_args(u32& out, u32& count) {
+  EXS_HD EXS_FI bool paren_args(u32& out, u32& count) {
     if (!need_p(P_LPAREN, EX_LPAREN)) return false;
     if (!call_args(out)) return false;
     count = 0;

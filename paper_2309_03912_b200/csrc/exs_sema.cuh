@@ -298,7 +298,24 @@ struct Sema {
     depth--;
     return st;
   }
-  EXS_HD u8 eval_(u32 e, const Env& env, bool f, Val& out) {
+  // T::member constant (sema.py:431-442); out of line so eval's frame stays small
+  EXS_HD EXS_NOINLINE u8 eval_mconst(const Node& n, const Env& env, bool f, Val& out) {
+    Val t;
+    u8 st = type_of(n.c0, env, t);
+    if (st != ST_OK) return st;
+    if (t.rec == NONE) return subst(SF_NO_MEMBERS, type_name_arg(t));
+    u32 mv = first_mvar(t.rec, K(n.tok).hv);
+    if (mv == NONE) return subst(SF_NO_MEMBER, type_name_arg(t), span(n.tok));
+    Env se;
+    struct_env(t.rec, t, se);
+    st = eval(N(mv).c0, se, f, out);
+    if (st != ST_OK) return st;
+    if (N(mv).sub == BT_HDC && out.k != V_HDC)
+      return sema(C_E0103, M_S_HDC_MEMBER, N(mv).tok, type_name_arg(t));
+    return ST_OK;
+  }
+
+  EXS_HD EXS_FI u8 eval_(u32 e, const Env& env, bool f, Val& out) {
     const Node& n = N(e);
     switch (n.kind) {
       case N_INT: out = vint(K(n.tok).hv); return ST_OK;
@@ -321,21 +338,7 @@ struct Sema {
         if (st != ST_OK) return st;
         return trait(t, f, out);
       }
-      case N_MCONST: {
-        Val t;
-        u8 st = type_of(n.c0, env, t);
-        if (st != ST_OK) return st;
-        if (t.rec == NONE) return subst(SF_NO_MEMBERS, type_name_arg(t));
-        u32 mv = first_mvar(t.rec, K(n.tok).hv);
-        if (mv == NONE) return subst(SF_NO_MEMBER, type_name_arg(t), span(n.tok));
-        Env se;
-        struct_env(t.rec, t, se);
-        st = eval(N(mv).c0, se, f, out);
-        if (st != ST_OK) return st;
-        if (N(mv).sub == BT_HDC && out.k != V_HDC)
-          return sema(C_E0103, M_S_HDC_MEMBER, N(mv).tok, type_name_arg(t));
-        return ST_OK;
-      }
+      case N_MCONST: return eval_mconst(n, env, f, out);
       case N_NOT: {
         Val v;
         u8 st = eval(n.c0, env, f, v);
@@ -392,7 +395,7 @@ struct Sema {
   }
 
   // _try_candidate (sema.py:545-607)
-  EXS_HD u8 try_cand(u32 fi, u32 targs, const Val* argtys, u32 nargs, const Env& env, u32 orec,
+  EXS_HD EXS_FI u8 try_cand(u32 fi, u32 targs, const Val* argtys, u32 nargs, const Env& env, u32 orec,
                      const Env& obinds, Binds& b) {
     const FnRec& fr = T->fns[fi];
     const Node& fn = N(fr.node);
@@ -429,6 +432,23 @@ struct Sema {
         }
       }
     }
+    // common case: everything bound, no argument types to check, no requires
+    bool pending = N(fr.node + 1).c0 != NONE;
+    for (u32 i = 0; i < nargs && !pending; i++) pending = argtys[i].k != V_NONE;
+    for (u32 tp = fn.c0; tp != NONE && !pending; tp = N(tp).next) {
+      Val dummy;
+      pending = !b.get(K(N(tp).tok).hv, dummy);
+    }
+    if (!pending) return ST_OK;
+    return cand_finish(fi, argtys, nargs, orec, obinds, b);
+  }
+
+  // defaults, argument types and requires of one candidate (sema.py:577-607);
+  // out of line: the candidate and full environments live only here
+  EXS_HD EXS_NOINLINE u8 cand_finish(u32 fi, const Val* argtys, u32 nargs, u32 orec,
+                                     const Env& obinds, Binds& b) {
+    const FnRec& fr = T->fns[fi];
+    const Node& fn = N(fr.node);
     // the candidate env is materialised only when a default or the requires
     // clause is evaluated; the full env only when an argument type is known
     Env mv_env, cenv;
@@ -500,14 +520,36 @@ struct Sema {
   // effective_spaces (sema.py:670-703): returns 1=H 2=D 3=HD 4=GLOBAL, or error status
   // merged = owner bindings + (tb, hb) bound to the decl's template params; it
   // is only materialised for conditional specifiers under proposal1
-  EXS_HD u8 spaces(u32 fi, const Env* obinds, const Val& tb, const Val& hb, u8 side, u32 at_tok,
+  EXS_HD EXS_FI u8 spaces(u32 fi, const Env* obinds, const Val& tb, const Val& hb, u8 side, u32 at_tok,
                    u32 orec, u8& out) {
     const FnRec& fr = T->fns[fi];
     const Node& fn = N(fr.node);
     u16 fl = fn.n;
     if (fl & FF_G) { out = 4; return ST_OK; }
     bool cond = (fl & (FF_HPRED | FF_DPRED)) != 0;
-    if (mode == MODE_P1 && cond) {
+    if (mode == MODE_P1 && cond) return spaces_p1(fi, obinds, tb, hb, at_tok, orec, out);
+    if (mode == MODE_P2) {
+      if (K(fn.tok).id == W_MAIN && !(fr.flags & FR_OWNER)) { out = 1; return ST_OK; }
+      if (!(fl & (FF_H | FF_D | FF_G))) {
+        if (orec != NONE) {
+          u16 sf = N(T->recs[orec].node).n;
+          if (sf & (SF_H | SF_D | SF_G)) { declared(sf, out); return ST_OK; }
+        }
+        out = (u8)(1u << side);
+        return ST_OK;
+      }
+    }
+    declared(fl, out);
+    return ST_OK;
+  }
+
+  // proposal1 conditional specifiers (sema.py:638-667), out of line
+  EXS_HD EXS_NOINLINE u8 spaces_p1(u32 fi, const Env* obinds, const Val& tb, const Val& hb,
+                                   u32 at_tok, u32 orec, u8& out) {
+    const FnRec& fr = T->fns[fi];
+    const Node& fn = N(fr.node);
+    u16 fl = fn.n;
+    {
       Env merged;
       if (obinds) merged = *obinds; else merged.clear();
       merged.nbase = merged.n;
@@ -540,19 +582,6 @@ struct Sema {
       out = r;
       return ST_OK;
     }
-    if (mode == MODE_P2) {
-      if (K(fn.tok).id == W_MAIN && !(fr.flags & FR_OWNER)) { out = 1; return ST_OK; }
-      if (!(fl & (FF_H | FF_D | FF_G))) {
-        if (orec != NONE) {
-          u16 sf = N(T->recs[orec].node).n;
-          if (sf & (SF_H | SF_D | SF_G)) { declared(sf, out); return ST_OK; }
-        }
-        out = (u8)(1u << side);
-        return ST_OK;
-      }
-    }
-    declared(fl, out);
-    return ST_OK;
   }
   EXS_HD u8 pred(u32 p, const Env& env, bool& t) {
     if (p == NONE) { t = true; return ST_OK; }

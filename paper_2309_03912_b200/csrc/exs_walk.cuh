@@ -239,7 +239,7 @@ struct Walker {
   }
 
   // _resolve_type_soft (spacecheck.py:363-370)
-  EXS_HD Val soft_type(u32 tr, u32 loc_tok) {
+  EXS_HD EXS_FI Val soft_type(u32 tr, u32 loc_tok) {
     Val t;
     S.depth = 0;
     u8 st = S.type_of(tr, env, t);
@@ -252,7 +252,7 @@ struct Walker {
 
   // ------------------------------------------------------------- instantiate
   // _instantiate (spacecheck.py:312-351); returns instance id or NONE
-  EXS_HD u32 instantiate(u32 fi, const Val& tb, const Val& hb, u8 want_side, u32 orec,
+  EXS_HD EXS_FI u32 instantiate(u32 fi, const Val& tb, const Val& hb, u8 want_side, u32 orec,
                          const Env& obinds, const Val& ot, u32 at_tok) {
     u32 my_local = (stmt_k << 12) | (stmt_ord++ & 0xFFFu);
     const Node& fnn = N(T->fns[fi].node);
@@ -307,7 +307,7 @@ struct Walker {
 
   // ------------------------------------------------------------- dispatch
   // _report_stray (spacecheck.py:604-613); callee 1=H 2=D
-  EXS_HD void stray(u8 callee, u32 loc_tok) {
+  EXS_HD EXS_FI void stray(u8 callee, u32 loc_tok) {
     if (from_hd) {
       u32 i = at_add(B->n_pend, 1);
       if (i < B->cap_pend) {
@@ -324,7 +324,7 @@ struct Walker {
   }
 
   // _dispatch (spacecheck.py:554-596)
-  EXS_HD void dispatch(u32 fi, const Val& tb, const Val& hb, u32 loc_tok, u32 orec,
+  EXS_HD EXS_FI void dispatch(u32 fi, const Val& tb, const Val& hb, u32 loc_tok, u32 orec,
                        const Env& obinds, const Val& ot) {
     const Node& fnn = N(T->fns[fi].node);
     u8 sp;
@@ -353,7 +353,7 @@ struct Walker {
 
   // _select + overload resolution (sema.py:491-542); cand list given as
   // (free: fcand run) or (member: struct rec).  Returns false on failure.
-  EXS_HD bool select(bool member, u32 first, u32 count, u32 rec, u64 mname, u32 targs,
+  EXS_HD EXS_FI bool select(bool member, u32 first, u32 count, u32 rec, u64 mname, u32 targs,
                      const Val* argtys, u32 nargs, u32 loc_tok, u8 ctx_side, const Env& obinds,
                      u64 name_a0, u64 name_a1, u32& out_fi, Val& out_tb, Val& out_hb,
                      u32 name_targ = 0) {
@@ -430,7 +430,7 @@ struct Walker {
 
   // walk args (post-order) pushing their types on the argument stack; the
   // caller pops with asp = base after dispatching
-  EXS_HD u32 walk_args(u32 args, u32& base) {
+  EXS_HD EXS_FI u32 walk_args(u32 args, u32& base) {
     base = asp;
     u32 n = 0;
     for (u32 a = args; a != NONE; a = N(a).next) {
@@ -449,7 +449,7 @@ struct Walker {
     return r;
   }
 
-  EXS_HD Val expr_(u32 e) {
+  EXS_HD EXS_FI Val expr_(u32 e) {
     const Node& n = N(e);
     switch (n.kind) {
       case N_INT: { Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int"); return t; }
@@ -526,7 +526,7 @@ struct Walker {
     }
   }
 
-  EXS_HD Val free_call(u32 e) {
+  EXS_HD EXS_FI Val free_call(u32 e) {
     const Node& n = N(e);
     u32 base;
     u32 na = walk_args(n.c2, base);
@@ -534,7 +534,7 @@ struct Walker {
     asp = base;
     return r;
   }
-  EXS_HD Val free_call_(const Node& n, const Val* tys, u32 na) {
+  EXS_HD EXS_NOINLINE Val free_call_(const Node& n, const Val* tys, u32 na) {
     bool is_std = n.sub == CALL_STD;
     u64 nm = is_std ? hcombine(word_hash("std::"), K(n.c0).hv) : K(n.tok).hv;
     u32 run = is_std ? NONE : T->fmap.find(vkey(S.view, nm));
@@ -561,7 +561,7 @@ struct Walker {
   }
 
   // _member_dispatch (spacecheck.py:529-550)
-  EXS_HD void member_dispatch(const Val& rt, u32 name_tok, u32 targs, const Val* tys, u32 na,
+  EXS_HD EXS_NOINLINE void member_dispatch(const Val& rt, u32 name_tok, u32 targs, const Val* tys, u32 na,
                               u32 loc_tok) {
     u64 mname = K(name_tok).hv;
     u64 tname = S.type_name_arg(rt);
@@ -635,13 +635,16 @@ struct Walker {
     u32 base;
     u32 na = walk_args(n.c2, base);
     if (side == 1) emit_tok(C_E1003, n.tok, M_W_LAUNCH_DEVICE);
+    if (!contract) launch_dispatch(n, astk + base, na);
+    asp = base;
+  }
+  EXS_HD EXS_NOINLINE void launch_dispatch(const Node& n, const Val* tys, u32 na) {
     u32 run = T->fmap.find(vkey(S.view, K(n.tok).hv));
-    if (run == NONE || contract) { asp = base; return; }
+    if (run == NONE) return;
     u32 fi; Val tb, hb;
     Env none; none.clear();
-    bool ok = select(false, run, T->fcand_cnt[run], NONE, 0, n.c0, astk + base, na, n.tok, 1, none,
+    bool ok = select(false, run, T->fcand_cnt[run], NONE, 0, n.c0, tys, na, n.tok, 1, none,
                      span(n.tok), 0, fi, tb, hb);
-    asp = base;
     if (!ok) return;
     if (!(N(T->fns[fi].node).n & FF_G)) { emit_tok(C_E1004, n.tok, M_W_LAUNCH_NONGLOBAL); return; }
     u32 tgt = instantiate(fi, tb, hb, 1, NONE, none, vnone(), n.tok);

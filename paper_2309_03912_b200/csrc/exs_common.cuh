@@ -208,6 +208,24 @@ EXS_HD inline u32 at_add(u32* p, u32 v) {
   u32 o = *p; *p = o + v; return o;
 #endif
 }
+// Warp-aggregated "allocate one slot" on a shared counter: the lanes that are
+// active together issue a single atomicAdd (the counters of the walk are hit
+// by every thread: instance ids, creation log, pending list, diagnostics).
+EXS_HD inline u32 at_inc_agg(u32* p) {
+#if EXS_DEV_PATH
+  u32 mask = __activemask();
+  u32 lane = threadIdx.x & 31;
+  // group lanes by counter address (different counters may be in flight)
+  u32 peers = __match_any_sync(mask, (unsigned long long)p);
+  u32 leader = __ffs(peers) - 1;
+  u32 base = 0;
+  if (lane == leader) base = atomicAdd(p, (u32)__popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  return base + __popc(peers & ((1u << lane) - 1));
+#else
+  u32 o = *p; *p = o + 1; return o;
+#endif
+}
 EXS_HD inline u32 at_min(u32* p, u32 v) {
 #if EXS_DEV_PATH
   return atomicMin(p, v);

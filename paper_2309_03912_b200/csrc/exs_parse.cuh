@@ -47,9 +47,13 @@ struct Parser {
   PErr e;
   int depth;
 
+  u32 defer_open, defer_close;  // view positions of a body parsed separately (or NONE)
+  bool deferred;
+
   EXS_HD void init(const PView& view, Node* nd, u32 base, u32 cap, u32 start) {
     v = view; nodes = nd; nbase = base; nused = 0; ncap = cap; pos = start;
     failed = false; overflow = false; depth = 0;
+    defer_open = NONE; defer_close = NONE; deferred = false;
     e.line = e.col = 0; e.msg = 0; e.a0 = e.a1 = 0;
   }
 
@@ -399,7 +403,13 @@ struct Parser {
     }
     u32 body = NONE;
     bool has_body = false;
-    if (at_p(P_LBRACE)) {
+    if (at_p(P_LBRACE) && pos == defer_open) {
+      // a large body: its statements are parsed in parallel afterwards and
+      // linked under this FN node (run_parse step 4b)
+      pos = defer_close + 1;
+      has_body = true;
+      deferred = true;
+    } else if (at_p(P_LBRACE)) {
       if (!block(body)) return NONE;
       has_body = true;
     } else if (!need_p(P_SEMI, EX_FN_BODY)) {

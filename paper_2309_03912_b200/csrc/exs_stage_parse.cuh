@@ -39,7 +39,10 @@ struct ParseState {
 
 EXS_HD inline u64 node_base(const u32* item_start, u32 j) { return 2ull * item_start[j] + 4ull * j; }
 
-inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& sc, cudaStream_t st) {
+// split_min: items at least this many tokens long have their function body
+// parsed statement-parallel (step 4b); exs_set_option(3, n)
+inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& sc, cudaStream_t st,
+                      u32 split_min = 192) {
   const u32 F = L.F, T = L.T;
   // 1. files whose passes see different token sets
   u32* split = dalloc<u32>(F + 1);
@@ -151,6 +154,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   sync(st);
   dfree(s0); dfree(s1); dfree(vcnt); dfree(fvc); dfree(fvb); dfree(split);
   // 3. segmentation: depth scan and item starts (depth over ( ) { })
+  i64* depth_after = nullptr;
   {
     i64* el = dalloc<i64>(VT + 1);
     i64* inc = dalloc<i64>(VT + 1);
@@ -186,9 +190,10 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       return endf[i - 1] && vv[i - 1] == vv[i];
     };
     P.I = select_idx(VT, pred, P.item_start, L.cnt, sc, st);
+    h2d(P.item_start + P.I, &VT, 4, st);  // sentinel: node_base(is, I) bounds the last view's arena
     sync(st);
-    dfree(inc);
     dfree(el);
+    depth_after = inc;  // kept for the statement segmentation of large bodies
   }
   const u32 I = P.I;
   P.item_view = dalloc<u32>(I + 1);
@@ -212,6 +217,58 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       if (v < V) vbad[v] = NONE;
     }, st);
   }
+  // 3b. large function bodies: statements are split at depth 1 so that one
+  //     giant body (a main calling every module, C2/C3) is not parsed by a
+  //     single thread.  Boundaries: ';' at depth 1, or a '}' returning to
+  //     depth 1 that is not followed by 'else' (parser.py:397-438).
+  const u32 BIG = split_min;
+  u32* ibody = dalloc<u32>(I + 1);  // body '{' of a split item (global view position) or NONE
+  u32 NSS = 0;
+  u32* ss = nullptr;                // statement-segment starts
+  {
+    const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase;
+    const u32* is = P.item_start; const u32* iv = P.item_view; const i64* da = depth_after;
+    par_for(I, [=] EXS_HD (i64 j) {
+      u32 v = iv[j];
+      u32 next = (j + 1 < I && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
+      ibody[j] = NONE;
+      if (next - is[j] < BIG) return;
+      // last token must be the body's '}' returning to depth 0
+      const Tok& last = tk[vt[next - 1]];
+      if (!(last.kind == TK_PUNCT && last.id == P_RBRACE && (u32)(da[next - 1] & 0xFFFFFFFFll) == 0)) return;
+      for (u32 i = is[j]; i < next; i++) {
+        const Tok& t = tk[vt[i]];
+        int dep_before = i == vb[v] ? 0 : (int)(u32)(da[i - 1] & 0xFFFFFFFFll);
+        if (dep_before != 0) continue;
+        if (t.kind == TK_IDENT && (t.id == W_STRUCT || t.id == W_CLASS || t.id == W_ENUM ||
+                                   t.id == W_STATIC_ASSERT)) return;
+        if (t.kind == TK_PUNCT && t.id == P_LBRACE) { ibody[j] = i; return; }
+      }
+    }, st);
+    ss = dalloc<u32>(VT + 1);
+    const u32 Ic = I;
+    auto pred = [=] EXS_HD (u32 i) -> bool {
+      u32 lo = 0, hi = Ic;  // item containing view position i
+      while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (is[mid] <= i) lo = mid; else hi = mid; }
+      u32 bo = ibody[lo];
+      if (bo == NONE || i <= bo) return false;
+      u32 v = iv[lo];
+      u32 next = (lo + 1 < Ic && iv[lo + 1] == v) ? is[lo + 1] : vb[v + 1];
+      if (i >= next - 1) return false;  // the closing '}'
+      if (i == bo + 1) return true;
+      const Tok& pt = tk[vt[i - 1]];
+      if ((u32)(da[i - 1] & 0xFFFFFFFFll) != 1 || pt.kind != TK_PUNCT) return false;
+      if (pt.id == P_SEMI) return true;
+      if (pt.id == P_RBRACE) {
+        const Tok& t = tk[vt[i]];
+        return !(t.kind == TK_IDENT && t.id == W_ELSE);
+      }
+      return false;
+    };
+    NSS = select_idx(VT, pred, ss, L.cnt, sc, st);
+    sync(st);
+  }
+  dfree(depth_after);
   // 4. item-parallel parse
   {
     const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase; const u32* ve = P.veof;
@@ -229,18 +286,88 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
                (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0)};
       Parser p;
       u64 base = node_base(is, (u32)j);
-      p.init(pv, nd, (u32)base, 2 * (next - is[j]) + 4, is[j] - vb[v]);
+      // a split item's header owns only the node slots below its body's
+      // first statement (step 4b uses the rest)
+      u32 bo = ibody[j];
+      p.init(pv, nd, (u32)base, bo != NONE ? 2 * (bo + 1 - is[j]) : 2 * (next - is[j]) + 4, is[j] - vb[v]);
       p.v_src = s; p.v_splice = sp;
+      if (bo != NONE) { p.defer_open = bo - vb[v]; p.defer_close = next - 1 - vb[v]; }
       u32 root = p.item();
       ir[j] = root;
       ie[j] = vb[v] + p.pos;
       u8 stt = 0;
       if (p.failed) stt = p.overflow ? 2 : 1;
+      // a deferred body must have been taken by the item's FN node
+      if (!p.failed && bo != NONE && (!p.deferred || root == NONE || nd[root].kind != N_FN)) stt = 2;
       ist[j] = stt;
       ier[j] = p.e;
       if (stt || vb[v] + p.pos != next) at_min(&vbad[v], (u32)j);
     }, st);
   }
+  // 4b. statements of the split bodies, in parallel; merged into item status
+  if (NSS) {
+    const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase; const u32* ve = P.veof;
+    const u32* is = P.item_start; const u32* iv = P.item_view; const u32* vf = P.vfile;
+    const u8* cf = L.cfg; const u8* s = L.src; const u32* sp = L.splice;
+    Node* nd = P.nodes; u8* ist = P.item_stat; PErr* ier = P.item_err; u32* vbad = P.vbad;
+    const u32* ssc = ss;
+    u32* sroot = dalloc<u32>(NSS + 1);
+    u32* sbad = dalloc<u32>(I + 1);
+    u8* sstat = dalloc<u8>(NSS + 1);
+    PErr* serr = dalloc<PErr>(NSS + 1);
+    dfill_ff(sbad, 4ull * (I + 1), st);
+    const u32 Ic = I, NSSc = NSS;
+    EXS_TAG("parse_body_stmts");
+    par_for_walk(NSS, [=] EXS_HD (i64 k) {
+      u32 i0 = ssc[k];
+      u32 lo = 0, hi = Ic;
+      while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (is[mid] <= i0) lo = mid; else hi = mid; }
+      u32 j = lo, v = iv[j];
+      u32 inext = (j + 1 < Ic && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
+      bool last = !(k + 1 < NSSc && ssc[k + 1] < inext);
+      u32 stop = last ? inext - 1 : ssc[k + 1];  // next segment, or the body's '}'
+      u8 c = cf[vf[v]];
+      PView pv{tk, vt, vb[v], vb[v + 1] - vb[v], ve[2 * v], ve[2 * v + 1],
+               (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0)};
+      Parser p;
+      p.init(pv, nd, (u32)(2ull * i0 + 4ull * j), 2 * (stop - i0), i0 - vb[v]);
+      p.v_src = s; p.v_splice = sp;
+      p.depth = 1;  // inside the body's block (parser depth limit)
+      u32 r = p.stmt();
+      sroot[k] = r;
+      u8 stt = p.failed ? (p.overflow ? 2 : 1) : 0;
+      if (!stt && vb[v] + p.pos != stop) stt = 3;  // statements do not chain: sequential repair
+      sstat[k] = stt;
+      serr[k] = p.e;
+      if (stt) at_min(&sbad[j], (u32)k);
+    }, st);
+    par_for(I, [=] EXS_HD (i64 j) {
+      u32 k = sbad[j];
+      if (k == NONE || ist[j]) return;  // an error before the body wins
+      ist[j] = sstat[k] == 1 ? 1 : 2;
+      ier[j] = serr[k];
+      at_min(&vbad[iv[j]], (u32)j);
+    }, st);
+    // link the statements under their FN nodes
+    const u32* ir = P.item_root;
+    par_for(NSS, [=] EXS_HD (i64 k) {
+      u32 i0 = ssc[k];
+      u32 lo = 0, hi = Ic;
+      while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (is[mid] <= i0) lo = mid; else hi = mid; }
+      u32 j = lo;
+      if (ist[j] || sroot[k] == NONE) return;
+      u32 v = iv[j];
+      u32 inext = (j + 1 < Ic && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
+      bool first = k == 0 || ssc[k - 1] < is[j];
+      bool last = !(k + 1 < NSSc && ssc[k + 1] < inext);
+      nd[sroot[k]].next = last ? NONE : sroot[k + 1];
+      if (first) nd[ir[j]].c2 = sroot[k];
+    }, st);
+    sync(st);
+    dfree(sroot); dfree(sbad); dfree(sstat); dfree(serr);
+  }
+  dfree(ss);
+  dfree(ibody);
   // 5. per view: parse error, ok, or sequential repair
   u32 nfb = 0;
   std::vector<u32> fb_views;

@@ -97,9 +97,12 @@ EXS_HD inline bool set_insert(u64* set, u32 mask, u64 k) {
 }
 
 EXS_HD inline void emit_diag(const WalkBufs& B, Diag d) {
+  // a full buffer means the batch is re-run with a larger one: stop early
+  // instead of probing an ever fuller dedup set
+  if (ld_volatile(B.n_diags) >= B.cap_diags) { at_or(B.overflow, 2); return; }
   u64 h = diag_hash(d);
   if (!set_insert(B.dset, B.dmask, h)) return;
-  u32 i = at_add(B.n_diags, 1);
+  u32 i = at_inc_agg(B.n_diags);
   if (i < B.cap_diags) B.diags[i] = d;
   else at_or(B.overflow, 2);
 }
@@ -127,10 +130,11 @@ EXS_HD inline bool ikey_cas(IKey* slot, const IKey& k, IKey& old) {
 EXS_HD inline u32 inst_lookup_or_insert(const WalkBufs& B, const IKey& k, bool& inserted) {
   u32 h = (u32)mix64(k.a ^ mix64(k.b)) & B.mask;
   inserted = false;
+  if (ld_volatile(B.n_inst) >= B.cap_inst) { at_or(B.overflow, 1u); return NONE; }
   for (u32 probes = 0; probes <= B.mask; probes++) {
     IKey old;
     if (ikey_cas(&B.slots[h], k, old)) {
-      u32 id = at_add(B.n_inst, 1u);
+      u32 id = at_inc_agg(B.n_inst);
       if (id >= B.cap_inst) { at_or(B.overflow, 1u); id = NONE; }
       inserted = true;
       return id;  // caller initialises the record, then publishes sid[h]
@@ -287,7 +291,7 @@ struct Walker {
     if (I.level == clevel) {
       // a creator in this level: log it; the minimum creation key wins
       if (!inserted) at_min64(&I.ckey, ck);
-      u32 li = at_add(B->n_log, 1);
+      u32 li = at_inc_agg(B->n_log);
       if (li < B->cap_log) {
         CreateLog& L = B->log[li];
         L.ckey = ck; L.inst = id; L.at = at_tok; L.fn = fi;
@@ -309,7 +313,7 @@ struct Walker {
   // _report_stray (spacecheck.py:604-613); callee 1=H 2=D
   EXS_HD EXS_FI void stray(u8 callee, u32 loc_tok) {
     if (from_hd) {
-      u32 i = at_add(B->n_pend, 1);
+      u32 i = at_inc_agg(B->n_pend);
       if (i < B->cap_pend) {
         Pending& p = B->pend[i];
         p.walk = walk; p.caller = inst_id; p.line = K(loc_tok).line; p.col = K(loc_tok).col;
@@ -649,7 +653,7 @@ struct Walker {
     if (!(N(T->fns[fi].node).n & FF_G)) { emit_tok(C_E1004, n.tok, M_W_LAUNCH_NONGLOBAL); return; }
     u32 tgt = instantiate(fi, tb, hb, 1, NONE, none, vnone(), n.tok);
     if (tgt != NONE && side == 0) {
-      u32 i = at_add(B->n_seeds, 1);
+      u32 i = at_inc_agg(B->n_seeds);
       if (i < B->cap_seeds) { B->seeds[2 * i] = walk; B->seeds[2 * i + 1] = tgt; }
       else at_or(B->overflow, 4);
     }

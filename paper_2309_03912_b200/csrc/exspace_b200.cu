@@ -148,6 +148,7 @@ struct Handle {
   exs_stats stats{};
   float t_stage[4] = {0, 0, 0, 0};
   bool want_demands = false;
+  u32 split_min = 192;  // statement-parallel body parsing threshold (tokens)
 
   void reset() {
     L.free_all(); L = LexState();
@@ -350,35 +351,52 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     H.t_stage[0] = t0.stop();
     prof_mark(st);
     Timer t1(st);
-    run_parse(L, H.P, B0, H.sc, st);
+    run_parse(L, H.P, B0, H.sc, st, H.split_min);
     H.t_stage[1] = t1.stop();
     prof_mark(st);
     Timer t2(st);
     run_sema(L, H.P, H.S, B0, H.sc, st);
     H.t_stage[2] = t2.stop();
     if (!cap_inst) cap_inst = (u32)std::min<u64>(std::max<u64>(65536, 4ull * H.S.NF + 1024), 0x7FFFFFFFull);
-    H.W.cap_inst = cap_inst;
+    // the walk is retried alone (bigger instance table) after restoring the
+    // diagnostics emitted by the earlier stages
+    u32 nd0 = get1(H.d_ndiags, st);
+    u64* dset_snap = dalloc<u64>((u64)H.dmask + 1);
+    u32* ct_snap = dalloc<u32>(n_files + 1);
+    d2d(dset_snap, H.d_dset, 8ull * (H.dmask + 1), st);
+    d2d(ct_snap, H.d_contract, 4ull * (n_files + 1), st);
     prof_mark(st);
     Timer t3(st);
-    bool ok = run_walk(L, H.P, H.S, H.W, B0, H.sc, st, cap_diags);
-    if (ok && (any_div || H.want_demands)) run_demands(H, any_div);
+    u32 walk_ovf = 0;
+    while (true) {
+      H.W.free_all();
+      H.W = WalkState();
+      H.W.cap_inst = cap_inst;
+      bool ok = run_walk(L, H.P, H.S, H.W, B0, H.sc, st, cap_diags);
+      if (ok && (any_div || H.want_demands)) run_demands(H, any_div);
+      walk_ovf = get1(H.W.counters + 4, st);
+      (void)ok;
+      if ((walk_ovf & 2) || !(walk_ovf & 5)) break;  // diagnostics overflow: outer loop
+      if (walk_ovf & 1) {
+        u32 n_now = get1(H.W.counters, st);
+        cap_inst = (u32)std::min<u64>(std::max<u64>(8ull * cap_inst, 2ull * n_now), 0x7FFFFFFFull);
+      }
+      h2d(H.d_ndiags, &nd0, 4, st);
+      d2d(H.d_dset, dset_snap, 8ull * (H.dmask + 1), st);
+      d2d(H.d_contract, ct_snap, 4ull * (n_files + 1), st);
+      retries++;
+    }
     H.t_stage[3] = t3.stop();
+    dfree(dset_snap);
+    dfree(ct_snap);
     u32 ovf_h = get1(ovf, st);
-    u32 walk_ovf = ok ? get1(H.W.counters + 4, st) : 0;
     u32 nd = get1(H.d_ndiags, st);
     dfree(ovf);
-    if (!ok || (walk_ovf & 1)) {
-      u32 n_now = get1(H.W.counters, st);
-      cap_inst = (u32)std::min<u64>(std::max<u64>(4ull * cap_inst, 2ull * n_now), 0x7FFFFFFFull);
-      retries++;
-      continue;
-    }
     if (nd > cap_diags || (ovf_h & 2) || (walk_ovf & 2)) {
       cap_diags = (u32)std::min<u64>(4ull * std::max(nd, cap_diags), 0x7FFFFFFFull);
       retries++;
       continue;
     }
-    if (walk_ovf & 4) { retries++; continue; }
     break;
   }
   // out-of-contract units get one marker record
@@ -545,6 +563,7 @@ int exs_set_option(exs_handle x, int key, int value) {
 #ifndef EXS_EMU
   else if (key == 2) g_profile = value != 0;  // per-launch device timing of later runs
 #endif
+  else if (key == 3) x->h.split_min = value < 4 ? 4u : (u32)value;  // statement-split threshold (tokens)
   else throw Err("unknown option");
   API_END
 }

@@ -2,6 +2,7 @@
 compiled as sequential host code (EXS_EMU build, build/libexspace_emu.so)
 against the golden vectors, to debug the CUDA sources without a GPU.
 The package never loads this library."""
+import os
 import sys
 from pathlib import Path
 
@@ -21,6 +22,8 @@ def unit_of(c):
 
 def main(groups, limit=None, batch=64, verbose=3):
     eng = X.Engine(0, LIB)
+    if os.environ.get("EXS_SPLIT"):  # force statement-parallel body parsing on small items
+        eng.handle.set_option(3, int(os.environ["EXS_SPLIT"]))
     bad = total = 0
     for g in groups:
         cases = load_golden(g)[:limit]

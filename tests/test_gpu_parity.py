@@ -36,10 +36,20 @@ def as_rows(a):
             for d in a.all_diagnostics]
 
 
+@pytest.fixture(scope="module")
+def eng_split(X):
+    """An engine that parses every function body of >= 4 tokens statement-
+    parallel (run_parse step 4b), so the golden vectors exercise that path."""
+    e = X.Engine(0)
+    e.handle.set_option(3, 4)
+    return e
+
+
+@pytest.mark.parametrize("split", [False, True], ids=["items", "stmt_split"])
 @pytest.mark.parametrize("group", GOLDEN_GROUPS)
-def test_golden_vectors(X, eng, group):
+def test_golden_vectors(X, eng, eng_split, group, split):
     cases = load_golden(group)
-    res = eng.run_batch([unit_of(X, c) for c in cases], want_walks=True)
+    res = (eng_split if split else eng).run_batch([unit_of(X, c) for c in cases], want_walks=True)
     bad = []
     for c, a in zip(cases, res):
         if as_rows(a) != c["diags"]:
@@ -154,9 +164,11 @@ def test_c4_callgraph_vs_oracle(X, eng):
     _check_against_oracle(X, eng, [text], ["sound"])
 
 
-def test_batch_invariance_and_determinism(X, eng):
+@pytest.mark.parametrize("split", [False, True], ids=["items", "stmt_split"])
+def test_batch_invariance_and_determinism(X, eng, eng_split, split):
     """A unit's result does not depend on its batch neighbours or on the run."""
     from paper_2309_03912_b200 import synth
+    eng = eng_split if split else eng
     rng = random.Random(5)
     texts = [synth.gen_c5_file(rng.randrange(10**6), 4000, 0.3) for _ in range(12)]
     units = [(t, f"b{i}.cu", X.CompileProfile(), X.Mode.SOUND, X.TraitConfig()) for i, t in enumerate(texts)]

@@ -15,6 +15,7 @@
 // so lines compose as {CODE,BLOCK}->{CODE,BLOCK} maps under a scan.
 #pragma once
 #include "exs_common.cuh"
+#include "exs_unicode.cuh"
 
 namespace exs {
 
@@ -173,27 +174,53 @@ constexpr u64 fnv_c(const char* s, u64 h = 1469598103934665603ull) {
 }
 constexpr u32 len_c(const char* s) { return *s ? 1 + len_c(s + 1) : 0; }
 
-// Vocabulary id from the token's text hash and length: a switch over
-// compile-time constants (no table walk, no divergent constant-memory reads).
-EXS_HD inline u8 vocab_hash(u64 hv, u32 len) {
-#define EXS_W(str, id) case fnv_c(str): return len == len_c(str) ? (u8)(id) : (u8)0;
-  switch (hv) {
-    EXS_W("struct", W_STRUCT) EXS_W("class", W_CLASS) EXS_W("enum", W_ENUM)
-    EXS_W("template", W_TEMPLATE) EXS_W("typename", W_TYPENAME) EXS_W("requires", W_REQUIRES)
-    EXS_W("return", W_RETURN) EXS_W("if", W_IF) EXS_W("else", W_ELSE) EXS_W("for", W_FOR)
-    EXS_W("void", W_VOID) EXS_W("int", W_INT) EXS_W("bool", W_BOOL) EXS_W("true", W_TRUE)
-    EXS_W("false", W_FALSE) EXS_W("constexpr", W_CONSTEXPR) EXS_W("static", W_STATIC)
-    EXS_W("static_assert", W_STATIC_ASSERT) EXS_W("HDC", W_HDC) EXS_W("__host__", W_HOST)
-    EXS_W("__device__", W_DEVICE) EXS_W("__global__", W_GLOBAL) EXS_W("main", W_MAIN)
-    EXS_W("cuda_arch", W_CUDA_ARCH) EXS_W("hdc", W_HDC_TRAIT) EXS_W("std", W_STD)
-    EXS_W("Hst", W_HST) EXS_W("Dev", W_DEV) EXS_W("HstDev", W_HSTDEV) EXS_W("printf", W_PRINTF)
-    EXS_W("release_assert", W_RELEASE_ASSERT) EXS_W("__trap", W_TRAP) EXS_W("abort", W_ABORT)
-    EXS_W("cudaDeviceSynchronize", W_CUDASYNC) EXS_W("hd_warning_disable", W_HD_WARNING_DISABLE)
-    EXS_W("nv_exec_check_disable", W_NV_EXEC_CHECK_DISABLE) EXS_W("!", W_BANG_STR)
-    EXS_W("(", W_LPAREN_STR)
-    default: return W_NONE;
+// Vocabulary id from the token's text hash and length: a perfect hash over
+// the 38 words (multiplier found offline: slot = (hv * K) >> 57, collision-
+// free) -- one table load, no divergent compare tree.
+struct VEnt { u64 hv; u32 len; u32 id; };
+struct VTable { VEnt e[128]; };
+constexpr u64 kVocabK = 0x326324dfb695ffbull;
+EXS_HD constexpr u32 vocab_slot(u64 hv) { return (u32)((hv * kVocabK) >> 57); }
+constexpr VTable make_vtable() {
+  VTable t{};
+  const char* ws[] = {"struct", "class", "enum", "template", "typename", "requires", "return", "if",
+                      "else", "for", "void", "int", "bool", "true", "false", "constexpr", "static",
+                      "static_assert", "HDC", "__host__", "__device__", "__global__", "main",
+                      "cuda_arch", "hdc", "std", "Hst", "Dev", "HstDev", "printf", "release_assert",
+                      "__trap", "abort", "cudaDeviceSynchronize", "hd_warning_disable",
+                      "nv_exec_check_disable", "!", "("};
+  const u8 ids[] = {W_STRUCT, W_CLASS, W_ENUM, W_TEMPLATE, W_TYPENAME, W_REQUIRES, W_RETURN, W_IF,
+                    W_ELSE, W_FOR, W_VOID, W_INT, W_BOOL, W_TRUE, W_FALSE, W_CONSTEXPR, W_STATIC,
+                    W_STATIC_ASSERT, W_HDC, W_HOST, W_DEVICE, W_GLOBAL, W_MAIN, W_CUDA_ARCH,
+                    W_HDC_TRAIT, W_STD, W_HST, W_DEV, W_HSTDEV, W_PRINTF, W_RELEASE_ASSERT, W_TRAP,
+                    W_ABORT, W_CUDASYNC, W_HD_WARNING_DISABLE, W_NV_EXEC_CHECK_DISABLE, W_BANG_STR,
+                    W_LPAREN_STR};
+  for (u32 i = 0; i < sizeof(ids); i++) {
+    const u64 h = fnv_c(ws[i]);
+    t.e[vocab_slot(h)] = VEnt{h, len_c(ws[i]), ids[i]};
   }
-#undef EXS_W
+  return t;
+}
+constexpr u32 vtable_fill() {
+  VTable t = make_vtable();
+  u32 n = 0;
+  for (u32 i = 0; i < 128; i++) n += t.e[i].len != 0;
+  return n;
+}
+static_assert(vtable_fill() == W_COUNT - 1, "vocabulary perfect hash: collision or missing word");
+#ifndef EXS_EMU
+__device__ const VTable kVTabDev = make_vtable();
+#endif
+static constexpr VTable kVTabHost = make_vtable();
+
+EXS_HD inline u8 vocab_hash(u64 hv, u32 len) {
+  // body-only __CUDA_ARCH__ switch, never in a signature
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  const VEnt& e = kVTabDev.e[vocab_slot(hv)];
+#else
+  const VEnt& e = kVTabHost.e[vocab_slot(hv)];
+#endif
+  return (e.hv == hv && e.len == len) ? (u8)e.id : (u8)W_NONE;
 }
 
 EXS_HD inline u8 vocab_lookup(const u8* t, u32 len) {
@@ -216,6 +243,55 @@ EXS_HD inline u8 vocab_lookup(const u8* t, u32 len) {
     v += l + 1;
   }
   return W_NONE;
+}
+
+// ---------------------------------------------------------------------------
+// Unicode classes of Python's str predicates (exs_unicode.cuh, generated)
+
+enum { UC_ALPHA = 1, UC_DIGIT = 2, UC_ALNUM = 4, UC_DECIMAL = 8, UC_SPACE = 16 };
+#ifndef EXS_EMU
+__device__ const u32 kUclsDev[EXS_UCLS_N] = {EXS_UCLS_TABLE};
+#endif
+static const u32 kUclsHost[EXS_UCLS_N] = {EXS_UCLS_TABLE};
+
+struct UClass { u8 cls; u32 start; };  // class bits, start of its run
+
+EXS_HD inline UClass uclass(u32 cp) {
+  if (cp < 0x80) {
+    u8 c = (u8)cp, k = 0;
+    if (is_alpha(c)) k = UC_ALPHA | UC_ALNUM;
+    else if (is_digit(c)) k = UC_DIGIT | UC_ALNUM | UC_DECIMAL;
+    else if (is_pyspace(c)) k = UC_SPACE;
+    return UClass{k, is_digit(c) ? (u32)'0' : cp};
+  }
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  const u32* t = kUclsDev;
+#else
+  const u32* t = kUclsHost;
+#endif
+  u32 lo = 0, hi = EXS_UCLS_N;  // last entry with start <= cp
+  while (hi - lo > 1) {
+    u32 mid = (lo + hi) / 2;
+    if ((t[mid] >> 8) <= cp) lo = mid; else hi = mid;
+  }
+  return UClass{(u8)(t[lo] & 0xFF), t[lo] >> 8};
+}
+
+// code point of the UTF-8 sequence whose lead byte is at p (no splice can fall
+// inside a code point of valid UTF-8)
+EXS_HD inline u32 utf8_at(const u8* s, u32 p, u32 lim) {
+  u8 c = s[p];
+  if (c < 0xC0) return c;
+  u32 n = c >= 0xF0 ? 3 : (c >= 0xE0 ? 2 : 1);
+  u32 cp = c & (0x3Fu >> n);
+  for (u32 k = 1; k <= n && p + k < lim; k++) cp = (cp << 6) | (s[p + k] & 0x3Fu);
+  return cp;
+}
+
+// class of the (blanked) character c yielded at raw position pos
+EXS_HD inline u8 char_class(const u8* s, u8 c, u32 pos, u32 lim) {
+  if (c < 0x80) return uclass(c).cls;
+  return uclass(utf8_at(s, pos, lim)).cls;
 }
 
 // directive kinds (per logical line)
@@ -255,9 +331,11 @@ EXS_HD inline LineInfo scan_line_directive(const u8* s, const u32* sp, u32 lo, u
   // pass 1: first non-space char, code points
   bool seen = false, directive = false;
   u32 hash_pos = 0;
+  bool ws = false;  // str.isspace of the current code point (continuation bytes inherit it)
   while (b.next(c, pos, w)) {
     li.cps += w;
-    if (!seen && !(w == 0 || is_pyspace(c))) {
+    if (w) ws = (char_class(s, c, pos, hi) & UC_SPACE) != 0;
+    if (!seen && !ws) {
       seen = true;
       if (c == '#') { directive = true; hash_pos = pos; }
     }
@@ -275,10 +353,12 @@ EXS_HD inline LineInfo scan_line_directive(const u8* s, const u32* sp, u32 lo, u
   int phase = 0;  // 0 before name, 1 in name, 2 after name, 3 in rest
   u32 idx = 0, rest_start_idx = 0, rest_end_idx = 0, name_start_idx = 0, name_end_idx = 0;
   bool pending_space = false;
+  ws = false;
   while (b.next(c, pos, w)) {
-    bool sp_ = (w != 0) && is_pyspace(c);
+    if (w) ws = (char_class(s, c, pos, hi) & UC_SPACE) != 0;
+    bool sp_ = (w != 0) && ws;
     if (w == 0) {   // continuation byte: part of the current char
-      if (c != ' ') {
+      if (c != ' ' && !ws) {
         if (phase == 1) name_end_idx = idx + 1;
         else if (phase == 3 && !pending_space) rest_end_idx = idx + 1;
       }
@@ -414,14 +494,21 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
       u32 consumed = 1;
       int nw = 0; bool inword = false, first_ok = true;
       u8 wbuf[8]; u32 wl = 0;
-      u32 name_pos = 0, name_end = 0; u64 h = fnv_init(); u8 nb[24]; u32 nl = 0;
+      u32 name_pos = 0, name_end = 0; u64 h = fnv_init(); u32 nl = 0;
       have = b.next(c, pos, w);
-      while (have && (w ? (is_ident_char(c) || c == ' ' || c == '\t') : c == ' ')) {
+      bool acc = true;
+      // lexer.py:67-70: isalnum, '_', ' ' and '\t' continue the directive
+      while (have) {
+        bool ok;
+        if (w == 0) ok = c == ' ' || (acc && c >= 0x80);
+        else ok = c == ' ' || c == '\t' || c == '_' || (char_class(s, c, pos, hi) & UC_ALNUM) != 0;
+        if (w) acc = ok;
+        if (!ok) break;
         bool spc = (c == ' ' || c == '\t');
         if (!spc) {
           if (!inword) { nw++; inword = true; if (nw == 2) name_pos = pos; }
           if (nw == 1) { if (wl < 8) wbuf[wl] = c; wl++; }
-          if (nw == 2) { h = fnv_step(h, c); if (nl < 24) nb[nl] = c; nl++; name_end = pos + 1; }
+          if (nw == 2) { h = fnv_step(h, c); nl++; name_end = pos + 1; }
         } else {
           inword = false;
         }
@@ -445,7 +532,7 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
     }
     if (c == '"') {
       u32 cw = 1;
-      u64 h = fnv_init(); u8 nb[24]; u32 nl = 0;
+      u64 h = fnv_init(); u32 nl = 0;
       u32 cstart = NONE, cend = 0;
       bool closed = false;
       have = b.next(c, pos, w);
@@ -454,7 +541,6 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
         if (cstart == NONE) cstart = pos;
         cend = pos + 1;
         h = fnv_step(h, c);
-        if (nl < 24) nb[nl] = c;
         nl++;
         cw += w;
         have = b.next(c, pos, w);
@@ -475,24 +561,39 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
       have = b.next(c, pos, w);
       continue;
     }
-    // identifiers: ASCII [A-Za-z_][A-Za-z0-9_]* plus any non-ASCII code point
-    // treated as a letter (Python str.isalpha for letters such as 'é')
-    if (is_digit(c) || is_ident_start(c) || c >= 0xC0) {
-      bool digits = is_digit(c);
+    // integers and identifiers (lexer.py:86-104): str.isdigit starts a
+    // number continued by isdigit; isalpha or '_' starts an identifier
+    // continued by isalnum or '_' (Unicode classes, exs_unicode.cuh)
+    const u8 k0 = char_class(s, c, pos, hi);
+    if ((k0 & (UC_DIGIT | UC_ALPHA)) || c == '_') {
+      bool digits = (k0 & UC_DIGIT) != 0;
       u64 h = fnv_init(), val = 0; bool ovf = false;
-      u8 nb[24]; u32 nl = 0, ncp = 0; u32 last = pos; bool spl = false;
+      u32 nl = 0, ncp = 0; u32 last = pos; bool spl = false;
       u32 prevpos = pos;
-      while (have && (digits ? (w && is_digit(c))
-                             : (w ? (is_ident_char(c) || c >= 0xC0) : (c >= 0x80)))) {
+      bool acc = true;  // the current code point is part of the token
+      while (have) {
+        bool ok;
+        if (w == 0) {
+          ok = acc && c >= 0x80;  // continuation byte of the current code point
+        } else {
+          const u32 cp = c < 0x80 ? (u32)c : utf8_at(s, pos, hi);
+          const UClass u = uclass(cp);
+          ok = digits ? (u.cls & UC_DIGIT) != 0 : ((u.cls & UC_ALNUM) != 0 || c == '_');
+          acc = ok;
+          if (ok && digits) {
+            // int(text): decimal digits only (a non-decimal digit makes the
+            // reference raise -- outside its contract; flagged like overflow)
+            u32 dv = (u.cls & UC_DECIMAL) ? (cp - u.start) % 10 : 0;
+            if (!(u.cls & UC_DECIMAL)) ovf = true;
+            u64 nv = val * 10 + dv;
+            if (val > 1844674407370955161ull || nv < val) ovf = true;
+            val = nv;
+          }
+        }
+        if (!ok) break;
         if (pos != prevpos + 1 && nl) spl = true;
         prevpos = pos;
         h = fnv_step(h, c);
-        if (digits) {
-          u64 nv = val * 10 + (c - '0');
-          if (val > 1844674407370955161ull || nv < val) ovf = true;
-          val = nv;
-        }
-        if (nl < 24) nb[nl] = c;
         nl++;
         ncp += w;
         last = pos;

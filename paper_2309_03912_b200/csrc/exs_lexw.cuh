@@ -1,0 +1,549 @@
+// exs_lexw.cuh -- K2/K3 word-parallel lexing: one thread per 32-byte word.
+//
+// The reference preprocesses and lexes line by line (syntax/preprocess.py:
+// 81-203, syntax/lexer.py:46-118).  Here the unit of work is a fixed 32-byte
+// word of the concatenated corpus, so every thread does the same amount of
+// work regardless of line lengths:
+//   * lex_words (word_info): the comment-DFA transfer map of the word over its
+//     logical (non-spliced) bytes, its line starts and newlines, and whether it
+//     holds a "special" byte (spliced byte, non-ASCII byte or '#');
+//   * one inclusive scan of WScan composes the maps (DFA state at every word
+//     start), counts line starts / newlines and carries the last line start;
+//   * plain logical lines (no special byte) are tokenized byte-parallel: a
+//     word emits the tokens that START in it; the token in progress at its
+//     first byte is recovered by a short look-back (identifier/number run, or
+//     the greedy alignment of a punctuator run);
+//   * special lines (continuations, UTF-8, directives, pragmas) are lexed
+//     whole by the word holding their first byte, with the sequential line
+//     lexer of exs_lex.cuh (same code as the reference's line loop).
+// Token counts per word -> exclusive scan -> emit pass writes tokens in source
+// order.  Lexical errors are reduced per (file, pass) with atomicMin on the
+// byte position; line/column/message are recovered from the position.
+#pragma once
+#include "exs_lex.cuh"
+
+namespace exs {
+
+// per (file, pass) status -- fp = 2*file + pass (pass 0 host, 1 device)
+struct FP {
+  u32 pp_line;    // line number of the first E0002 directive (NONE = ok, NONE-1 = no such pass)
+  u16 pp_msg;
+  u16 lex_msg;    // first lexical error: message (resolved from lex_pos)
+  u64 pp_a0;      // text span / flags for the message
+  u32 pp_a1;
+  u32 lex_line;   // first lexical error in an active line: line number (NONE = ok)
+  u32 lex_col;
+  u32 lex_pos;    // its byte position (atomicMin over the emit pass)
+  u32 eof_line, eof_col;
+  u32 view;       // view serving this pass (NONE if none)
+  u32 perr;       // parse failed (1) / ok (0)
+};
+
+// packed 6-state map of the comment DFA: 4 bits per start state
+constexpr u32 MAP_ID = 0x543210u;
+EXS_HD inline u32 map_at(u32 m, u32 s) { return (m >> (4 * s)) & 15u; }
+EXS_HD inline u32 map_compose(u32 a, u32 b) {  // a, then b
+  u32 r = 0;
+#pragma unroll
+  for (u32 s = 0; s < 6; s++) r |= map_at(b, map_at(a, s)) << (4 * s);
+  return r;
+}
+
+struct WScan {
+  u32 map;  // comment-DFA transfer map over the word's logical bytes
+  u32 lsp;  // last logical-line start in the word (0 if none; max-scanned)
+  u64 lc;   // line starts << 32 | newline bytes (summed)
+};
+struct WScanOp {
+  EXS_HD WScan operator()(const WScan& a, const WScan& b) const {
+    WScan r;
+    r.map = map_compose(a.map, b.map);
+    r.lsp = a.lsp > b.lsp ? a.lsp : b.lsp;
+    r.lc = a.lc + b.lc;
+    return r;
+  }
+};
+
+// one directive line (preprocess.py:168-200), in source order after sorting
+struct DirRec {
+  u32 pos, file, line_no;
+  u8 kind, macro, is_ifndef, pad;
+  u64 span;
+};
+
+// one special logical line (continuation, UTF-8, '#'): lexed by its own
+// thread with the reference's sequential line loop (run_lex K3s)
+struct SRec {
+  u32 pos, file, line_no;
+  u32 count;   // tokens (0 for a directive line)
+  u32 slot;    // first token index (emit pass)
+  u8 lst;      // comment state at the line start (S_CODE / S_BLOCK)
+  u8 kind;     // LK_* of the line
+  u8 mask;     // pass activity of the line (emit pass)
+  u8 pad;
+};
+
+struct LexW {
+  const u8* src; u32 n; bool vec;  // vec: 16-byte aligned source, vector loads allowed
+  const u32* sp; const u32* fs;    // splice / file-start bitmaps
+  const WScan* wsc;                // inclusive scan (word w reads wsc[w-1])
+  u8* special;                     // per logical line
+  const u32* foff; u32 F; const u8* cfg;
+  const u32* fnl;                  // global newline count before each file start
+  u32* nspecial;                   // special lines (upper bound, mark pass)
+  // count pass: special-line records
+  SRec* srec; u32* nsrec; u32 srcap;
+  u32 ns;                          // emit pass: special lines, sorted by position
+  // emit pass
+  const u32* fdir; const DirRec* dirs; const u8* dlive; FP* fp;
+};
+
+EXS_HD inline u32 upper_file(const u32* foff, u32 F, u32 p) {
+  // last f with foff[f] <= p
+  u32 lo = 0, hi = F;
+  while (hi - lo > 1) {
+    u32 mid = (lo + hi) / 2;
+    if (foff[mid] <= p) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+EXS_HD inline u8 file_passes(u8 cfg) { return (cfg & CFG_PLAIN) ? 1 : 3; }
+
+// punctuators that can start a multi-character token (lexer.py:30-39)
+EXS_HD inline bool is_pset(u8 c) {
+  return c == '<' || c == '>' || c == ':' || c == '=' || c == '!' || c == '&' || c == '|' || c == '+';
+}
+// greedy punctuator at c followed by c1, c2 (0 = none); pid 0: not a punctuator
+EXS_HD inline u32 punct_len(u8 c, u8 c1, u8 c2, u8& pid) {
+  if (c == '<' && c1 == '<' && c2 == '<') { pid = P_LLL; return 3; }
+  if (c == '>' && c1 == '>' && c2 == '>') { pid = P_GGG; return 3; }
+  if (c == ':' && c1 == ':') { pid = P_SCOPE; return 2; }
+  if (c == '=' && c1 == '=') { pid = P_EQ; return 2; }
+  if (c == '!' && c1 == '=') { pid = P_NE; return 2; }
+  if (c == '&' && c1 == '&') { pid = P_AND; return 2; }
+  if (c == '|' && c1 == '|') { pid = P_OR; return 2; }
+  if (c == '+' && c1 == '+') { pid = P_INC; return 2; }
+  switch (c) {
+    case '{': pid = P_LBRACE; break;
+    case '}': pid = P_RBRACE; break;
+    case '(': pid = P_LPAREN; break;
+    case ')': pid = P_RPAREN; break;
+    case '<': pid = P_LT; break;
+    case '>': pid = P_GT; break;
+    case ',': pid = P_COMMA; break;
+    case ';': pid = P_SEMI; break;
+    case '.': pid = P_DOT; break;
+    case '!': pid = P_BANG; break;
+    case '=': pid = P_ASSIGN; break;
+    default: pid = 0;
+  }
+  return 1;
+}
+
+EXS_HD inline u8 byte_of(const u32 r[8], u32 j) {
+  u32 k = j >> 2;
+  u32 v = k < 4 ? (k < 2 ? (k == 0 ? r[0] : r[1]) : (k == 2 ? r[2] : r[3]))
+                : (k < 6 ? (k == 4 ? r[4] : r[5]) : (k == 6 ? r[6] : r[7]));
+  return (u8)(v >> (8 * (j & 3)));
+}
+
+EXS_HD inline void load_word(const LexW& X, u32 base, u32 r[8]) {
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  if (X.vec && base + 32 <= X.n) {
+    const uint4* q = reinterpret_cast<const uint4*>(X.src + base);
+    uint4 a = __ldg(q), b = __ldg(q + 1);
+    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+    r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+    return;
+  }
+#endif
+  for (u32 k = 0; k < 8; k++) r[k] = 0;
+  for (u32 j = 0; j < 32 && base + j < X.n; j++) r[j >> 2] |= (u32)X.src[base + j] << (8 * (j & 3));
+}
+
+// comment-DFA step as a table: the transition map of the character's class
+// (other, '"', '/', '*', '\n'), 4 bits per state -- branch-free
+EXS_HD inline u32 dfa_class_map(u8 c) {
+  return c == '"' ? 0x443022u : (c == '/' ? 0x043231u : (c == '*' ? 0x553240u : (c == '\n' ? 0x440000u : 0x443200u)));
+}
+EXS_HD inline bool is_single(u8 c) {
+  return c == '{' || c == '}' || c == '(' || c == ')' || c == ',' || c == ';' || c == '.';
+}
+
+// K2: per-word scan record and special flag
+EXS_HD inline WScan word_info(const LexW& X, u32 w, u8& special, u32& nhash) {
+  WScan o{MAP_ID, 0, 0};
+  special = 0; nhash = 0;
+  const u32 base = w * 32;
+  if (base >= X.n) return o;
+  u32 r[8];
+  load_word(X, base, r);
+  const u32 spw = X.sp[w], fsw = X.fs[w];
+  u32 s0 = 0, s1 = 1, s2 = 2, s3 = 3, s4 = 4, s5 = 5;
+  u32 nls = 0, nnl = 0, spec = 0, nh = 0;
+  bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
+  const u32 m = X.n - base < 32 ? X.n - base : 32;
+#pragma unroll
+  for (u32 j = 0; j < 32; j++) {
+    if (j < m) {
+      const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
+      const bool spl = (spw >> j) & 1u, fsb = (fsw >> j) & 1u;
+      if (fsb) { s0 = s1 = s2 = s3 = s4 = s5 = S_CODE; }
+      if (fsb || prev_nl) { nls++; o.lsp = base + j; }
+      nnl += c == '\n';
+      spec |= (u32)(spl || c >= 0x80 || c == '#');
+      nh += c == '#';
+      if (!spl) {
+        const u32 mp = dfa_class_map(c);
+        s0 = (mp >> (4 * s0)) & 15u; s1 = (mp >> (4 * s1)) & 15u; s2 = (mp >> (4 * s2)) & 15u;
+        s3 = (mp >> (4 * s3)) & 15u; s4 = (mp >> (4 * s4)) & 15u; s5 = (mp >> (4 * s5)) & 15u;
+      }
+      prev_nl = c == '\n' && !spl;
+    }
+  }
+  special = (u8)spec; nhash = nh;
+  o.map = s0 | (s1 << 4) | (s2 << 8) | (s3 << 12) | (s4 << 16) | (s5 << 20);
+  o.lc = ((u64)nls << 32) | nnl;
+  return o;
+}
+
+// K2b: flag the logical lines holding a special byte (word w has one)
+EXS_HD inline void mark_special(const LexW& X, u32 w) {
+  const u32 base = w * 32;
+  u32 li = w ? (u32)(X.wsc[w - 1].lc >> 32) - 1 : NONE;
+  bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
+  const u32 spw = X.sp[w], fsw = X.fs[w];
+  for (u32 j = 0; j < 32 && base + j < X.n; j++) {
+    u8 c = X.src[base + j];
+    bool spl = (spw >> j) & 1u;
+    if (((fsw >> j) & 1u) || prev_nl) li++;
+    if ((spl || c >= 0x80 || c == '#') && !X.special[li]) {
+      X.special[li] = 1;
+      at_add(X.nspecial, 1u);
+    }
+    prev_nl = c == '\n' && !spl;
+  }
+}
+
+// end of the logical line starting at lo: first non-spliced '\n' or the file end
+EXS_HD inline u32 logical_line_end(const LexW& X, u32 lo, u32 fend) {
+  u32 q = lo;
+  while (q < fend && !(X.src[q] == '\n' && !bit_get(X.sp, q))) q++;
+  return q;
+}
+
+EXS_HD inline u32 ffs32(u32 x) {  // index of the lowest set bit (x != 0)
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  return (u32)__ffs((int)x) - 1;
+#else
+  return (u32)__builtin_ctz(x);
+#endif
+}
+EXS_HD inline u32 hib32(u32 x) {  // index of the highest set bit (x != 0)
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  return 31u - (u32)__clz((int)x);
+#else
+  return 31u - (u32)__builtin_clz(x);
+#endif
+}
+EXS_HD inline u32 popc32(u32 x) {
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  return (u32)__popc(x);
+#else
+  return (u32)__builtin_popcount(x);
+#endif
+}
+
+// K3: count (EMIT=false) or emit (EMIT=true) the tokens attributed to word w.
+//
+// Phase 1 (branch-uniform, unrolled): comment-DFA state before every byte and
+// byte-class bitmasks.  Phase 2 (bit arithmetic): token starts of the plain
+// lines -- identifier/number runs (a number is the all-digit prefix of a run
+// that starts with a digit: X & ~(X + S) over the digit mask), single
+// punctuators, string openers and the greedy alignment of punctuator runs.
+// The count pass is a popcount; the emit pass walks the starts in order,
+// interleaved with the special lines this word owns and with file starts.
+template <bool EMIT>
+EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
+  const u32 base = w * 32;
+  if (base >= X.n) return 0;
+  u32 r[8];
+  load_word(X, base, r);
+  const u32 m = X.n - base < 32 ? X.n - base : 32;
+  const u32 valid = m == 32 ? ~0u : ((1u << m) - 1);
+  const u32 spw = X.sp[w], fsw = X.fs[w] & valid;
+  u32 st = S_CODE, lsp0 = 0, li0 = NONE, gnl0 = 0;
+  if (w) {
+    const WScan e = X.wsc[w - 1];
+    st = map_at(e.map, S_CODE);
+    lsp0 = e.lsp;
+    li0 = (u32)(e.lc >> 32) - 1;
+    gnl0 = (u32)e.lc;
+  }
+  const u32 st0 = st;
+  bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
+  // ---- phase 1
+  u32 bl = 0, sm = 0, sbb = 0, nl = 0, lsb = 0;
+  u32 id = 0, dg = 0, ws = 0, ps = 0, sg = 0, qt = 0, sl = 0;
+#pragma unroll
+  for (u32 j = 0; j < 32; j++) {
+    const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
+    const u32 b = 1u << j;
+    const bool spl = (spw & b) != 0, fsb = (fsw & b) != 0;
+    if (fsb) st = S_CODE;
+    const u32 sb = st;
+    if (!spl) st = (dfa_class_map(c) >> (4 * st)) & 15u;
+    if (sb >= S_LINE) bl |= b;                                     // comment text
+    if (sb == S_SLASH && (c == '/' || c == '*') && !spl) bl |= b | (b >> 1);  // opener
+    if (sb == S_STR) sm |= b;                                      // string text and closing quote
+    if (sb == S_BLOCK) sbb |= b;
+    if (c == '\n') nl |= b;
+    if (fsb || prev_nl) lsb |= b;
+    prev_nl = c == '\n' && !spl;
+    if (is_ident_char(c)) id |= b;
+    if (is_digit(c)) dg |= b;
+    if (c == ' ' || c == '\t' || c == '\r') ws |= b;
+    if (is_pset(c)) ps |= b;
+    if (is_single(c)) sg |= b;
+    if (c == '"') qt |= b;
+    if (c == '/') sl |= b;
+  }
+  lsb &= valid; nl &= valid;
+  // ---- special lines: bytes excluded from the plain tokenizer; owned ones
+  u32 spm = 0, own = 0;
+  {
+    u32 li = li0, seg = 0, rest = lsb;
+    bool cur = li != NONE && X.special[li] != 0;
+    while (true) {
+      const u32 nx = rest ? ffs32(rest) : 32;
+      if (cur && nx > seg) spm |= (nx >= 32 ? ~0u : ((1u << nx) - 1)) & ~((1u << seg) - 1);
+      if (nx >= 32) break;
+      li++;
+      cur = X.special[li] != 0;
+      if (cur) own |= 1u << nx;
+      seg = nx;
+      rest &= rest - 1;
+    }
+    spm &= valid;
+  }
+  // file of the word's first byte
+  u32 f = upper_file(X.foff, X.F, base);
+  u32 fend = X.foff[f + 1];
+  // end of the file holding the word's last byte (look-ahead past the word)
+  const u32 fe_last = (fsw & ~1u) ? X.foff[upper_file(X.foff, X.F, base + m - 1) + 1] : fend;
+  // ---- phase 2: code characters and token starts
+  u32 code = valid & ~(bl | sm | spw | nl | spm);
+  if ((sl & code) >> 31) {  // a '/' opening a comment in the next word
+    const u32 q = base + 32;
+    const u8 nx = q < fe_last ? X.src[q] : 0;
+    if (nx == '/' || nx == '*') code &= ~0x80000000u;
+  }
+  const u32 IDc = id & code, DGc = dg & code, ALc = IDc & ~DGc;
+  u32 cin_id = 0, cin_num = 0, cin_ps = 0, pskip = 0;
+  if ((code & 1u) && !(lsb & 1u) && base > 0 && st0 == S_CODE) {
+    const u8 pc = X.src[base - 1];
+    if (is_ident_char(pc)) {
+      cin_id = 1;
+      u32 q = base - 1;  // all-digit run back to its start -> inside a number
+      while (q > lsp0 && is_digit(X.src[q])) q--;
+      cin_num = (is_digit(X.src[q]) || !is_ident_char(X.src[q])) ? 1u : 0u;
+    } else if (is_pset(pc)) {
+      cin_ps = 1;
+      u32 q = base - 1;
+      while (q > lsp0 && is_pset(X.src[q - 1])) q--;
+      while (q < base) {
+        const u8 c1 = q + 1 < fend ? X.src[q + 1] : 0, c2 = q + 2 < fend ? X.src[q + 2] : 0;
+        u8 pid;
+        q += punct_len(X.src[q], c1, c2, pid);
+      }
+      pskip = q - base;
+    }
+  }
+  // runs never continue across a file start (files are concatenated)
+  const u32 rs = IDc & ~(((IDc << 1) | cin_id) & ~fsw);
+  const u32 S = (rs & DGc) | (cin_num & DGc & 1u);
+  u32 P = 0;  // digits of number prefixes, per file segment of the word
+  {
+    u32 lo = 0, rest = fsw & ~1u;
+    while (true) {
+      const u32 hi = rest ? ffs32(rest) : 32;
+      const u32 seg = (hi >= 32 ? ~0u : ((1u << hi) - 1)) & ~((1u << lo) - 1);
+      const u32 Xs = DGc & seg;
+      P |= Xs & ~(Xs + (S & seg)) & seg;
+      if (hi >= 32) break;
+      lo = hi;
+      rest &= rest - 1;
+    }
+  }
+  const u32 idst = rs | (ALc & ((P << 1) | cin_num));
+  const u32 qs = qt & code;
+  const u32 sgs = sg & code;
+  const u32 PSc = ps & code;
+  u32 pst = 0, perr = 0;
+  {
+    u32 runs = PSc & ~(((PSc << 1) | cin_ps) & ~fsw);
+    if (cin_ps && pskip < 32 && ((PSc >> pskip) & 1u)) runs |= 1u << pskip;
+    while (runs) {
+      u32 p = ffs32(runs);
+      runs &= runs - 1;
+      while (p < 32 && ((PSc >> p) & 1u)) {
+        const u8 c = byte_of(r, p);
+        u8 c1 = 0, c2 = 0;
+        if (p + 1 < 32) { if (!((fsw >> (p + 1)) & 1u)) c1 = byte_of(r, p + 1); }
+        else if (base + p + 1 < fe_last) c1 = X.src[base + p + 1];
+        if (c1) {
+          if (p + 2 < 32) { if (!((fsw >> (p + 2)) & 1u)) c2 = byte_of(r, p + 2); }
+          else if (base + p + 2 < fe_last) c2 = X.src[base + p + 2];
+        }
+        u8 pid;
+        const u32 len = punct_len(c, c1, c2, pid);
+        if (pid) pst |= 1u << p; else perr |= 1u << p;
+        p += len;
+      }
+    }
+  }
+  const u32 starts = idst | qs | sgs | pst;
+  u32 ntok = EMIT ? 0 : popc32(starts);
+  const u32 err = (code & ~(id | ws | ps | sg | qt | sl)) | (sl & code) | perr;
+  // ---- phase 3: events in source order
+  u32 fnl0 = X.fnl[f];
+  u8 fmask = 0, live = 3;
+  u32 dcur = 0, dend = 0;
+  auto file_state = [&](u32 pos) {
+    fnl0 = X.fnl[f];
+    if (EMIT) {
+      fmask = 0;
+      for (u32 p = 0; p < 2; p++)
+        if (X.fp[2 * f + p].pp_line == NONE) fmask |= (u8)(1u << p);
+      dcur = X.fdir[f]; dend = X.fdir[f + 1]; live = 3;
+      if (dcur < dend) {
+        u32 lo = dcur, hi = dend;  // first directive at or after pos
+        while (lo < hi) { u32 mid = (lo + hi) / 2; if (X.dirs[mid].pos < pos) lo = mid + 1; else hi = mid; }
+        if (lo > dcur) live = X.dlive[lo - 1];
+        dcur = lo;
+      }
+    }
+  };
+  file_state(base);
+  u32 ev = own | fsw | (EMIT ? (starts | err) : 0u);
+  while (ev) {
+    const u32 j = ffs32(ev);
+    ev &= ev - 1;
+    const u32 i = base + j, bj = 1u << j, below = bj - 1;
+    if (fsw & bj) {
+      while (X.foff[f + 1] <= i) f++;
+      fend = X.foff[f + 1];
+      file_state(i);
+    }
+    const u32 lsj = lsb & (below | bj);
+    const u32 lsp = lsj ? base + hib32(lsj) : lsp0;
+    const u32 gnl = gnl0 + popc32(nl & below);
+    const u8 mask = fmask & live;
+    if (own & bj) {
+      // a special line this word owns: recorded here, lexed by run_lex K3s
+      if (!EMIT) {
+        const u32 k = at_add(X.nsrec, 1u);
+        if (k < X.srcap) {
+          SRec q;
+          q.pos = i; q.file = f; q.line_no = 1 + gnl - fnl0; q.count = 0; q.slot = 0;
+          q.lst = (sbb & bj) ? S_BLOCK : S_CODE; q.kind = 0; q.mask = 0; q.pad = 0;
+          X.srec[k] = q;
+        }
+      } else {
+        u32 lo = 0, hi = X.ns;  // the record of this line
+        while (lo < hi) { u32 mid = (lo + hi) / 2; if (X.srec[mid].pos < i) lo = mid + 1; else hi = mid; }
+        SRec& q = X.srec[lo];
+        if (q.kind >= LK_IFDEF) {
+          if (dcur < dend && X.dirs[dcur].pos == i) { live = X.dlive[dcur]; dcur++; }
+        } else {
+          q.slot = tbase + ntok;
+          q.mask = mask;
+          ntok += q.count;
+        }
+      }
+      continue;
+    }
+    if (!EMIT) continue;
+    if (err & bj)
+      for (u32 p = 0; p < 2; p++)
+        if ((mask >> p) & 1u) at_min(&X.fp[2 * f + p].lex_pos, i);
+    if (!(starts & bj)) continue;
+    const u32 tl = 1 + gnl - fnl0, col = i - lsp + 1;
+    const u8 c = byte_of(r, j);
+    Tok t;
+    t.pos = i; t.line = tl; t.col = col; t.mask = mask; t.flags = 0; t.file = f; t.hv = 0; t.id = 0;
+    if (idst & bj) {
+      const bool num = (DGc & bj) != 0;
+      const u32 run = num ? DGc : IDc;
+      const u32 stop = (~run | fsw) & ~(below | bj);
+      u32 end;
+      if (stop) {
+        end = base + ffs32(stop);
+      } else {
+        end = base + 32;
+        while (end < fend && (num ? is_digit(X.src[end]) : is_ident_char(X.src[end]))) end++;
+      }
+      u64 h = fnv_init(), v = 0;
+      bool ovf = false;
+      for (u32 q = i; q < end; q++) {
+        const u8 ch = q < base + 32 ? byte_of(r, q - base) : X.src[q];
+        if (num) {
+          const u64 nv = v * 10 + (ch - '0');
+          if (v > 1844674407370955161ull || nv < v) ovf = true;
+          v = nv;
+        } else {
+          h = fnv_step(h, ch);
+        }
+      }
+      t.end = end;
+      if (num) { t.kind = TK_INT; t.hv = v; t.flags = ovf ? TF_INT_OVERFLOW : 0; }
+      else { t.kind = TK_IDENT; t.hv = h; t.id = vocab_hash(h, end - i); }
+    } else if (qs & bj) {
+      // the closing quote: first quote in string state after i, unless a newline
+      // or the file end comes first (unterminated: an error and a dead slot)
+      const u32 above = ~(below | bj);
+      const u32 cq = qt & sm & above, nlm = (nl | fsw) & above;
+      u32 close = NONE;
+      bool term;
+      if (cq && (!nlm || ffs32(cq) < ffs32(nlm))) { close = base + ffs32(cq); term = true; }
+      else if (nlm) { term = false; }
+      else {
+        u32 q = base + 32;
+        while (q < fend && X.src[q] != '"' && X.src[q] != '\n') q++;
+        term = q < fend && X.src[q] == '"';
+        close = q;
+      }
+      t.kind = TK_STRING;
+      if (term) {
+        u64 h = fnv_init();
+        for (u32 q = i + 1; q < close; q++) h = fnv_step(h, q < base + 32 ? byte_of(r, q - base) : X.src[q]);
+        const u32 len = close - i - 1;
+        t.pos = len ? i + 1 : close; t.end = close; t.hv = h; t.id = vocab_hash(h, len);
+      } else {
+        for (u32 p = 0; p < 2; p++)
+          if ((mask >> p) & 1u) at_min(&X.fp[2 * f + p].lex_pos, i);
+        t.end = i + 1; t.mask = 0;
+      }
+    } else {
+      u8 c1 = 0, c2 = 0;
+      if (pst & bj) {
+        if (j + 1 < 32) { if (!((fsw >> (j + 1)) & 1u)) c1 = byte_of(r, j + 1); }
+        else if (i + 1 < fend) c1 = X.src[i + 1];
+        if (c1) {
+          if (j + 2 < 32) { if (!((fsw >> (j + 2)) & 1u)) c2 = byte_of(r, j + 2); }
+          else if (i + 2 < fend) c2 = X.src[i + 2];
+        }
+      }
+      u8 pid;
+      const u32 len = punct_len(c, c1, c2, pid);
+      t.kind = TK_PUNCT; t.id = pid; t.end = i + len;
+    }
+    {
+      TokStore ts_{out + ntok, &t};
+    }
+    ntok++;
+  }
+  return ntok;
+}
+
+}  // namespace exs

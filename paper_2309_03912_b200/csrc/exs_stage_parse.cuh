@@ -62,7 +62,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     par_for(F + 1, [=] EXS_HD (i64 f) {
       if (f == F) { fvc[f] = 0; return; }
       bool ok[2];
-      for (int p = 0; p < 2; p++) ok[p] = fp[2 * f + p].pp_line == NONE && fp[2 * f + p].lex_line == NONE;
+      for (int p = 0; p < 2; p++) ok[p] = fp[2 * f + p].pp_line == NONE && fp[2 * f + p].lex_pos == NONE;
       u32 c;
       if (cf[f] & CFG_PLAIN) c = ok[0];
       else if (ok[0] && ok[1] && !split[f]) c = 1;
@@ -98,15 +98,15 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     dfree(f1);
   }
   {
-    FP* fp = L.fp; const u8* cf = L.cfg; const u32* fl = L.fline; const u32* lt = L.line_tok;
+    FP* fp = L.fp; const u8* cf = L.cfg; const u32* ft = L.ftok;
     u32* vf = P.vfile; u8* vp = P.vpass; u32* ve = P.veof; u32* vd = P.vdirect;
     par_for(F, [=] EXS_HD (i64 f) {
       u32 v = fvb[f];
       u32 c = fvc[f];
       if (!c) return;
-      u32 tf0 = lt[fl[f]], tf1 = lt[fl[f + 1]];
-      bool ok0 = fp[2 * f].pp_line == NONE && fp[2 * f].lex_line == NONE;
-      bool ok1 = !(cf[f] & CFG_PLAIN) && fp[2 * f + 1].pp_line == NONE && fp[2 * f + 1].lex_line == NONE;
+      u32 tf0 = ft[f], tf1 = ft[f + 1];
+      bool ok0 = fp[2 * f].pp_line == NONE && fp[2 * f].lex_pos == NONE;
+      bool ok1 = !(cf[f] & CFG_PLAIN) && fp[2 * f + 1].pp_line == NONE && fp[2 * f + 1].lex_pos == NONE;
       if (c == 1 && ok0 && ok1) {
         vf[v] = (u32)f; vp[v] = 3;
         fp[2 * f].view = v; fp[2 * f + 1].view = v;
@@ -134,12 +134,12 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   P.vtok = dalloc<u32>(VT + 1);
   P.vview = dalloc<u32>(VT + 1);
   {
-    const Tok* tk = L.toks; const FP* fp = L.fp; const u32* fl = L.fline; const u32* lt = L.line_tok;
+    const Tok* tk = L.toks; const FP* fp = L.fp; const u32* ft = L.ftok;
     const u32* vb = P.vbase; const u8* vp = P.vpass; u32* vt = P.vtok; u32* vv = P.vview;
     par_for(T, [=] EXS_HD (i64 t) {
       u32 f = tk[t].file;
       u8 m = tk[t].mask;
-      u32 tf0 = lt[fl[f]];
+      u32 tf0 = ft[f];
       for (u32 p = 0; p < 2; p++) {
         u32 v = fp[2 * f + p].view;
         if (v == NONE) continue;

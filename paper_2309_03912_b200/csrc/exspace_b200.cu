@@ -609,14 +609,7 @@ int exs_get_pass_status(exs_handle x, exs_pass_status* out, uint64_t cap) {
   bind_stream(H);
   u32 F = H.L.F;
   std::vector<FP> fp(2 * F);
-  std::vector<u32> lno(H.L.L + 1), lec(H.L.L + 1);
-  std::vector<u16> le(H.L.L + 1);
   if (F) d2h(fp.data(), H.L.fp, sizeof(FP) * 2 * F, H.st);
-  if (H.L.L) {
-    d2h(lno.data(), H.L.line_no, 4ull * H.L.L, H.st);
-    d2h(lec.data(), H.L.line_err_col, 4ull * H.L.L, H.st);
-    d2h(le.data(), H.L.line_err, 2ull * H.L.L, H.st);
-  }
   sync(H.st);
   for (u64 i = 0; i < std::min<u64>(cap, 2ull * F); i++) {
     exs_pass_status& o = out[i];
@@ -624,8 +617,8 @@ int exs_get_pass_status(exs_handle x, exs_pass_status* out, uint64_t cap) {
     const FP& r = fp[i];
     o.exists = r.pp_line != NONE - 1;
     if (!o.exists) continue;
-    if (r.pp_line != NONE) { o.pp_line = lno[r.pp_line]; o.pp_msg = r.pp_msg; }
-    if (r.lex_line != NONE) { o.lex_line = lno[r.lex_line]; o.lex_col = lec[r.lex_line]; o.lex_msg = le[r.lex_line]; }
+    if (r.pp_line != NONE) { o.pp_line = r.pp_line; o.pp_msg = r.pp_msg; }
+    if (r.lex_pos != NONE) { o.lex_line = r.lex_line; o.lex_col = r.lex_col; o.lex_msg = r.lex_msg; }
     o.eof_line = r.eof_line; o.eof_col = r.eof_col; o.view = r.view; o.parse_failed = r.perr;
   }
   API_END
@@ -636,11 +629,8 @@ int exs_get_tokens(exs_handle x, uint32_t file, exs_token* out, uint64_t cap, ui
   Handle& H = x->h;
   bind_stream(H);
   if (file >= H.L.F) throw Err("file index out of range");
-  u32 fl[2], lt[2];
-  d2h(fl, H.L.fline + file, 8, H.st);
-  sync(H.st);
-  d2h(&lt[0], H.L.line_tok + fl[0], 4, H.st);
-  d2h(&lt[1], H.L.line_tok + fl[1], 4, H.st);
+  u32 lt[2];
+  d2h(lt, H.L.ftok + file, 8, H.st);
   sync(H.st);
   u64 cnt = lt[1] - lt[0];
   *n = cnt;

@@ -9,7 +9,7 @@ import random
 
 import pytest
 
-from exs_testlib import GOLDEN_GROUPS, load_golden
+from exs_testlib import GOLDEN_GROUPS, lex_stream_mismatches, load_golden
 from oracle import exs_oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -68,51 +68,16 @@ def test_golden_vectors(X, eng, eng_split, group, split):
     assert not bad, bad[:5]
 
 
-def test_golden_token_streams(X, eng):
-    """K1-K3 lexer parity: per-pass token streams / first E0002 / LexError."""
-    cases = [c for g in ("corpus", "mutations", "synthetic") for c in load_golden(g) if "lex" in c]
-    res = eng.run_batch([unit_of(X, c) for c in cases], want_walks=True)
-    bad = 0
-    h = eng.handle
-    st = h.pass_status(len(cases))
-    data = b"".join(c["text"].encode() for c in cases)
-    offs = [0]
-    for c in cases:
-        offs.append(offs[-1] + len(c["text"].encode()))
-    from paper_2309_03912_b200.messages import Renderer
-    ren = Renderer(data, offs, h.arena())
-    kinds = {1: "ident", 2: "int", 3: "string", 4: "punct", 5: "pragma"}
-    puncts = [None, "<<<", ">>>", "::", "==", "!=", "&&", "||", "++", "{", "}", "(", ")", "<",
-              ">", ",", ";", ".", "!", "="]
-    for f, c in enumerate(cases):
-        toks = h.tokens(f)
-        for p, kind in enumerate(["host", "device"][: len(c["lex"])]):
-            want = c["lex"][kind]
-            s = st[2 * f + p]
-            if "pp_error" in want:
-                ok = s["pp_line"] == want["pp_error"][0]
-            elif "lex_error" in want:
-                ok = (s["pp_line"] == 0 and s["lex_line"] == want["lex_error"][0]
-                      and s["lex_col"] == want["lex_error"][1])
-            else:
-                got = []
-                for t in toks:
-                    if not (int(t["mask"]) >> p) & 1:
-                        continue
-                    k = kinds[int(t["kind"])]
-                    if k == "punct":
-                        text = puncts[int(t["id"])]
-                    elif k == "int":
-                        text = None
-                    else:
-                        text = ren.span_text((int(t["pos"]) << 32) | (int(t["end"]) - int(t["pos"])))
-                    got.append([k, text, int(t["line"]), int(t["col"])])
-                got.append(["eof", "", int(s["eof_line"]), int(s["eof_col"])])
-                exp = [[k, (None if k == "int" else tx), ln, co] for k, tx, ln, co in want["tokens"]]
-                ok = s["pp_line"] == 0 and s["lex_line"] == 0 and got == exp
-            if not ok:
-                bad += 1
-    assert bad == 0
+@pytest.mark.parametrize("source", ["golden", "lexfuzz"])
+def test_golden_token_streams(X, eng, source):
+    """K1-K3 lexer parity: per-pass token streams / first E0002 / LexError,
+    against the reference's own preprocess + tokenize."""
+    if source == "golden":
+        cases = [c for g in ("corpus", "mutations", "synthetic") for c in load_golden(g) if "lex" in c]
+    else:
+        cases = load_golden("lexfuzz")
+    bad = lex_stream_mismatches(X, eng, cases)
+    assert not bad, bad[:8]
 
 
 def _oracle_rows(text, mode):

@@ -52,3 +52,15 @@ def test_oracle_matches_reference(group):
             if got != want:
                 bad.append((c["name"], "lex", kind))
     assert not bad, bad[:5]
+
+
+def test_oracle_lexer_fuzz():
+    """The oracle's preprocess + tokenize against the reference on the lexer
+    fuzz vectors (tests/golden/make_lexfuzz.py)."""
+    bad = []
+    for c in load_golden("lexfuzz"):
+        for kind, want in c["lex"].items():
+            got = _lex(c["text"], kind, c["compiler"], c["relaxed"])
+            if got != want:
+                bad.append((c["name"], kind))
+    assert not bad, bad[:5]

@@ -7,11 +7,16 @@
 
 namespace exs {
 
+// walk counters, each on its own 128-byte line (hot atomics must not share one)
+enum { CNT_INST = 0, CNT_PEND = 1, CNT_SEEDS = 2, CNT_LOG = 3, CNT_OVF = 4, CNT_N = 5 };
+constexpr u32 CNT_STRIDE = 32;
+
 struct WalkState {
   u32 cap_inst = 0, n_inst = 0, levels = 0;
   u64 n_edges = 0, edge_cap = 0, callsites = 0;
   IKey* slots = nullptr;
   u32* sid = nullptr;
+  unsigned long long* sck = nullptr;
   u32 mask = 0;
   Inst* inst = nullptr;
   u32* edges = nullptr;
@@ -27,10 +32,18 @@ struct WalkState {
   u8* visited = nullptr;
   // per walk statistics
   std::vector<u32> w_inst, w_edges, w_demands;
+  u32* ctr(u32 k) const { return counters + k * CNT_STRIDE; }
+  std::vector<u32> read_counters(cudaStream_t st) const {
+    std::vector<u32> raw(CNT_N * CNT_STRIDE), out(8, 0);
+    d2h(raw.data(), counters, 4ull * CNT_N * CNT_STRIDE, st);
+    sync(st);
+    for (u32 k = 0; k < CNT_N; k++) out[k] = raw[k * CNT_STRIDE];
+    return out;
+  }
   void free_all() {
-    void* ps[] = {slots, sid, inst, edges, pend, seeds, log, main_inst, main_key, counters, visited};
+    void* ps[] = {slots, sid, sck, inst, edges, pend, seeds, log, main_inst, main_key, counters, visited};
     for (void* p : ps) dfree(p);
-    slots = nullptr; sid = nullptr; inst = nullptr; edges = nullptr; pend = nullptr; seeds = nullptr;
+    slots = nullptr; sid = nullptr; sck = nullptr; inst = nullptr; edges = nullptr; pend = nullptr; seeds = nullptr;
     log = nullptr; main_inst = nullptr; main_key = nullptr; counters = nullptr; visited = nullptr;
   }
 };
@@ -83,15 +96,15 @@ EXS_HD inline void walker_for(Walker& w, const WalkCfg& C, const WalkBufs& B, u3
 inline WalkBufs make_bufs(WalkState& W, u32* n_diags, Diag* diags, u32 cap_diags, u64* dset,
                           u32 dmask, u32* contract) {
   WalkBufs B;
-  B.slots = W.slots; B.sid = W.sid; B.mask = W.mask; B.inst = W.inst;
-  B.n_inst = W.counters + 0; B.cap_inst = W.cap_inst;
+  B.slots = W.slots; B.sid = W.sid; B.sck = W.sck; B.mask = W.mask; B.inst = W.inst;
+  B.n_inst = W.ctr(CNT_INST); B.cap_inst = W.cap_inst; B.lvl_base = 0;
   B.edges = W.edges;
-  B.pend = W.pend; B.n_pend = W.counters + 1; B.cap_pend = W.cap_pend;
-  B.seeds = W.seeds; B.n_seeds = W.counters + 2; B.cap_seeds = W.cap_seeds;
-  B.log = W.log; B.n_log = W.counters + 3; B.cap_log = W.cap_log;
+  B.pend = W.pend; B.n_pend = W.ctr(CNT_PEND); B.cap_pend = W.cap_pend;
+  B.seeds = W.seeds; B.n_seeds = W.ctr(CNT_SEEDS); B.cap_seeds = W.cap_seeds;
+  B.log = W.log; B.n_log = W.ctr(CNT_LOG); B.cap_log = W.cap_log;
   B.main_inst = W.main_inst; B.main_key = W.main_key;
   B.diags = diags; B.n_diags = n_diags; B.cap_diags = cap_diags; B.dset = dset; B.dmask = dmask;
-  B.overflow = W.counters + 4;
+  B.overflow = W.ctr(CNT_OVF);
   B.contract = contract;
   return B;
 }
@@ -120,11 +133,13 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   W.mask = pow2_at_least(2ull * W.cap_inst) - 1;
   W.slots = dalloc<IKey>((u64)W.mask + 1);
   W.sid = dalloc<u32>((u64)W.mask + 1);
+  W.sck = dalloc<unsigned long long>((u64)W.mask + 1);
   dzero(W.slots, sizeof(IKey) * ((u64)W.mask + 1), st);
   dfill_ff(W.sid, 4ull * ((u64)W.mask + 1), st);
+  dfill_ff(W.sck, 8ull * ((u64)W.mask + 1), st);
   W.inst = dalloc<Inst>(W.cap_inst);
-  W.counters = dalloc<u32>(8);
-  dzero(W.counters, 32, st);
+  W.counters = dalloc<u32>(CNT_N * CNT_STRIDE);
+  dzero(W.counters, 4ull * CNT_N * CNT_STRIDE, st);
   W.main_inst = dalloc<u32>(NW + 1);
   W.main_key = dalloc<unsigned long long>(NW + 1);
   dfill_ff(W.main_inst, 4ull * (NW + 1), st);
@@ -210,24 +225,25 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   u64 edges_used = 0;
   W.callsites = 0;
   while (true) {
-    std::vector<u32> cnt(8);
-    d2h(cnt.data(), W.counters, 32, st);
-    sync(st);
-    if (cnt[4]) { dfree(dtab); dfree(front); return false; }
-    u32 n_now = cnt[0];
+    std::vector<u32> cnt = W.read_counters(st);
+    if (cnt[CNT_OVF]) { dfree(dtab); dfree(front); return false; }
+    u32 n_now = cnt[CNT_INST];
     prof_mark(st);
-    // fixup creators of this level (min creation key wins)
+    // creation keys of this level's instances (min over creators), then the
+    // first creator's location (spacecheck.py:331-337)
+    {
+      Inst* in = W.inst; const unsigned long long* sk = W.sck; const u32 base = prev_n;
+      par_for(n_now - prev_n, [=] EXS_HD (i64 j) { Inst& I = in[base + j]; I.ckey = sk[I.slot]; }, st);
+    }
     {
       const CreateLog* lg = W.log; Inst* in = W.inst;
-      par_for(cnt[3], [=] EXS_HD (i64 j) {
+      par_for(cnt[CNT_LOG], [=] EXS_HD (i64 j) {
         const CreateLog& e = lg[j];
         Inst& I = in[e.inst];
         if (I.ckey == e.ckey) { I.at = e.at; I.fn = e.fn; }
       }, st);
     }
-    dzero(W.counters + 3, 4, st);
-    // ckey: atomicMin over creators
-    // (done inside instantiate via the log; apply min here)
+    dzero(W.ctr(CNT_LOG), 4, st);
     u32 nnew = n_now - prev_n;
     if (!nnew) break;
     prof_mark(st);
@@ -263,10 +279,11 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     W.callsites += S_level;
     grow(W.edges, edge_cap, edges_used + S_level + 1, edges_used, st);
     grow(W.log, log_cap, 2 * S_level + 64, 0, st);
-    u32 npend = cnt[1], nseeds = cnt[2];
+    u32 npend = cnt[CNT_PEND], nseeds = cnt[CNT_SEEDS];
     grow(W.pend, pend_cap, (u64)npend + S_level + 64, npend, st);
     grow(W.seeds, seed_cap, 2ull * (nseeds + S_level) + 64, 2ull * nseeds, st);
     B = bufs();
+    B.lvl_base = n_now;
     {
       Inst* in = W.inst; const u32* fl = front; u64 eu = edges_used;
       par_for(nf, [=] EXS_HD (i64 j) { in[fl[j]].ebase = (u32)(eu + eb[j]); }, st);
@@ -345,10 +362,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     u32* qn = dalloc<u32>(2);
     dzero(qn, 8, st);
     u8* vis = W.visited; const u32* mi = W.main_inst; const u32* sd = W.seeds; const Inst* in = W.inst;
-    std::vector<u32> cnt(8);
-    d2h(cnt.data(), W.counters, 32, st);
-    sync(st);
-    u32 nseeds = cnt[2];
+    std::vector<u32> cnt = W.read_counters(st);
+    u32 nseeds = cnt[CNT_SEEDS];
     // host walks: main; device walks: launch seeds
     par_for(NW, [=] EXS_D (i64 w) {
       if (w & 1) return;
@@ -409,14 +424,12 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   prof_mark(st);
   // ---- pending verdicts (spacecheck.py:634-655)
   {
-    std::vector<u32> cnt(8);
-    d2h(cnt.data(), W.counters, 32, st);
-    sync(st);
+    std::vector<u32> cnt = W.read_counters(st);
     const Pending* pd = W.pend; const Inst* in = W.inst; const u8* vis = W.visited;
     const FnRec* fr = S.fns; const Node* nd = P.nodes; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
     WalkBufs Bc = B;
     EXS_TAG("walk_pending");
-    par_for(cnt[1], [=] EXS_HD (i64 j) {
+    par_for(cnt[CNT_PEND], [=] EXS_HD (i64 j) {
       const Pending& p = pd[j];
       const Inst& I = in[p.caller];
       u8 native = (u8)(p.walk & 1);

@@ -22,7 +22,7 @@ struct Inst {
   u32 ebase, ecnt;          // legal edges (callee instance ids)
   Val tb, hb, ot;           // type binding, hdc binding, owner type
   u8 side, spaces, level, flags;
-  u32 pad;
+  u32 slot;                 // hash slot of the key (creation key lives in sck[slot] during its level)
 };
 enum { IF_BODY = 1, IF_MAIN = 2 };
 
@@ -39,10 +39,12 @@ struct WalkBufs {
   // instance table
   IKey* slots;
   u32* sid;
+  unsigned long long* sck;  // per slot: min creation key of the current level (atomicMin)
   u32 mask;
   Inst* inst;
   u32* n_inst;
   u32 cap_inst;
+  u32 lvl_base;             // ids >= lvl_base were created in the level being walked
   // outputs
   u32* edges;
   Pending* pend;
@@ -127,23 +129,32 @@ EXS_HD inline bool ikey_cas(IKey* slot, const IKey& k, IKey& old) {
 #endif
   return old.a == 0 && old.b == 0;
 }
-EXS_HD inline u32 inst_lookup_or_insert(const WalkBufs& B, const IKey& k, bool& inserted) {
+// Lookup-or-insert of an instance key.  The inserter allocates the id and
+// publishes it in sid[slot]; the record itself is only read by later kernels
+// (kernel boundaries order it), so no fence is needed -- other creators of
+// the same level need the id alone, and "created in this level" is
+// id >= lvl_base (ids are allocated monotonically).
+EXS_HD inline u32 inst_lookup_or_insert(const WalkBufs& B, const IKey& k, bool& inserted, u32& slot) {
   u32 h = (u32)mix64(k.a ^ mix64(k.b)) & B.mask;
   inserted = false;
-  if (ld_volatile(B.n_inst) >= B.cap_inst) { at_or(B.overflow, 1u); return NONE; }
+  // the table holds 2x the id capacity, so probing stays short even past an
+  // overflow; the flag word sits on its own cache line
+  if (ld_volatile(B.overflow) & 1u) return NONE;
   for (u32 probes = 0; probes <= B.mask; probes++) {
     IKey old;
     if (ikey_cas(&B.slots[h], k, old)) {
       u32 id = at_inc_agg(B.n_inst);
       if (id >= B.cap_inst) { at_or(B.overflow, 1u); id = NONE; }
       inserted = true;
-      return id;  // caller initialises the record, then publishes sid[h]
+      slot = h;
+      return id;  // caller initialises the record, then publishes sid[slot]
     }
     if (old.a == k.a && old.b == k.b) {
       u32 id;
       while ((id = ld_volatile(&B.sid[h])) == NONE) {
         if (ld_volatile(B.overflow) & 1u) return NONE;
       }
+      slot = h;
       return id;
     }
     h = (h + 1) & B.mask;
@@ -151,11 +162,8 @@ EXS_HD inline u32 inst_lookup_or_insert(const WalkBufs& B, const IKey& k, bool& 
   at_or(B.overflow, 1u);
   return NONE;
 }
-EXS_HD inline void inst_publish(const WalkBufs& B, const IKey& k, u32 id) {
-  u32 h = (u32)mix64(k.a ^ mix64(k.b)) & B.mask;
-  while (!(B.slots[h].a == k.a && B.slots[h].b == k.b)) h = (h + 1) & B.mask;
-  fence_gpu();  // the record is visible before its id is published
-  at_cas(&B.sid[h], NONE, id);
+EXS_HD inline void inst_publish(const WalkBufs& B, u32 slot, u32 id) {
+  *(volatile u32*)&B.sid[slot] = id;
 }
 
 // ---------------------------------------------------------------------------
@@ -272,25 +280,26 @@ struct Walker {
     k.b = (1ull << 63) | ((u64)tcode(ot) << 32) | ((u64)walk << 3) |
           ((u64)(hb.k == V_HDC ? hb.x : 0) << 1) | want_side;
     bool inserted;
-    u32 id = inst_lookup_or_insert(*B, k, inserted);
+    u32 slot;
+    u32 id = inst_lookup_or_insert(*B, k, inserted, slot);
     if (id == NONE) return NONE;
     unsigned long long ck = ((unsigned long long)clevel << 54) |
                             ((unsigned long long)(parent_rank & 0x3FFFFFFull) << 28) |
                             (my_local & 0xFFFFFFFu);
-    Inst& I = B->inst[id];
     if (inserted) {
+      Inst& I = B->inst[id];
       I.ka = k.a; I.kb = k.b;
-      I.ckey = ck; I.fn = fi; I.orec = orec; I.walk = walk; I.at = at_tok;
+      I.ckey = ~0ull; I.fn = fi; I.orec = orec; I.walk = walk; I.at = at_tok;
       I.ebase = 0; I.ecnt = 0;
       I.tb = tb; I.hb = hb; I.ot = ot;
-      I.side = want_side; I.spaces = sp; I.level = clevel;
+      I.side = want_side; I.spaces = sp; I.level = clevel; I.slot = slot;
       I.flags = (fnn.n & FF_BODY) ? IF_BODY : 0;
       if (K(fnn.tok).id == W_MAIN && !(fr.flags & FR_OWNER)) I.flags |= IF_MAIN;
-      inst_publish(*B, k, id);
+      inst_publish(*B, slot, id);
     }
-    if (I.level == clevel) {
+    if (id >= B->lvl_base) {
       // a creator in this level: log it; the minimum creation key wins
-      if (!inserted) at_min64(&I.ckey, ck);
+      at_min64(&B->sck[slot], ck);
       u32 li = at_inc_agg(B->n_log);
       if (li < B->cap_log) {
         CreateLog& L = B->log[li];

@@ -265,7 +265,7 @@ static void run_demands(Handle& H, bool emit_e1201) {
   dzero(dem, 4ull * (2 * F + 1), st);
   WalkBufs B{};
   B.diags = H.d_diags; B.n_diags = H.d_ndiags; B.cap_diags = H.cap_diags; B.dset = H.d_dset;
-  B.dmask = H.dmask; B.overflow = W.counters + 4;
+  B.dmask = H.dmask; B.overflow = W.ctr(CNT_OVF);
   const u8* cfgs = L.cfg;
   par_for(NE, [=] EXS_HD (i64 i) {
     if (keys[i] == ~0ull) return;
@@ -374,11 +374,11 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       H.W.cap_inst = cap_inst;
       bool ok = run_walk(L, H.P, H.S, H.W, B0, H.sc, st, cap_diags);
       if (ok && (any_div || H.want_demands)) run_demands(H, any_div);
-      walk_ovf = get1(H.W.counters + 4, st);
+      walk_ovf = get1(H.W.ctr(CNT_OVF), st);
       (void)ok;
       if ((walk_ovf & 2) || !(walk_ovf & 5)) break;  // diagnostics overflow: outer loop
       if (walk_ovf & 1) {
-        u32 n_now = get1(H.W.counters, st);
+        u32 n_now = get1(H.W.ctr(CNT_INST), st);
         cap_inst = (u32)std::min<u64>(std::max<u64>(8ull * cap_inst, 2ull * n_now), 0x7FFFFFFFull);
       }
       h2d(H.d_ndiags, &nd0, 4, st);
@@ -404,7 +404,7 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     u32* ct = H.d_contract;
     WalkBufs B{};
     B.diags = H.d_diags; B.n_diags = H.d_ndiags; B.cap_diags = H.cap_diags; B.dset = H.d_dset;
-    B.dmask = H.dmask; B.overflow = H.W.counters + 4;
+    B.dmask = H.dmask; B.overflow = H.W.ctr(CNT_OVF);
     par_for(n_files, [=] EXS_HD (i64 f) {
       if (ct[f]) emit_diag(B, mkdiag((u32)f, 1, 1, C_X9999, M_X_CONTRACT));
     }, st);

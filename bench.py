@@ -258,9 +258,12 @@ def run_gpu_arm(a, rank, world, local):
     lex_bytes = nbytes + 32 * st["tokens"]
     lex_ach = lex_bytes / (statistics.mean(lex_ms) / 1e3) / 1e9
     # per-kernel algorithmic bytes: per step
+    words = nbytes // 32 + 1
     algo = {
-        "lex_emit": nbytes + 32 * st["tokens"],             # source read + token records
-        "lex_directive_count": nbytes + 40 * st["tokens"] // 8,
+        "lex_splice": nbytes + 4 * words,                    # source read + splice bitmap
+        "lex_words": nbytes + 16 * words + words,            # source read + WScan record + flag
+        "lex_count": nbytes + 4 * words,                     # source read + per-word count
+        "lex_emit": nbytes + 32 * st["tokens"],              # source read + token records
         "walk_chunks": 48 * st["callsites"],                 # 48 B per edge
         "walk_roots": 48 * st["functions"],
         "parse_items": 32 * st["tokens"] + 24 * st["tokens"] // 2,

@@ -91,7 +91,9 @@ struct Parser {
   }
 
   // ------------------------------------------------------------ errors
-  EXS_HD bool fail_at(u32 tokpos, u16 msg, u64 a0 = 0, u64 a1 = 0) {
+  // error paths are cold: out of line to keep the parse kernels' instruction
+  // footprint small
+  EXS_HD EXS_NOINLINE bool fail_at(u32 tokpos, u16 msg, u64 a0 = 0, u64 a1 = 0) {
     if (!failed) {
       failed = true;
       loc_of(tokpos, e.line, e.col);
@@ -99,7 +101,7 @@ struct Parser {
     }
     return false;
   }
-  EXS_HD bool fail_tok(u32 gt, u16 msg, u64 a0 = 0, u64 a1 = 0) {
+  EXS_HD EXS_NOINLINE bool fail_tok(u32 gt, u16 msg, u64 a0 = 0, u64 a1 = 0) {
     // error located at a global token (already consumed)
     if (!failed) {
       failed = true;
@@ -112,17 +114,19 @@ struct Parser {
     const Tok& t = v.toks[gt];
     return ((u64)t.pos << 32) | (u64)(t.end - t.pos);
   }
+  // failure at the current token with its text span (out of line, cold)
+  EXS_HD EXS_NOINLINE bool fail_here(u16 msg, u64 a0) { return fail_at(pos, msg, a0, span_of(pos)); }
   // expect(text[, what]) -- tokens of kind ident/punct with the given id
   EXS_HD bool need_p(u8 p, u8 ex) {
     if (at_p(p)) { take(); return true; }
-    return fail_at(pos, M_P_EXPECTED, ex, span_of(pos));
+    return fail_here(M_P_EXPECTED, ex);
   }
   EXS_HD bool need_w(u8 w, u8 ex) {
     if (at_w(w)) { take(); return true; }
-    return fail_at(pos, M_P_EXPECTED, ex, span_of(pos));
+    return fail_here(M_P_EXPECTED, ex);
   }
   EXS_HD bool need_name(u8 what, u32& gt) {
-    if (kind() != TK_IDENT || is_kw()) return fail_at(pos, M_P_EXPECTED_NAME, what, span_of(pos));
+    if (kind() != TK_IDENT || is_kw()) return fail_here(M_P_EXPECTED_NAME, what);
     gt = take();
     return true;
   }

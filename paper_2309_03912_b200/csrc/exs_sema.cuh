@@ -135,11 +135,14 @@ struct Sema {
   EXS_HD const Tok& K(u32 t) const { return T->toks[t]; }
   EXS_HD u64 span(u32 t) const { const Tok& k = K(t); return ((u64)k.pos << 32) | (u64)(k.end - k.pos); }
 
-  EXS_HD u8 subst(u16 sf, u64 a0 = 0, u64 a1 = 0, u64 a2 = 0) {
+  // error setters are cold paths: out of line so the (large) walk kernel's
+  // instruction footprint stays small (profiles/r01_walk: ~30% of stalls were
+  // instruction-cache misses)
+  EXS_HD EXS_NOINLINE u8 subst(u16 sf, u64 a0 = 0, u64 a1 = 0, u64 a2 = 0) {
     err.code = 0; err.msg = sf; err.a0 = a0; err.a1 = a1; err.a2 = a2;
     return ST_SUBST;
   }
-  EXS_HD u8 sema(u16 code, u16 msg, u32 tok, u64 a0 = 0, u64 a1 = 0, u64 a2 = 0) {
+  EXS_HD EXS_NOINLINE u8 sema(u16 code, u16 msg, u32 tok, u64 a0 = 0, u64 a1 = 0, u64 a2 = 0) {
     err.code = code; err.msg = msg; err.line = K(tok).line; err.col = K(tok).col;
     err.a0 = a0; err.a1 = a1; err.a2 = a2;
     return ST_SEMA;
@@ -173,7 +176,14 @@ struct Sema {
   EXS_HD bool env_get(const Env& env, u64 name, Val& out) {
     for (int i = env.n - 1; i >= env.nbase; i--)
       if (env.names[i] == name) { out = env.vals[i]; return true; }
-    if (env.mv_rec != NONE) {
+    if (env.mv_rec != NONE) return env_get_mv(env, name, out);
+    for (int i = env.nbase - 1; i >= 0; i--)
+      if (env.names[i] == name) { out = env.vals[i]; return true; }
+    return false;
+  }
+  // env_get through the member-variable layer (rare): out of line
+  EXS_HD EXS_NOINLINE bool env_get_mv(const Env& env, u64 name, Val& out) {
+    {
       // last member variable with this name whose value evaluates wins
       u32 last_ok = NONE;
       Val lv = vnone();

@@ -7,6 +7,10 @@
 
 namespace exs {
 
+#ifndef EXS_KCH
+#define EXS_KCH 1  // top-level statements per walk_chunks thread (measured: 1 beats 2 and 4 at 1 GB)
+#endif
+
 // walk counters, each on its own 128-byte line (hot atomics must not share one)
 enum { CNT_INST = 0, CNT_PEND = 1, CNT_SEEDS = 2, CNT_LOG = 3, CNT_OVF = 4, CNT_N = 5 };
 constexpr u32 CNT_STRIDE = 32;
@@ -293,7 +297,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     prof_mark(st);
     // walk the frontier: one thread per (instance, chunk of top-level statements)
     {
-      const u32 KCH = 2;
+      const u32 KCH = EXS_KCH;
       u32* wc = dalloc<u32>(nf + 1);
       u32* wb = dalloc<u32>(nf + 1);
       const Inst* in = W.inst; const FnRec* fr = S.fns; const u32* fl = front;

@@ -98,7 +98,8 @@ EXS_HD inline bool set_insert(u64* set, u32 mask, u64 k) {
   return false;
 }
 
-EXS_HD inline void emit_diag(const WalkBufs& B, Diag d) {
+// out of line: called from many sites, executed at a small fraction of them
+EXS_HD EXS_NOINLINE void emit_diag(const WalkBufs& B, Diag d) {
   // a full buffer means the batch is re-run with a larger one: stop early
   // instead of probing an ever fuller dedup set
   if (ld_volatile(B.n_diags) >= B.cap_diags) { at_or(B.overflow, 2); return; }

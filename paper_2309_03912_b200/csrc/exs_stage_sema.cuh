@@ -400,9 +400,11 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       }
     }, st);
     FnRec* fr = S.fns;
-    EXS_TAG("sema_bodyscan");
-    par_for_walk(NF, [=] EXS_HD (i64 i) {
+    // bodies are scanned statement-parallel (BodyScan carries no state across
+    // top-level statements): count, tabulate, scan each statement once
+    par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
+      r.nstmts = 0; r.ncalls = 0;
       if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) return;  // not in the struct any more
       u8 c = cfgs[vf[r.view]];
       u8 mode = c & CFG_MODE_MASK;
@@ -411,39 +413,54 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
         const Tok& t = tk[n.tok];
         emit_diag(B, mkdiag(vf[r.view], t.line, t.col, C_E0001, M_S_COND_SPEC_MODE));
       }
-      r.nstmts = 0;
-      if (n.n & FF_BODY) {
-        BodyScan bs{nd, tk, &tab, r.view, (c & CFG_PLAIN) != 0, 0, &B, vf[r.view], 0};
-        bs.stmts(n.c2);
-        r.ncalls = bs.ncalls;
+      if (n.n & FF_BODY)
         for (u32 s = n.c2; s != NONE; s = nd[s].next) r.nstmts++;
-      }
     }, st);
-    // per-statement tables: chunks of a body are walked in parallel (K6)
+    // per-statement tables: statements of a body are walked in parallel (K6)
     u32* ns = dalloc<u32>(NF + 1);
     u32* sb = dalloc<u32>(NF + 1);
     par_for(NF + 1, [=] EXS_HD (i64 i) { ns[i] = i < NF ? fr[i].nstmts : 0; }, st);
     excl_scan_u32(ns, sb, NF + 1, sc, st);
     S.NS = get1(sb + NF, st);
-    S.stmt_node = dalloc<u32>(S.NS + 1);
-    S.stmt_cs = dalloc<u32>(S.NS + 1);
+    const u32 NSt = S.NS;
+    S.stmt_node = dalloc<u32>(NSt + 1);
+    S.stmt_cs = dalloc<u32>(NSt + 1);
+    u32* sfn = dalloc<u32>(NSt + 1);
+    u32* scnt = dalloc<u32>(NSt + 1);
+    u32* cpre = dalloc<u32>(NSt + 1);
     u32* sn = S.stmt_node; u32* scs = S.stmt_cs;
     par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
       r.stmt_base = sb[i];
       if (!r.nstmts) return;
-      BodyScan bs{nd, tk, &tab, r.view, false, 0, nullptr, 0, 0};
-      u32 k = 0;
+      u32 k = sb[i];
       for (u32 s = nd[r.node].c2; s != NONE; s = nd[s].next, k++) {
-        sn[sb[i] + k] = s;
-        scs[sb[i] + k] = bs.ncalls;
+        sn[k] = s;
+        sfn[k] = (u32)i;
         if (nd[s].kind == N_SVAR) r.flags |= FR_VARDECL;
-        bs.one(s);
       }
+    }, st);
+    EXS_TAG("sema_bodyscan");
+    par_for_walk(NSt + 1, [=] EXS_HD (i64 k) {
+      if (k == NSt) { scnt[k] = 0; return; }
+      const FnRec& r = fr[sfn[k]];
+      u8 c = cfgs[vf[r.view]];
+      BodyScan bs{nd, tk, &tab, r.view, (c & CFG_PLAIN) != 0, 0, &B, vf[r.view], 0};
+      bs.one(sn[k]);
+      scnt[k] = bs.ncalls;
+    }, st);
+    excl_scan_u32(scnt, cpre, NSt + 1, sc, st);
+    par_for(NSt, [=] EXS_HD (i64 k) { scs[k] = cpre[k] - cpre[fr[sfn[k]].stmt_base]; }, st);
+    par_for(NF, [=] EXS_HD (i64 i) {
+      FnRec& r = fr[i];
+      if (r.nstmts) r.ncalls = cpre[r.stmt_base + r.nstmts] - cpre[r.stmt_base];
     }, st);
     sync(st);
     dfree(ns);
     dfree(sb);
+    dfree(sfn);
+    dfree(scnt);
+    dfree(cpre);
   }
   // 7. static assertions (sema.py:200-217)
   {

@@ -7,6 +7,9 @@
 
 namespace exs {
 
+#ifndef EXS_WALK_SORT
+#define EXS_WALK_SORT 1  // order walk work items by statement shape (C2 1 GB: walk 137 -> 76 us/MB)
+#endif
 #ifndef EXS_KCH
 #define EXS_KCH 1  // top-level statements per walk_chunks thread (measured: 1 beats 2 and 4 at 1 GB)
 #endif
@@ -311,8 +314,38 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       u32* ct = B.contract;
       const u32* sn = S.stmt_node; const u32* scs = S.stmt_cs;
       const u32 nfc = nf;
+      // work items in statement-shape order (statement kind, expression kind):
+      // warps then run similar code paths.  Results do not depend on the order
+      // (creation keys and edge slots are order-free).
+      u32* perm = nullptr;
+#if EXS_WALK_SORT
+      {
+        perm = dalloc<u32>(nwi + 1);
+        u64* key = dalloc<u64>(nwi + 1);
+        const Node* nd = P.nodes;
+        par_for(nwi, [=] EXS_HD (i64 i) {
+          u32 lo = 0, hi = nfc;
+          while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (wb[mid] <= (u32)i) lo = mid; else hi = mid; }
+          const FnRec& r = fr[in[fl[lo]].fn];
+          u32 k = ((u32)i - wb[lo]) * KCH;
+          u64 shape = 0;
+          if (k < r.nstmts) {
+            const Node& s = nd[sn[r.stmt_base + k]];
+            u32 sub = s.c0 != NONE ? nd[s.c0].kind : 0;
+            shape = ((u64)s.kind << 8) | sub;
+          }
+          key[i] = shape;
+          perm[i] = (u32)i;
+        }, st);
+        sort_pairs(key, perm, nwi, sc, st, 16);
+        sync(st);
+        dfree(key);
+      }
+#endif
+      const u32* pm = perm;
       EXS_TAG("walk_chunks");
-      par_for_walk(nwi, [=] EXS_HD (i64 i) {
+      par_for_walk(nwi, [=] EXS_HD (i64 ii) {
+        const u32 i = pm ? pm[ii] : (u32)ii;
         u32 lo = 0, hi = nfc;  // instance j with wb[j] <= i < wb[j+1]
         while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (wb[mid] <= (u32)i) lo = mid; else hi = mid; }
         u32 j = lo, c = (u32)i - wb[j];
@@ -327,6 +360,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       sync(st);
       dfree(wc);
       dfree(wb);
+      dfree(perm);
     }
     dfree(ec);
     dfree(eb);

@@ -42,7 +42,7 @@ EXS_HD inline u64 node_base(const u32* item_start, u32 j) { return 2ull * item_s
 // split_min: items at least this many tokens long have their function body
 // parsed statement-parallel (step 4b); exs_set_option(3, n)
 inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& sc, cudaStream_t st,
-                      u32 split_min = 192) {
+                      u32 split_min = 16) {
   const u32 F = L.F, T = L.T;
   // 1. files whose passes see different token sets
   u32* split = dalloc<u32>(F + 1);
@@ -260,8 +260,12 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       if ((u32)(da[i - 1] & 0xFFFFFFFFll) != 1 || pt.kind != TK_PUNCT) return false;
       if (pt.id == P_SEMI) return true;
       if (pt.id == P_RBRACE) {
+        // a block ends a statement unless 'else' or an operator follows (a
+        // brace-initialised temporary: D{}.call(), D{} == x, f(D{}, ...))
         const Tok& t = tk[vt[i]];
-        return !(t.kind == TK_IDENT && t.id == W_ELSE);
+        if (t.kind == TK_IDENT) return t.id != W_ELSE;
+        if (t.kind == TK_PUNCT) return t.id == P_LBRACE || t.id == P_RBRACE || t.id == P_LPAREN || t.id == P_BANG;
+        return true;
       }
       return false;
     };
@@ -277,8 +281,29 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     const u8* cf = L.cfg; const u8* s = L.src; const u32* sp = L.splice;
     Node* nd = P.nodes; u32* ir = P.item_root; u32* ie = P.item_end; u8* ist = P.item_stat;
     PErr* ier = P.item_err; u32* vbad = P.vbad;
+    // items in (header length bucket, first token) order: similar items per warp
+    u32* iperm = dalloc<u32>(I + 1);
+    {
+      u64* key = dalloc<u64>(I + 1);
+      const u32* ib = ibody;
+      par_for(I, [=] EXS_HD (i64 j) {
+        u32 v = iv[j];
+        u32 next = (j + 1 < I && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
+        u32 len = (ib[j] != NONE ? ib[j] + 1 : next) - is[j];  // tokens this thread parses
+        u32 lb = 0;
+        while ((1u << lb) < len && lb < 31) lb++;
+        const Tok& t = tk[vt[is[j]]];
+        key[j] = ((u64)lb << 16) | ((u64)t.kind << 8) | t.id;
+        iperm[j] = (u32)j;
+      }, st);
+      sort_pairs(key, iperm, I, sc, st, 24);
+      sync(st);
+      dfree(key);
+    }
+    const u32* ipm = iperm;
     EXS_TAG("parse_items");
-    par_for_walk(I, [=] EXS_HD (i64 j) {
+    par_for_walk(I, [=] EXS_HD (i64 jj) {
+      const u32 j = ipm[jj];
       u32 v = iv[j];
       u32 next = (j + 1 < I && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
       u8 c = cf[vf[v]];
@@ -303,6 +328,8 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       ier[j] = p.e;
       if (stt || vb[v] + p.pos != next) at_min(&vbad[v], (u32)j);
     }, st);
+    sync(st);
+    dfree(iperm);
   }
   // 4b. statements of the split bodies, in parallel; merged into item status
   if (NSS) {
@@ -317,8 +344,23 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     PErr* serr = dalloc<PErr>(NSS + 1);
     dfill_ff(sbad, 4ull * (I + 1), st);
     const u32 Ic = I, NSSc = NSS;
+    // segments in first-token order: warps parse statements of the same shape
+    u32* sperm = dalloc<u32>(NSS + 1);
+    {
+      u64* key = dalloc<u64>(NSS + 1);
+      par_for(NSS, [=] EXS_HD (i64 k) {
+        const Tok& t = tk[vt[ssc[k]]];
+        key[k] = ((u64)t.kind << 8) | t.id;
+        sperm[k] = (u32)k;
+      }, st);
+      sort_pairs(key, sperm, NSS, sc, st, 16);
+      sync(st);
+      dfree(key);
+    }
+    const u32* spm = sperm;
     EXS_TAG("parse_body_stmts");
-    par_for_walk(NSS, [=] EXS_HD (i64 k) {
+    par_for_walk(NSS, [=] EXS_HD (i64 kk) {
+      const u32 k = spm[kk];
       u32 i0 = ssc[k];
       u32 lo = 0, hi = Ic;
       while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (is[mid] <= i0) lo = mid; else hi = mid; }
@@ -364,7 +406,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       if (first) nd[ir[j]].c2 = sroot[k];
     }, st);
     sync(st);
-    dfree(sroot); dfree(sbad); dfree(sstat); dfree(serr);
+    dfree(sroot); dfree(sbad); dfree(sstat); dfree(serr); dfree(sperm);
   }
   dfree(ss);
   dfree(ibody);

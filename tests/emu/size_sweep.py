@@ -12,6 +12,8 @@ ns = [int(a) for a in sys.argv[1:]] or [125, 250, 500, 1000, 2000, 4000, 10000]
 N = max(ns)
 blobs, offs_all = bench.make_corpus(N, 100_000, 0, os.cpu_count())
 h = _native.Handle(0, os.environ.get("EXS_LIB"))
+if os.environ.get("EXS_SPLIT"):  # statement-parallel body parsing threshold (tokens)
+    h.set_option(3, int(os.environ["EXS_SPLIT"]))
 for n in ns:
     data = np.frombuffer(b"".join(blobs[:n]), np.uint8)
     offs = np.zeros(n + 1, np.uint64); offs[1:] = np.cumsum([len(b) for b in blobs[:n]])

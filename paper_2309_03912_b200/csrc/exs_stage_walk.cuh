@@ -170,25 +170,52 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     const FnRec* fr = S.fns; const RecRec* rr = S.recs; const Node* nd = P.nodes; const Tok* tk = L.toks;
     const FP* fp = L.fp; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
     const Tables* tab = dtab;
-    EXS_TAG("walk_roots");
-    par_for_walk(2ull * NF, [=] EXS_HD (i64 x) {
-      u32 i = (u32)(x >> 1), p = (u32)(x & 1);
+    // root candidates (spacecheck.py:272-283 filters), compacted and ordered by
+    // declaration shape so warps evaluate the same specifier paths
+    auto is_root = [=] EXS_HD (u32 x) -> bool {
+      u32 i = x >> 1, p = x & 1;
       const FnRec& r = fr[i];
       u32 file = vf[r.view];
       u32 walk = 2 * file + p;
-      if (fp[walk].view != r.view || fp[walk].perr) return;
-      if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) return;
+      if (fp[walk].view != r.view || fp[walk].perr) return false;
+      if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) return false;
       const Node& fn = nd[r.node];
-      if (fn.c0 != NONE || !(fn.n & FF_BODY)) return;
-      if (r.rec != NONE && nd[rr[r.rec].node].c0 != NONE) return;
+      if (fn.c0 != NONE || !(fn.n & FF_BODY)) return false;
+      if (r.rec != NONE && nd[rr[r.rec].node].c0 != NONE) return false;
+      u8 mode = cfgs[file] & CFG_MODE_MASK;
+      if (mode == MODE_P2) {
+        bool undec = !(fn.n & (FF_H | FF_D | FF_G));
+        return (tk[fn.tok].id == W_MAIN && r.rec == NONE) || !undec ||
+               (r.rec != NONE && (nd[rr[r.rec].node].n & (SF_H | SF_D | SF_G)));
+      }
+      return true;
+    };
+    u32* rcand = dalloc<u32>(2ull * NF + 1);
+    const u32 NRC = select_idx(2ull * NF, is_root, rcand, L.cnt, sc, st);
+    if (NRC) {
+      u64* key = dalloc<u64>(NRC);
+      const u32* rcc = rcand;
+      par_for(NRC, [=] EXS_HD (i64 k) {
+        const FnRec& r = fr[rcc[k] >> 1];
+        const Node& fn = nd[r.node];
+        key[k] = (u64)(fn.n & (FF_H | FF_D | FF_G | FF_HPRED | FF_DPRED | FF_CX)) |
+                 ((u64)(r.rec != NONE) << 16) | ((u64)(cfgs[vf[r.view]] & CFG_MODE_MASK) << 17);
+      }, st);
+      sort_pairs(key, rcand, NRC, sc, st, 20);
+      sync(st);
+      dfree(key);
+    }
+    const u32* rcc = rcand;
+    EXS_TAG("walk_roots");
+    par_for_walk(NRC, [=] EXS_HD (i64 kk) {
+      const u32 x = rcc[kk];
+      u32 i = x >> 1, p = x & 1;
+      const FnRec& r = fr[i];
+      u32 file = vf[r.view];
+      u32 walk = 2 * file + p;
+      const Node& fn = nd[r.node];
       u8 c = cfgs[file];
       u8 mode = c & CFG_MODE_MASK;
-      bool undec = !(fn.n & (FF_H | FF_D | FF_G));
-      if (mode == MODE_P2) {
-        bool rooted = (tk[fn.tok].id == W_MAIN && r.rec == NONE) || !undec ||
-                      (r.rec != NONE && (nd[rr[r.rec].node].n & (SF_H | SF_D | SF_G)));
-        if (!rooted) return;
-      }
       Walker w;
       w.S.init(tab, r.view, c);
       w.B = &B; w.T = tab; w.file = file; w.walk = walk; w.inst_id = NONE;
@@ -222,6 +249,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         w.instantiate(i, vnone(), vnone(), sd, r.rec, none, ot, fn.tok);
       }
     }, st);
+    sync(st);
+    dfree(rcand);
   }
   prof_mark(st);
   // ---- levels

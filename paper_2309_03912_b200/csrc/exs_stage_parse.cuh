@@ -16,6 +16,7 @@ struct ParseState {
   u32* veof = nullptr;    // 2V (line, col)
   u32* vtok = nullptr;    // VT
   u32* vview = nullptr;   // VT
+  u16* vkid = nullptr;    // VT kind << 8 | id
   u32* item_start = nullptr, *item_view = nullptr, *item_root = nullptr, *item_end = nullptr;
   u8* item_stat = nullptr;
   PErr* item_err = nullptr;
@@ -32,7 +33,7 @@ struct ParseState {
   void free_all() {
     void* ps[] = {vbase, vfile, vpass, veof, vtok, vview, item_start, item_view, item_root,
                   item_end, item_stat, item_err, vfirst, vbad, vstat, vfb_base, vfb_cnt,
-                  fb_items, vfi, fitems, fitem_view, nodes, vdirect};
+                  fb_items, vfi, fitems, fitem_view, nodes, vdirect, vkid};
     for (void* p : ps) dfree(p);
   }
 };
@@ -133,9 +134,11 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   const u32 VT = P.VT;
   P.vtok = dalloc<u32>(VT + 1);
   P.vview = dalloc<u32>(VT + 1);
+  P.vkid = dalloc<u16>(VT + 1);
   {
     const Tok* tk = L.toks; const FP* fp = L.fp; const u32* ft = L.ftok;
     const u32* vb = P.vbase; const u8* vp = P.vpass; u32* vt = P.vtok; u32* vv = P.vview;
+    u16* vkd = P.vkid;
     par_for(T, [=] EXS_HD (i64 t) {
       u32 f = tk[t].file;
       u8 m = tk[t].mask;
@@ -148,6 +151,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
         u32 i = vb[v] + (p ? (s1[t] - s1[tf0]) : (s0[t] - s0[tf0]));
         vt[i] = (u32)t;
         vv[i] = v;
+        vkd[i] = (u16)(((u32)tk[t].kind << 8) | tk[t].id);
       }
     }, st);
   }
@@ -276,6 +280,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   // 4. item-parallel parse
   {
     const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase; const u32* ve = P.veof;
+    const u16* vk = P.vkid;
     const u32* vdr = P.vdirect;
     const u32* is = P.item_start; const u32* iv = P.item_view; const u32* vf = P.vfile;
     const u8* cf = L.cfg; const u8* s = L.src; const u32* sp = L.splice;
@@ -308,7 +313,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       u32 next = (j + 1 < I && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
       u8 c = cf[vf[v]];
       PView pv{tk, vt, vb[v], vb[v + 1] - vb[v], ve[2 * v], ve[2 * v + 1],
-               (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0)};
+               (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0), vk};
       Parser p;
       u64 base = node_base(is, (u32)j);
       // a split item's header owns only the node slots below its body's
@@ -334,6 +339,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   // 4b. statements of the split bodies, in parallel; merged into item status
   if (NSS) {
     const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase; const u32* ve = P.veof;
+    const u16* vk = P.vkid;
     const u32* is = P.item_start; const u32* iv = P.item_view; const u32* vf = P.vfile;
     const u8* cf = L.cfg; const u8* s = L.src; const u32* sp = L.splice;
     Node* nd = P.nodes; u8* ist = P.item_stat; PErr* ier = P.item_err; u32* vbad = P.vbad;
@@ -370,7 +376,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       u32 stop = last ? inext - 1 : ssc[k + 1];  // next segment, or the body's '}'
       u8 c = cf[vf[v]];
       PView pv{tk, vt, vb[v], vb[v + 1] - vb[v], ve[2 * v], ve[2 * v + 1],
-               (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0)};
+               (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0), vk};
       Parser p;
       p.init(pv, nd, (u32)(2ull * i0 + 4ull * j), 2 * (stop - i0), i0 - vb[v]);
       p.v_src = s; p.v_splice = sp;
@@ -455,6 +461,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     u32* fbl = dalloc<u32>(nfb);
     h2d(fbl, fb_views.data(), nfb * 4, st);
     const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase; const u32* ve = P.veof;
+    const u16* vk = P.vkid;
     const u32* vdr = P.vdirect;
     const u32* is = P.item_start; const u32* vfst = P.vfirst; const u32* vf = P.vfile;
     const u8* cf = L.cfg; const u8* s = L.src; const u32* sp = L.splice; Node* nd = P.nodes;
@@ -464,7 +471,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       u32 v = fbl[k];
       u8 c = cf[vf[v]];
       PView pv{tk, vt, vb[v], vb[v + 1] - vb[v], ve[2 * v], ve[2 * v + 1],
-               (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0)};
+               (u8)((c & CFG_PLAIN) ? ((c & CFG_ERASE) ? 1 : 2) : 0), vk};
       u64 base = node_base(is, vfst[v]);
       u64 lim = node_base(is, vfst[v + 1]);
       Parser p;

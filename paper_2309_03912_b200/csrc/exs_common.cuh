@@ -118,8 +118,10 @@ struct Node {
   u32 tok;          // main token (global index)
   u32 c0, c1, c2;   // children / misc
   u32 next;         // sibling link
+  u64 hv;           // the main token's text hash / int value, copied at parse time:
+                    // sema and the walk read names without the 32-byte token record
 };
-static_assert(sizeof(Node) == 24, "node record is 24 bytes");
+static_assert(sizeof(Node) == 32, "node record is 32 bytes (one sector)");
 
 // ---------------------------------------------------------------------------
 // diagnostics (reference: diagnostics.py:15-37)

@@ -139,6 +139,7 @@ struct Parser {
     u32 id = nbase + nused++;
     Node& n = nodes[id];
     n.kind = k; n.sub = 0; n.n = 0; n.tok = tok; n.c0 = n.c1 = n.c2 = NONE; n.next = NONE;
+    n.hv = tok != NONE ? v.toks[tok].hv : 0;
     return id;
   }
   EXS_HD Node& N(u32 id) { return nodes[id]; }

@@ -167,10 +167,10 @@ struct Sema {
   EXS_HD u32 struct_of(u64 name) const { return T->smap.find(vkey(view, name)); }
   EXS_HD u32 first_mvar(u32 rec, u64 name) const {
     for (u32 m = N(T->recs[rec].node).c1; m != NONE; m = N(m).next)
-      if (N(m).kind == N_MVAR && K(N(m).tok).hv == name) return m;
+      if (N(m).kind == N_MVAR && N(m).hv == name) return m;
     return NONE;
   }
-  EXS_HD u64 type_name_hash(u32 tnode) const { return K(N(tnode).tok).hv; }
+  EXS_HD u64 type_name_hash(u32 tnode) const { return N(tnode).hv; }
 
   // env lookup with dict layering; returns false if absent
   EXS_HD bool env_get(const Env& env, u64 name, Val& out) {
@@ -189,7 +189,7 @@ struct Sema {
       Val lv = vnone();
       EErr save = err;
       for (u32 m = N(T->recs[env.mv_rec].node).c1; m != NONE; m = N(m).next) {
-        if (N(m).kind != N_MVAR || K(N(m).tok).hv != name) continue;
+        if (N(m).kind != N_MVAR || N(m).hv != name) continue;
         Val v;
         u8 st = eval(N(m).c0, *env.mv_env, false, v);
         if (contract) return false;
@@ -206,7 +206,7 @@ struct Sema {
   EXS_HD void struct_env(u32 rec, const Val& t, Env& out) const {
     out.clear();
     u32 tp = N(T->recs[rec].node).c0;
-    if (tp != NONE && t.targ) out.add(K(N(tp).tok).hv, vhdc(t.targ));
+    if (tp != NONE && t.targ) out.add(N(tp).hv, vhdc(t.targ));
     out.nbase = out.n;
   }
 
@@ -220,7 +220,7 @@ struct Sema {
   EXS_HD u8 type_of(u32 tr, const Env& env, Val& out) {
     const Node& t = N(tr);
     u8 bt = t.sub;
-    u64 name = K(t.tok).hv;
+    u64 name = t.hv;
     if (bt == BT_INT || bt == BT_BOOL || bt == BT_VOID) {
       if (t.c0 != NONE) return sema(C_E0001, M_S_NO_TARGS_BUILTIN, t.tok, bt);
       out = vnone(); out.k = V_TYPE; out.bt = bt; out.x = name; out.rec = NONE;
@@ -274,7 +274,7 @@ struct Sema {
     if (t.kind == N_TYPE) {
       if (t.c0 != NONE) return subst(SF_EXPECTED_HDC);
       Val b;
-      if (env_get(env, K(t.tok).hv, b)) {
+      if (env_get(env, t.hv, b)) {
         if (b.k == V_HDC) { out = b; return ST_OK; }
         return subst(SF_EXPECTED_HDC);
       }
@@ -314,7 +314,7 @@ struct Sema {
     u8 st = type_of(n.c0, env, t);
     if (st != ST_OK) return st;
     if (t.rec == NONE) return subst(SF_NO_MEMBERS, type_name_arg(t));
-    u32 mv = first_mvar(t.rec, K(n.tok).hv);
+    u32 mv = first_mvar(t.rec, n.hv);
     if (mv == NONE) return subst(SF_NO_MEMBER, type_name_arg(t), span(n.tok));
     Env se;
     struct_env(t.rec, t, se);
@@ -328,13 +328,13 @@ struct Sema {
   EXS_HD EXS_FI u8 eval_(u32 e, const Env& env, bool f, Val& out) {
     const Node& n = N(e);
     switch (n.kind) {
-      case N_INT: out = vint(K(n.tok).hv); return ST_OK;
+      case N_INT: out = vint(n.hv); return ST_OK;
       case N_BOOL: out = vbool(n.sub != 0); return ST_OK;
       case N_HDCV: out = vhdc(n.sub); return ST_OK;
       case N_ARCH: return subst(SF_ARCH);
       case N_NAME: {
         Val b;
-        if (!env_get(env, K(n.tok).hv, b)) {
+        if (!env_get(env, n.hv, b)) {
           if (contract) return ST_SUBST;
           return subst(SF_UNBOUND, span(n.tok));
         }
@@ -427,18 +427,18 @@ struct Sema {
         if (st == ST_OK && v.k != V_HDC) return subst(SF_OTHER);
       }
       if (st != ST_OK) return st;
-      b.set(K(N(tp).tok).hv, v);
+      b.set(N(tp).hv, v);
     }
     if (nargs != fn.sub) return subst(SF_OTHER);
     for (u32 tp = fn.c0; tp != NONE; tp = N(tp).next) {
-      u64 tn = K(N(tp).tok).hv;
+      u64 tn = N(tp).hv;
       Val dummy;
       if (N(tp).sub != 0 || b.get(tn, dummy)) continue;
       u32 i = 0;
       for (u32 p = fn.c1; p != NONE; p = N(p).next, i++) {
         const Node& pty = N(N(p).c0);
         if (pty.sub == BT_NONE || pty.sub == BT_HDC) {
-          if (K(pty.tok).hv == tn && pty.c0 == NONE && argtys[i].k != V_NONE) { b.set(tn, argtys[i]); break; }
+          if (pty.hv == tn && pty.c0 == NONE && argtys[i].k != V_NONE) { b.set(tn, argtys[i]); break; }
         }
       }
     }
@@ -447,7 +447,7 @@ struct Sema {
     for (u32 i = 0; i < nargs && !pending; i++) pending = argtys[i].k != V_NONE;
     for (u32 tp = fn.c0; tp != NONE && !pending; tp = N(tp).next) {
       Val dummy;
-      pending = !b.get(K(N(tp).tok).hv, dummy);
+      pending = !b.get(N(tp).hv, dummy);
     }
     if (!pending) return ST_OK;
     return cand_finish(fi, argtys, nargs, orec, obinds, b);
@@ -464,7 +464,7 @@ struct Sema {
     Env mv_env, cenv;
     bool have_cenv = false;
     for (u32 tp = fn.c0; tp != NONE; tp = N(tp).next) {
-      u64 tn = K(N(tp).tok).hv;
+      u64 tn = N(tp).hv;
       Val dummy;
       if (b.get(tn, dummy)) continue;
       if (N(tp).sub == 1 && N(tp).c0 != NONE) {
@@ -565,7 +565,7 @@ struct Sema {
       merged.nbase = merged.n;
       for (u32 tp = fn.c0; tp != NONE; tp = N(tp).next) {
         const Val& v = N(tp).sub == 0 ? tb : hb;
-        if (v.k != V_NONE) merged.add(K(N(tp).tok).hv, v);
+        if (v.k != V_NONE) merged.add(N(tp).hv, v);
       }
       merged.nbase = merged.n;
       Env mv_env = merged, env = merged;

@@ -315,7 +315,7 @@ struct Walker {
   EXS_HD void add_binds(const Node& fnn, const Val& tb, const Val& hb, Env& e) const {
     for (u32 tp = fnn.c0; tp != NONE; tp = N(tp).next) {
       const Val& v = N(tp).sub == 0 ? tb : hb;
-      if (v.k != V_NONE) e.add(K(N(tp).tok).hv, v);
+      if (v.k != V_NONE) e.add(N(tp).hv, v);
     }
   }
 
@@ -382,7 +382,7 @@ struct Walker {
         // member functions with this name, in member order (dups were removed)
         while (m != NONE) {
           const Node& mn = N(m);
-          if (mn.kind == N_FN && K(mn.tok).hv == mname) {
+          if (mn.kind == N_FN && mn.hv == mname) {
             u32 fx = N(m + 1).tok;  // FNX.tok holds the decl record index
             if (!(T->fns[fx].flags & FR_DUP)) break;
           }
@@ -429,7 +429,7 @@ struct Walker {
     const Node& fnn = N(T->fns[fi].node);
     for (u32 tp = fnn.c0; tp != NONE; tp = N(tp).next) {
       Val v;
-      if (b.get(K(N(tp).tok).hv, v)) {
+      if (b.get(N(tp).hv, v)) {
         if (N(tp).sub == 0) tb = v; else hb = v;
       }
     }
@@ -472,7 +472,7 @@ struct Walker {
       case N_STR:
       case N_HDCV: return vnone();
       case N_NAME: {
-        u64 nm = K(n.tok).hv;
+        u64 nm = n.hv;
         Val v;
         if (local_get(nm, v)) return v;
         for (int i = 0; i < env.n; i++)
@@ -550,7 +550,7 @@ struct Walker {
   }
   EXS_HD EXS_NOINLINE Val free_call_(const Node& n, const Val* tys, u32 na) {
     bool is_std = n.sub == CALL_STD;
-    u64 nm = is_std ? hcombine(word_hash("std::"), K(n.c0).hv) : K(n.tok).hv;
+    u64 nm = is_std ? hcombine(word_hash("std::"), K(n.c0).hv) : n.hv;
     u32 run = is_std ? NONE : T->fmap.find(vkey(S.view, nm));
     if (run == NONE) {
       // builtin_spaces (sema.py:99-102)
@@ -584,7 +584,7 @@ struct Walker {
     if (rt.rec != NONE) {
       for (u32 m = N(T->recs[rt.rec].node).c1; m != NONE; m = N(m).next) {
         const Node& mn = N(m);
-        if (mn.kind == N_FN && K(mn.tok).hv == mname && !(T->fns[N(m + 1).tok].flags & FR_DUP)) { any = true; break; }
+        if (mn.kind == N_FN && mn.hv == mname && !(T->fns[N(m + 1).tok].flags & FR_DUP)) { any = true; break; }
       }
     }
     if (!any) {
@@ -614,7 +614,7 @@ struct Walker {
       case N_SRET: if (n.c0 != NONE) expr(n.c0); break;
       case N_SVAR: {
         Val t = soft_type(n.c0, N(n.c0).tok);
-        local_set(K(n.tok).hv, t);
+        local_set(n.hv, t);
         break;
       }
       case N_SIF: {
@@ -630,7 +630,7 @@ struct Walker {
         expr(n.c1);
         u32 mark = nloc;
         Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int");
-        local_set(K(n.tok).hv, t);
+        local_set(n.hv, t);
         stmts(n.c2);
         nloc = mark;
         break;
@@ -653,7 +653,7 @@ struct Walker {
     asp = base;
   }
   EXS_HD EXS_NOINLINE void launch_dispatch(const Node& n, const Val* tys, u32 na) {
-    u32 run = T->fmap.find(vkey(S.view, K(n.tok).hv));
+    u32 run = T->fmap.find(vkey(S.view, n.hv));
     if (run == NONE) return;
     u32 fi; Val tb, hb;
     Env none; none.clear();
@@ -681,12 +681,12 @@ struct Walker {
     silent = k0 != 0;
     for (u32 p = fnn.c1; p != NONE; p = N(p).next) {
       Val t = soft_type(N(p).c0, N(p).tok);
-      local_set(K(N(p).tok).hv, t);
+      local_set(N(p).hv, t);
     }
     if (T->fns[fn].flags & FR_VARDECL) {
       for (u32 k = 0; k < k0; k++) {
         const Node& s = N(stmt_node[sbase + k]);
-        if (s.kind == N_SVAR) local_set(K(s.tok).hv, soft_type(s.c0, N(s.c0).tok));
+        if (s.kind == N_SVAR) local_set(s.hv, soft_type(s.c0, N(s.c0).tok));
       }
     }
     silent = false;

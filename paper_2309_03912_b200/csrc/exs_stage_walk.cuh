@@ -128,6 +128,37 @@ void grow(T*& p, u64& cap_or_dummy, u64 need, u64 used, cudaStream_t st) {
   cap_or_dummy = nc;
 }
 
+// Grow the instance store to hold `need` ids and rehash the keys of the n
+// existing instances (between levels only: no creator is running).  A level
+// creates at most two instances per call site (spacecheck.py:591-596), so
+// growing before each level replaces the overflow-and-rerun of the whole walk.
+inline void grow_inst(WalkState& W, u64 need, u32 n, cudaStream_t st) {
+  if (need <= W.cap_inst) return;
+  const u32 cap = (u32)std::min<u64>(std::max<u64>(need + need / 2, 2ull * W.cap_inst), 0x7FFFFFFFull);
+  Inst* in = dalloc<Inst>(cap);
+  if (n) d2d(in, W.inst, sizeof(Inst) * (u64)n, st);
+  const u32 mask = (u32)(pow2_at_least(2ull * cap) - 1);
+  IKey* slots = dalloc<IKey>((u64)mask + 1);
+  u32* sid = dalloc<u32>((u64)mask + 1);
+  unsigned long long* sck = dalloc<unsigned long long>((u64)mask + 1);
+  dzero(slots, sizeof(IKey) * ((u64)mask + 1), st);
+  dfill_ff(sid, 4ull * ((u64)mask + 1), st);
+  dfill_ff(sck, 8ull * ((u64)mask + 1), st);
+  par_for(n, [=] EXS_HD (i64 i) {
+    Inst& I = in[i];
+    IKey k; k.a = I.ka; k.b = I.kb;
+    u32 h = (u32)mix64(k.a ^ mix64(k.b)) & mask;
+    IKey old;
+    while (!ikey_cas(&slots[h], k, old)) h = (h + 1) & mask;
+    sid[h] = (u32)i;
+    I.slot = h;
+  }, st);
+  sync(st);
+  dfree(W.inst); dfree(W.slots); dfree(W.sid); dfree(W.sck);
+  W.inst = in; W.slots = slots; W.sid = sid; W.sck = sck;
+  W.cap_inst = cap; W.mask = mask;
+}
+
 // returns false if a buffer overflowed (caller grows and retries)
 inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, WalkBufs& B0,
                      Scratch& sc, cudaStream_t st, u32 diag_cap) {
@@ -318,6 +349,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     u32 npend = cnt[CNT_PEND], nseeds = cnt[CNT_SEEDS];
     grow(W.pend, pend_cap, (u64)npend + S_level + 64, npend, st);
     grow(W.seeds, seed_cap, 2ull * (nseeds + S_level) + 64, 2ull * nseeds, st);
+    grow_inst(W, (u64)n_now + 2ull * S_level + 64, n_now, st);
     B = bufs();
     B.lvl_base = n_now;
     {

@@ -376,7 +376,26 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       if (ok && (any_div || H.want_demands)) run_demands(H, any_div);
       walk_ovf = get1(H.W.ctr(CNT_OVF), st);
       (void)ok;
-      if ((walk_ovf & 2) || !(walk_ovf & 5)) break;  // diagnostics overflow: outer loop
+      if (!(walk_ovf & 7)) break;
+      if ((walk_ovf & 2) && !(get1(ovf, st) & 2) && nd0 <= cap_diags) {
+        // diagnostics overflowed inside the walk: grow the buffer and its dedup
+        // set, keep the diagnostics of the earlier stages, re-run the walk only
+        const u32 nd_now = get1(H.d_ndiags, st);
+        const u32 ncap = (u32)std::min<u64>(4ull * std::max(nd_now, cap_diags), 0x7FFFFFFFull);
+        Diag* ndg = dalloc<Diag>(ncap);
+        if (nd0) d2d(ndg, H.d_diags, sizeof(Diag) * (u64)nd0, st);
+        const u32 nmask = pow2_at_least(2ull * ncap) - 1;
+        u64* nset = dalloc<u64>((u64)nmask + 1);
+        dzero(nset, 8ull * ((u64)nmask + 1), st);
+        par_for(nd0, [=] EXS_HD (i64 i) { set_insert(nset, nmask, diag_hash(ndg[i])); }, st);
+        dfree(H.d_diags); dfree(H.d_dset); dfree(dset_snap);
+        H.d_diags = ndg; H.d_dset = nset; H.dmask = nmask; H.cap_diags = ncap; cap_diags = ncap;
+        B0.diags = ndg; B0.cap_diags = ncap; B0.dset = nset; B0.dmask = nmask;
+        dset_snap = dalloc<u64>((u64)nmask + 1);
+        d2d(dset_snap, nset, 8ull * ((u64)nmask + 1), st);
+      } else if (walk_ovf & 2) {
+        break;  // the earlier stages overflowed too: outer loop
+      }
       if (walk_ovf & 1) {
         u32 n_now = get1(H.W.ctr(CNT_INST), st);
         cap_inst = (u32)std::min<u64>(std::max<u64>(8ull * cap_inst, 2ull * n_now), 0x7FFFFFFFull);

@@ -151,3 +151,15 @@ void b() { D{}.call(); }
 """
     got = [(d.code, d.loc.line) for d in X.check_unit(src, "u.mcu")]
     assert got == [("E1001", 2), ("E1001", 3)]
+
+
+def test_diagnostic_overflow_regrows_inside_the_walk(X, eng):
+    """A unit whose walk emits more diagnostics than the initial buffer holds
+    (C4 shape: ~87k E1xxx) is re-walked with a grown buffer, keeping the
+    earlier stages' diagnostics -- same ordered set as the oracle."""
+    from paper_2309_03912_b200 import synth
+    text = synth.gen_callgraph(20000, 10, 3)
+    a = eng.run_batch([(text, "c4.cu", X.CompileProfile(), X.Mode.SOUND, X.TraitConfig())])[0]
+    assert eng.last_stats["retries"] >= 1
+    rows, _, _ = _oracle_rows(text, "sound")
+    assert as_rows(a) == rows

@@ -295,11 +295,17 @@ def run_gpu_arm(a, rank, world, local):
                                      "diagnostics", "retries")},
         "stage_ms": {k: statistics.mean(s[k] for s in steps) for k in ("ms_lex", "ms_parse", "ms_sema", "ms_walk")},
         "gpu_launches": int(sum(s["gpu_launches"] for s in steps)),
+        # achieved = algorithmic bytes of one launch / its mean launch time (CUDA
+        # events on the launching stream); traffic = measured DRAM bytes of one
+        # launch (ncu dram__bytes_{read,write}.sum, profiles/ncu_traffic.json)
         "roofline": ({"bound": "hbm", "achieved": per_kernel[dom].get("achieved_gbs"),
                       "peak": HBM_PEAK, "unit": "GB/s", "frac": per_kernel[dom].get("frac"),
-                      "traffic": traffic_db.get(dom, {}).get("dram_bytes_per_step"),
-                      "algorithmic_bytes": algo.get(dom), "kernel": dom,
-                      "share_of_step": per_kernel[dom]["share"], "peak_source": HBM_PEAK_SRC}
+                      "traffic": traffic_db.get(dom, {}).get("dram_bytes_per_launch"),
+                      "algorithmic_bytes": (algo[dom] / max(1.0, per_kernel[dom]["launches_per_step"])
+                                            if dom in algo else None),
+                      "kernel": dom, "launches_per_step": per_kernel[dom]["launches_per_step"],
+                      "share_of_step": per_kernel[dom]["share"], "peak_source": HBM_PEAK_SRC,
+                      "traffic_source": traffic_db.get(dom, {}).get("source")}
                      if dom else None),
         "roofline_lex_stage": {"bound": "hbm", "achieved": lex_ach, "peak": HBM_PEAK, "unit": "GB/s",
                                "frac": lex_ach / HBM_PEAK, "kernel": "lex stage K1-K3 (all launches)"},

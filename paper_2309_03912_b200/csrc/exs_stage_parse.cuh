@@ -307,7 +307,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     }
     const u32* ipm = iperm;
     EXS_TAG("parse_items");
-    par_for_walk(I, [=] EXS_HD (i64 jj) {
+    par_for_parse(I, [=] EXS_HD (i64 jj) {
       const u32 j = ipm[jj];
       u32 v = iv[j];
       u32 next = (j + 1 < I && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
@@ -365,7 +365,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     }
     const u32* spm = sperm;
     EXS_TAG("parse_body_stmts");
-    par_for_walk(NSS, [=] EXS_HD (i64 kk) {
+    par_for_parse(NSS, [=] EXS_HD (i64 kk) {
       const u32 k = spm[kk];
       u32 i0 = ssc[k];
       u32 lo = 0, hi = Ic;

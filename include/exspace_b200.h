@@ -98,6 +98,10 @@ int exs_run_device(exs_handle h, const uint8_t* d_bytes, uint64_t n_bytes,
 int exs_get_stats(exs_handle h, exs_stats* out);
 /* diagnostics ordered by (file, line, col, code), duplicates removed */
 int exs_get_diags(exs_handle h, exs_diag* out, uint64_t cap, uint64_t* n);
+/* Zero-copy view of the ordered diagnostics of the last run: *out points to
+ * *n records in page-locked host memory owned by the handle, valid until the
+ * next exs_run / exs_run_device / exs_destroy on it. */
+int exs_diags_view(exs_handle h, const exs_diag** out, uint64_t* n);
 int exs_get_arena(exs_handle h, uint8_t* out, uint64_t cap, uint64_t* n);
 int exs_get_pass_status(exs_handle h, exs_pass_status* out, uint64_t cap);
 int exs_get_tokens(exs_handle h, uint32_t file, exs_token* out, uint64_t cap, uint64_t* n);

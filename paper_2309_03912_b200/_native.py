@@ -56,7 +56,7 @@ class Stats(C.Structure):
 
 EXPORTS = [
     "exs_create", "exs_destroy", "exs_last_error", "exs_run", "exs_run_device", "exs_get_stats",
-    "exs_get_diags", "exs_get_arena", "exs_get_pass_status", "exs_get_tokens",
+    "exs_get_diags", "exs_diags_view", "exs_get_arena", "exs_get_pass_status", "exs_get_tokens",
     "exs_get_walk_stats", "exs_describe", "exs_set_option", "exs_stage_times", "exs_profile_text",
 ]
 
@@ -81,6 +81,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     lib.exs_run_device.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint32, vp]
     lib.exs_get_stats.argtypes = [vp, C.POINTER(Stats)]
     lib.exs_get_diags.argtypes = [vp, vp, C.c_uint64, u64p]
+    lib.exs_diags_view.argtypes = [vp, C.POINTER(C.c_void_p), u64p]
     lib.exs_get_arena.argtypes = [vp, vp, C.c_uint64, u64p]
     lib.exs_get_pass_status.argtypes = [vp, vp, C.c_uint64]
     lib.exs_get_tokens.argtypes = [vp, C.c_uint32, vp, C.c_uint64, u64p]
@@ -144,13 +145,22 @@ class Handle:
         self._check(self.lib.exs_get_stats(self.h, C.byref(s)))
         return s.as_dict()
 
-    def diags(self) -> np.ndarray:
+    def diags(self, copy: bool = True) -> np.ndarray:
+        """Ordered diagnostic records of the last run.  copy=False returns a
+        read-only view of the handle's page-locked buffer (valid until the
+        next run on this handle) instead of copying it."""
         n = C.c_uint64()
-        self._check(self.lib.exs_get_diags(self.h, None, 0, C.byref(n)))
-        out = np.zeros(n.value, dtype=DIAG_DTYPE)
-        if n.value:
-            self._check(self.lib.exs_get_diags(self.h, _ptr(out), n.value, C.byref(n)))
-        return out
+        p = C.c_void_p()
+        self._check(self.lib.exs_diags_view(self.h, C.byref(p), C.byref(n)))
+        if not n.value:
+            return np.zeros(0, dtype=DIAG_DTYPE)
+        buf = (C.c_uint8 * (n.value * DIAG_DTYPE.itemsize)).from_address(p.value)
+        raw = np.frombuffer(buf, dtype=np.uint8)
+        if copy:  # a byte copy: numpy copies structured records field by field
+            return raw.copy().view(DIAG_DTYPE)
+        view = raw.view(DIAG_DTYPE)
+        view.flags.writeable = False
+        return view
 
     def arena(self) -> bytes:
         n = C.c_uint64()

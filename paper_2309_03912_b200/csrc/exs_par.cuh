@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) k_for(F f, i64 n) {
 // latency-bound walkers: cap registers so enough warps fit per SM
 // (EXS_WALK_MINB blocks of 128 threads: 8 -> 64 regs, 6 -> 80, 4 -> 128)
 #ifndef EXS_WALK_MINB
-#define EXS_WALK_MINB 16  // measured on C2 1 GB: 16 beats 12 (-4% walk), 8 (+17%)
+#define EXS_WALK_MINB 8  // C2 1 GB after the shape sort: 16/12/8/4 -> 76.3/73.4/72.5/74.6 us/MB walk
 #endif
 template <class F>
 __global__ void __launch_bounds__(128, EXS_WALK_MINB) k_for_walk(F f, i64 n) {

@@ -143,7 +143,10 @@ struct Handle {
   u32* d_ndiags = nullptr;
   u32* d_contract = nullptr;
   u8* d_src_owned = nullptr;
-  std::vector<Diag> diags;
+  // ordered diagnostics on the host: pinned, so the D2H runs at full PCIe
+  // speed and exs_diags_view can hand them out without a copy
+  Diag* diags = nullptr;
+  u64 n_diags_host = 0, diags_host_cap = 0;
   std::vector<u32> walk_inst, walk_edges, walk_dem;
   exs_stats stats{};
   float t_stage[4] = {0, 0, 0, 0};
@@ -162,6 +165,11 @@ struct Handle {
   }
   ~Handle() {
     reset();
+#ifndef EXS_EMU
+    if (diags) cudaFreeHost(diags);
+#else
+    free(diags);
+#endif
     dfree(d_src_owned);
     dfree(sc.p);
     sc.p = nullptr;
@@ -440,9 +448,20 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     sort_pairs(k, ix, nd, H.sc, st);
     Diag* out = dalloc<Diag>(nd + 1);
     par_for(nd, [=] EXS_HD (i64 i) { out[i] = dd[ix[i]]; }, st);
-    H.diags.resize(nd);
+    if ((u64)nd > H.diags_host_cap) {
+      u64 cap = (u64)nd + nd / 4 + 1024;
+#ifndef EXS_EMU
+      if (H.diags) cudaFreeHost(H.diags);
+      CK(cudaHostAlloc((void**)&H.diags, cap * sizeof(Diag), cudaHostAllocDefault));
+#else
+      free(H.diags);
+      H.diags = (Diag*)malloc(cap * sizeof(Diag));
+#endif
+      H.diags_host_cap = cap;
+    }
+    H.n_diags_host = nd;
     Timer td(st);
-    if (nd) d2h(H.diags.data(), out, sizeof(Diag) * (u64)nd, st);
+    if (nd) d2h(H.diags, out, sizeof(Diag) * (u64)nd, st);
     sync(st);
     H.stats.ms_d2h = td.stop();
     dfree(out); dfree(k); dfree(ix);
@@ -603,10 +622,18 @@ int exs_stage_times(exs_handle x, float* out4) {
 
 int exs_get_diags(exs_handle x, exs_diag* out, uint64_t cap, uint64_t* n) {
   API_TRY
-  auto& d = x->h.diags;
-  *n = d.size();
-  u64 m = std::min<u64>(cap, d.size());
-  if (m) memcpy(out, d.data(), m * sizeof(Diag));
+  const Handle& H = x->h;
+  *n = H.n_diags_host;
+  u64 m = std::min<u64>(cap, H.n_diags_host);
+  if (m) memcpy(out, H.diags, m * sizeof(Diag));
+  API_END
+}
+
+int exs_diags_view(exs_handle x, const exs_diag** out, uint64_t* n) {
+  API_TRY
+  const Handle& H = x->h;
+  *n = H.n_diags_host;
+  *out = reinterpret_cast<const exs_diag*>(H.diags);
   API_END
 }
 

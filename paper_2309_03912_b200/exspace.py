@@ -285,7 +285,7 @@ class Engine:
         with self.lock:
             self.handle.set_option(1, 1 if want_walks else 0)
             self.handle.run(data, offsets, cfg)
-            recs = self.handle.diags()
+            recs = self.handle.diags(copy=False)  # consumed under the lock, before the next run
             arena = self.handle.arena()
             self.last_stats = self.handle.stats()
             walks = self.handle.walk_stats(len(units)) if want_walks else None

@@ -87,13 +87,13 @@ struct LexW {
   const u8* src; u32 n; bool vec;  // vec: 16-byte aligned source, vector loads allowed
   const u32* sp; const u32* fs;    // splice / file-start bitmaps
   const WScan* wsc;                // inclusive scan (word w reads wsc[w-1])
-  u8* special;                     // per logical line
+  u32* special;                    // per logical line: 0 plain, else special (count pass: SRec index + 1)
   const u32* foff; u32 F; const u8* cfg;
   const u32* fnl;                  // global newline count before each file start
   u32* nspecial;                   // special lines (upper bound, mark pass)
   // count pass: special-line records
   SRec* srec; u32* nsrec; u32 srcap;
-  u32 ns;                          // emit pass: special lines, sorted by position
+  u32 ns;                          // special lines recorded
   // emit pass
   const u32* fdir; const DirRec* dirs; const u8* dlive; FP* fp;
 };
@@ -140,12 +140,25 @@ EXS_HD inline u32 punct_len(u8 c, u8 c1, u8 c2, u8& pid) {
   return 1;
 }
 
-EXS_HD inline u8 byte_of(const u32 r[8], u32 j) {
-  u32 k = j >> 2;
-  u32 v = k < 4 ? (k < 2 ? (k == 0 ? r[0] : r[1]) : (k == 2 ? r[2] : r[3]))
-                : (k < 6 ? (k == 4 ? r[4] : r[5]) : (k == 6 ? r[6] : r[7]));
-  return (u8)(v >> (8 * (j & 3)));
+EXS_HD inline u32 word_of(const u32 r[8], u32 k) {  // r[k] without local memory
+  return k < 4 ? (k < 2 ? (k == 0 ? r[0] : r[1]) : (k == 2 ? r[2] : r[3]))
+               : (k < 6 ? (k == 4 ? r[4] : r[5]) : (k == 6 ? r[6] : r[7]));
 }
+EXS_HD inline u8 byte_of(const u32 r[8], u32 j) { return (u8)(word_of(r, j >> 2) >> (8 * (j & 3))); }
+// sequential reader of a token's bytes: registers inside the word (one select
+// chain per 4 bytes), global memory past it
+struct ByteCursor {
+  const u32* r; const u8* src; u32 base, cur;
+  u32 wv;
+  EXS_HD u8 at(u32 q) {
+    if (q < base + 32) {
+      const u32 j = q - base;
+      if ((j >> 2) != cur) { cur = j >> 2; wv = word_of(r, cur); }
+      return (u8)(wv >> (8 * (j & 3)));
+    }
+    return src[q];
+  }
+};
 
 EXS_HD inline void load_word(const LexW& X, u32 base, u32 r[8]) {
 #if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
@@ -441,6 +454,7 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
     const u8 mask = fmask & live;
     if (own & bj) {
       // a special line this word owns: recorded here, lexed by run_lex K3s
+      const u32 lij = li0 + popc32(lsb & (below | bj));  // this line's index
       if (!EMIT) {
         const u32 k = at_add(X.nsrec, 1u);
         if (k < X.srcap) {
@@ -448,11 +462,10 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
           q.pos = i; q.file = f; q.line_no = 1 + gnl - fnl0; q.count = 0; q.slot = 0;
           q.lst = (sbb & bj) ? S_BLOCK : S_CODE; q.kind = 0; q.mask = 0; q.pad = 0;
           X.srec[k] = q;
+          X.special[lij] = k + 1;  // the emit pass finds its record here
         }
       } else {
-        u32 lo = 0, hi = X.ns;  // the record of this line
-        while (lo < hi) { u32 mid = (lo + hi) / 2; if (X.srec[mid].pos < i) lo = mid + 1; else hi = mid; }
-        SRec& q = X.srec[lo];
+        SRec& q = X.srec[X.special[lij] - 1];
         if (q.kind >= LK_IFDEF) {
           if (dcur < dend && X.dirs[dcur].pos == i) { live = X.dlive[dcur]; dcur++; }
         } else {
@@ -485,8 +498,9 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
       }
       u64 h = fnv_init(), v = 0;
       bool ovf = false;
+      ByteCursor bc{r, X.src, base, 8u, 0u};
       for (u32 q = i; q < end; q++) {
-        const u8 ch = q < base + 32 ? byte_of(r, q - base) : X.src[q];
+        const u8 ch = bc.at(q);
         if (num) {
           const u64 nv = v * 10 + (ch - '0');
           if (v > 1844674407370955161ull || nv < v) ovf = true;
@@ -516,7 +530,8 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
       t.kind = TK_STRING;
       if (term) {
         u64 h = fnv_init();
-        for (u32 q = i + 1; q < close; q++) h = fnv_step(h, q < base + 32 ? byte_of(r, q - base) : X.src[q]);
+        ByteCursor bc{r, X.src, base, 8u, 0u};
+        for (u32 q = i + 1; q < close; q++) h = fnv_step(h, bc.at(q));
         const u32 len = close - i - 1;
         t.pos = len ? i + 1 : close; t.end = close; t.hv = h; t.id = vocab_hash(h, len);
       } else {

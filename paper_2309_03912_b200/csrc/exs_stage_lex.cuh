@@ -37,7 +37,7 @@ struct LexState {
   u32* splice = nullptr;    // W bitmap
   WScan* wsc = nullptr;     // W inclusive word scan
   u8* wflag = nullptr;      // W: word holds a special byte
-  u8* special = nullptr;    // L: logical line holds a special byte
+  u32* special = nullptr;   // L: logical line holds a special byte (0 / SRec index + 1)
   u32* fnl = nullptr;       // F+1 global newline count before each file
   u32* wtok = nullptr;      // W+1 first token of each word
   u32* ftok = nullptr;      // F+1 first token of each file
@@ -126,8 +126,8 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
     WScan last = get1(S.wsc + (W - 1), st);
     S.L = (u32)(last.lc >> 32);
   }
-  S.special = dalloc<u8>(S.L + 1);
-  dzero(S.special, S.L + 1, st);
+  S.special = dalloc<u32>(S.L + 1);
+  dzero(S.special, 4ull * (S.L + 1), st);
   X.special = S.special;
   X.nspecial = S.cnt + 3;
   {
@@ -185,18 +185,8 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
       r.count = lex_line(s, sp, r.pos, hi, r.lst, r.line_no, r.file, 0, nullptr, &e);
       if (r.count) at_add(&wcnt[r.pos >> 5], r.count);
     }, st);
-    // records in source order (the emit pass finds its lines by position)
-    u64* kk = dalloc<u64>(NS);
-    u32* kv = dalloc<u32>(NS);
-    par_for(NS, [=] EXS_HD (i64 i) { kk[i] = srec[i].pos; kv[i] = (u32)i; }, st);
-    sort_pairs(kk, kv, NS, sc, st, 32);
-    S.srec = dalloc<SRec>(NS);
-    SRec* so = S.srec;
-    par_for(NS, [=] EXS_HD (i64 i) { so[i] = srec[kv[i]]; }, st);
-    sync(st);
-    dfree(kk); dfree(kv);
   }
-  dfree(srec);
+  S.srec = srec;  // the emit pass finds a line's record through special[line]
   X.srec = S.srec; X.ns = NS;
   S.wtok = dalloc<u32>(W + 1);
   excl_scan_u32(wcnt, S.wtok, W + 1, sc, st);

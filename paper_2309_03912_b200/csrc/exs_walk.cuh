@@ -299,8 +299,12 @@ struct Walker {
       inst_publish(*B, slot, id);
     }
     if (id >= B->lvl_base) {
-      // a creator in this level: log it; the minimum creation key wins
+      // a creator in this level: the minimum creation key wins.  The inserter's
+      // location and decl are already in the record, so only the other
+      // creators are logged (the post-level fixup applies the log entry whose
+      // key is the minimum; none matches when the inserter holds it)
       at_min64(&B->sck[slot], ck);
+      if (inserted) return id;
       u32 li = at_inc_agg(B->n_log);
       if (li < B->cap_log) {
         CreateLog& L = B->log[li];

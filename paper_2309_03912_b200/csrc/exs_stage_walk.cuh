@@ -374,7 +374,14 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       WalkCfg Cc = C;
       u32* ct = B.contract;
       const u32* sn = S.stmt_node; const u32* scs = S.stmt_cs;
-      const u32 nfc = nf;
+      // the (frontier instance, chunk) of every work item, materialised once
+      // (no per-thread binary search over the chunk prefix)
+      u32* itj = dalloc<u32>(nwi + 1);
+      u32* itc = dalloc<u32>(nwi + 1);
+      par_for(nf, [=] EXS_HD (i64 j) {
+        const u32 b0 = wb[j], n = wc[j];
+        for (u32 c = 0; c < n; c++) { itj[b0 + c] = (u32)j; itc[b0 + c] = c; }
+      }, st);
       // work items in statement-shape order (statement kind, expression kind):
       // warps then run similar code paths.  Results do not depend on the order
       // (creation keys and edge slots are order-free).
@@ -385,10 +392,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         u64* key = dalloc<u64>(nwi + 1);
         const Node* nd = P.nodes;
         par_for(nwi, [=] EXS_HD (i64 i) {
-          u32 lo = 0, hi = nfc;
-          while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (wb[mid] <= (u32)i) lo = mid; else hi = mid; }
-          const FnRec& r = fr[in[fl[lo]].fn];
-          u32 k = ((u32)i - wb[lo]) * KCH;
+          const FnRec& r = fr[in[fl[itj[i]]].fn];
+          u32 k = itc[i] * KCH;
           u64 shape = 0;
           if (k < r.nstmts) {
             const Node& s = nd[sn[r.stmt_base + k]];
@@ -407,9 +412,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       EXS_TAG("walk_chunks");
       par_for_walk(nwi, [=] EXS_HD (i64 ii) {
         const u32 i = pm ? pm[ii] : (u32)ii;
-        u32 lo = 0, hi = nfc;  // instance j with wb[j] <= i < wb[j+1]
-        while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (wb[mid] <= (u32)i) lo = mid; else hi = mid; }
-        u32 j = lo, c = (u32)i - wb[j];
+        const u32 j = itj[i], c = itc[i];
         Walker w;
         walker_for(w, Cc, B, fl[j], (u64)j);
         const FnRec& r = fr[w.fn];
@@ -422,6 +425,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       dfree(wc);
       dfree(wb);
       dfree(perm);
+      dfree(itj);
+      dfree(itc);
     }
     dfree(ec);
     dfree(eb);

@@ -130,8 +130,9 @@ void grow(T*& p, u64& cap_or_dummy, u64 need, u64 used, cudaStream_t st) {
 
 // Grow the instance store to hold `need` ids and rehash the keys of the n
 // existing instances (between levels only: no creator is running).  A level
-// creates at most two instances per call site (spacecheck.py:591-596), so
-// growing before each level replaces the overflow-and-rerun of the whole walk.
+// creates at most two instances per call site (spacecheck.py:591-596) and
+// usually at most one; growing before each level replaces the overflow-and-
+// rerun of the whole walk.
 inline void grow_inst(WalkState& W, u64 need, u32 n, cudaStream_t st) {
   if (need <= W.cap_inst) return;
   const u32 cap = (u32)std::min<u64>(std::max<u64>(need + need / 2, 2ull * W.cap_inst), 0x7FFFFFFFull);
@@ -349,7 +350,10 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     u32 npend = cnt[CNT_PEND], nseeds = cnt[CNT_SEEDS];
     grow(W.pend, pend_cap, (u64)npend + S_level + 64, npend, st);
     grow(W.seeds, seed_cap, 2ull * (nseeds + S_level) + 64, 2ull * nseeds, st);
-    grow_inst(W, (u64)n_now + 2ull * S_level + 64, n_now, st);
+    // typically <= one new instance per call site (exact for deep chains, C3);
+    // the rarer second instance of an nvcc native-side call can still overflow,
+    // which the caller handles with a walk-only retry
+    grow_inst(W, (u64)n_now + S_level + S_level / 8 + 64, n_now, st);
     B = bufs();
     B.lvl_base = n_now;
     {

@@ -38,6 +38,10 @@ struct ParseState {
   }
 };
 
+struct MaxU32Op {
+  EXS_HD u32 operator()(u32 a, u32 b) const { return a > b ? a : b; }
+};
+
 EXS_HD inline u64 node_base(const u32* item_start, u32 j) { return 2ull * item_start[j] + 4ull * j; }
 
 // split_min: items at least this many tokens long have their function body
@@ -71,6 +75,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       fvc[f] = c;
     }, st);
   }
+  prof_mark(st);
   excl_scan_u32(fvc, fvb, F + 1, sc, st);
   P.V = get1(fvb + F, st);
   const u32 V = P.V;
@@ -92,9 +97,11 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       f0[t] = tk[t].mask & 1;
       f1[t] = (tk[t].mask >> 1) & 1;
     }, st);
+    prof_mark(st);
     excl_scan_u32(f0, s0, T + 1, sc, st);
     excl_scan_u32(f1, s1, T + 1, sc, st);
     sync(st);
+    prof_mark(st);
     dfree(f0);
     dfree(f1);
   }
@@ -173,7 +180,9 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       bool head = vb[vv[i]] == (u32)i;
       el[i] = (d & 0xFFFFFFFFll) | (head ? (1ll << 40) : 0);
     }, st);
+    prof_mark(st);
     incl_scan(el, inc, VT, DepthOp(), sc, st);
+    prof_mark(st);
     u8* endf = (u8*)el;  // reuse as end flags (VT bytes)
     par_for(VT, [=] EXS_HD (i64 i) {
       const Tok& t = tk[vt[i]];
@@ -193,7 +202,9 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       if (vb[vv[i]] == i) return true;
       return endf[i - 1] && vv[i - 1] == vv[i];
     };
+    prof_mark(st);
     P.I = select_idx(VT, pred, P.item_start, L.cnt, sc, st);
+    prof_mark(st);
     h2d(P.item_start + P.I, &VT, 4, st);  // sentinel: node_base(is, I) bounds the last view's arena
     sync(st);
     dfree(el);
@@ -250,10 +261,17 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       }
     }, st);
     ss = dalloc<u32>(VT + 1);
+    // the item of every view position: item index scattered at its start,
+    // max-scanned (O(1) per token instead of a search for the enclosing item)
+    u32* tit0 = dalloc<u32>(VT + 1);
+    u32* titem = dalloc<u32>(VT + 1);
+    dzero(tit0, 4ull * (VT + 1), st);
+    par_for(I, [=] EXS_HD (i64 j) { tit0[is[j]] = (u32)j; }, st);
+    incl_scan(tit0, titem, VT, MaxU32Op(), sc, st);
+    const u32* ti = titem;
     const u32 Ic = I;
     auto pred = [=] EXS_HD (u32 i) -> bool {
-      u32 lo = 0, hi = Ic;  // item containing view position i
-      while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (is[mid] <= i) lo = mid; else hi = mid; }
+      const u32 lo = ti[i];
       u32 bo = ibody[lo];
       if (bo == NONE || i <= bo) return false;
       u32 v = iv[lo];
@@ -273,8 +291,12 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       }
       return false;
     };
+    prof_mark(st);
     NSS = select_idx(VT, pred, ss, L.cnt, sc, st);
+    prof_mark(st);
     sync(st);
+    dfree(tit0);
+    dfree(titem);
   }
   dfree(depth_after);
   // 4. item-parallel parse
@@ -301,7 +323,9 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
         key[j] = ((u64)lb << 16) | ((u64)t.kind << 8) | t.id;
         iperm[j] = (u32)j;
       }, st);
+      prof_mark(st);
       sort_pairs(key, iperm, I, sc, st, 24);
+      prof_mark(st);
       sync(st);
       dfree(key);
     }

@@ -240,6 +240,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   u32* ibody = dalloc<u32>(I + 1);  // body '{' of a split item (global view position) or NONE
   u32 NSS = 0;
   u32* ss = nullptr;                // statement-segment starts
+  u32* titem = nullptr;             // item of every view position (kept through step 4b)
   {
     const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase;
     const u32* is = P.item_start; const u32* iv = P.item_view; const i64* da = depth_after;
@@ -264,7 +265,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     // the item of every view position: item index scattered at its start,
     // max-scanned (O(1) per token instead of a search for the enclosing item)
     u32* tit0 = dalloc<u32>(VT + 1);
-    u32* titem = dalloc<u32>(VT + 1);
+    titem = dalloc<u32>(VT + 1);
     dzero(tit0, 4ull * (VT + 1), st);
     par_for(I, [=] EXS_HD (i64 j) { tit0[is[j]] = (u32)j; }, st);
     incl_scan(tit0, titem, VT, MaxU32Op(), sc, st);
@@ -296,7 +297,6 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     prof_mark(st);
     sync(st);
     dfree(tit0);
-    dfree(titem);
   }
   dfree(depth_after);
   // 4. item-parallel parse
@@ -374,6 +374,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     PErr* serr = dalloc<PErr>(NSS + 1);
     dfill_ff(sbad, 4ull * (I + 1), st);
     const u32 Ic = I, NSSc = NSS;
+    const u32* titm = titem;
     // segments in first-token order: warps parse statements of the same shape
     u32* sperm = dalloc<u32>(NSS + 1);
     {
@@ -392,8 +393,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     par_for_parse(NSS, [=] EXS_HD (i64 kk) {
       const u32 k = spm[kk];
       u32 i0 = ssc[k];
-      u32 lo = 0, hi = Ic;
-      while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (is[mid] <= i0) lo = mid; else hi = mid; }
+      u32 lo = titm[i0];  // the item holding segment start i0
       u32 j = lo, v = iv[j];
       u32 inext = (j + 1 < Ic && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
       bool last = !(k + 1 < NSSc && ssc[k + 1] < inext);
@@ -424,8 +424,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     const u32* ir = P.item_root;
     par_for(NSS, [=] EXS_HD (i64 k) {
       u32 i0 = ssc[k];
-      u32 lo = 0, hi = Ic;
-      while (hi - lo > 1) { u32 mid = (lo + hi) / 2; if (is[mid] <= i0) lo = mid; else hi = mid; }
+      u32 lo = titm[i0];  // the item holding segment start i0
       u32 j = lo;
       if (ist[j] || sroot[k] == NONE) return;
       u32 v = iv[j];
@@ -439,6 +438,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     dfree(sroot); dfree(sbad); dfree(sstat); dfree(serr); dfree(sperm);
   }
   dfree(ss);
+  dfree(titem);
   dfree(ibody);
   // 5. per view: parse error, ok, or sequential repair
   u32 nfb = 0;

@@ -50,13 +50,15 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
                       u32 split_min = 16) {
   const u32 F = L.F, T = L.T;
   // 1. files whose passes see different token sets
-  u32* split = dalloc<u32>(F + 1);
-  dzero(split, (F + 1) * 4, st);
+  u32* split = dalloc<u32>(F + 2);
+  dzero(split, (F + 2) * 4, st);
+  u32* irr = split + F + 1;  // some token is not live in all its file's passes, or a pass failed
   {
-    const Tok* tk = L.toks;
+    const Tok* tk = L.toks; const u8* cf = L.cfg;
     par_for(T, [=] EXS_HD (i64 t) {
-      u8 m = tk[t].mask;
+      const u8 m = tk[t].mask;
       if (m == 1 || m == 2) at_or(&split[tk[t].file], 1u);
+      if (m != ((cf[tk[t].file] & CFG_PLAIN) ? 1 : 3)) at_or(irr, 1u);
     }, st);
   }
   // 2. views per file
@@ -73,97 +75,138 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       else if (ok[0] && ok[1] && !split[f]) c = 1;
       else c = (u32)ok[0] + (u32)ok[1];
       fvc[f] = c;
+      if (!ok[0] || (!(cf[f] & CFG_PLAIN) && !ok[1])) at_or(irr, 1u);
     }, st);
   }
-  prof_mark(st);
-  excl_scan_u32(fvc, fvb, F + 1, sc, st);
-  P.V = get1(fvb + F, st);
-  const u32 V = P.V;
-  P.vbase = dalloc<u32>(V + 1);
-  P.vfile = dalloc<u32>(V + 1);
-  P.vpass = dalloc<u8>(V + 1);
-  P.veof = dalloc<u32>(2 * (size_t)V + 2);
-  P.vdirect = dalloc<u32>(V + 1);
-  u32* vcnt = dalloc<u32>(V + 1);
-  // token pass flags and their scans
-  u32* s0 = dalloc<u32>(T + 1);
-  u32* s1 = dalloc<u32>(T + 1);
-  {
-    u32* f0 = dalloc<u32>(T + 1);
-    u32* f1 = dalloc<u32>(T + 1);
-    const Tok* tk = L.toks;
-    par_for(T + 1, [=] EXS_HD (i64 t) {
-      if (t == T) { f0[t] = f1[t] = 0; return; }
-      f0[t] = tk[t].mask & 1;
-      f1[t] = (tk[t].mask >> 1) & 1;
-    }, st);
-    prof_mark(st);
-    excl_scan_u32(f0, s0, T + 1, sc, st);
-    excl_scan_u32(f1, s1, T + 1, sc, st);
+  u32 V = 0, VT = 0;
+  if (!get1(irr, st)) {
+    // every token is live in all its file's passes and no pass failed (the
+    // common case): one view per file, view positions are token indices
+    V = P.V = F;
+    VT = P.VT = T;
+    P.vbase = dalloc<u32>(V + 1);
+    P.vfile = dalloc<u32>(V + 1);
+    P.vpass = dalloc<u8>(V + 1);
+    P.veof = dalloc<u32>(2 * (size_t)V + 2);
+    P.vdirect = dalloc<u32>(V + 1);
+    {
+      FP* fp = L.fp; const u8* cf = L.cfg; const u32* ft = L.ftok;
+      u32* vb = P.vbase; u32* vf = P.vfile; u8* vp = P.vpass; u32* ve = P.veof; u32* vd = P.vdirect;
+      par_for(F + 1, [=] EXS_HD (i64 f) {
+        vb[f] = ft[f];
+        if (f == F) return;
+        const bool plain = (cf[f] & CFG_PLAIN) != 0;
+        vf[f] = (u32)f; vp[f] = plain ? 1 : 3; vd[f] = ft[f];
+        fp[2 * f].view = (u32)f;
+        if (!plain) fp[2 * f + 1].view = (u32)f;
+        ve[2 * f] = fp[2 * f].eof_line; ve[2 * f + 1] = fp[2 * f].eof_col;
+      }, st);
+    }
+    P.vtok = dalloc<u32>(VT + 1);
+    P.vview = dalloc<u32>(VT + 1);
+    P.vkid = dalloc<u16>(VT + 1);
+    {
+      const Tok* tk = L.toks; u32* vt = P.vtok; u32* vv = P.vview; u16* vkd = P.vkid;
+      par_for(T, [=] EXS_HD (i64 t) {
+        const Tok& k = tk[t];
+        vt[t] = (u32)t;
+        vv[t] = k.file;
+        vkd[t] = (u16)(((u32)k.kind << 8) | k.id);
+      }, st);
+    }
     sync(st);
+    dfree(fvc); dfree(fvb); dfree(split);
+  } else {
     prof_mark(st);
-    dfree(f0);
-    dfree(f1);
+    excl_scan_u32(fvc, fvb, F + 1, sc, st);
+    P.V = get1(fvb + F, st);
+    V = P.V;
+    P.vbase = dalloc<u32>(V + 1);
+    P.vfile = dalloc<u32>(V + 1);
+    P.vpass = dalloc<u8>(V + 1);
+    P.veof = dalloc<u32>(2 * (size_t)V + 2);
+    P.vdirect = dalloc<u32>(V + 1);
+    u32* vcnt = dalloc<u32>(V + 1);
+    // token pass flags and their scans
+    u32* s0 = dalloc<u32>(T + 1);
+    u32* s1 = dalloc<u32>(T + 1);
+    {
+      u32* f0 = dalloc<u32>(T + 1);
+      u32* f1 = dalloc<u32>(T + 1);
+      const Tok* tk = L.toks;
+      par_for(T + 1, [=] EXS_HD (i64 t) {
+        if (t == T) { f0[t] = f1[t] = 0; return; }
+        f0[t] = tk[t].mask & 1;
+        f1[t] = (tk[t].mask >> 1) & 1;
+      }, st);
+      prof_mark(st);
+      excl_scan_u32(f0, s0, T + 1, sc, st);
+      excl_scan_u32(f1, s1, T + 1, sc, st);
+      sync(st);
+      prof_mark(st);
+      dfree(f0);
+      dfree(f1);
+    }
+    {
+      FP* fp = L.fp; const u8* cf = L.cfg; const u32* ft = L.ftok;
+      u32* vf = P.vfile; u8* vp = P.vpass; u32* ve = P.veof; u32* vd = P.vdirect;
+      par_for(F, [=] EXS_HD (i64 f) {
+        u32 v = fvb[f];
+        u32 c = fvc[f];
+        if (!c) return;
+        u32 tf0 = ft[f], tf1 = ft[f + 1];
+        bool ok0 = fp[2 * f].pp_line == NONE && fp[2 * f].lex_pos == NONE;
+        bool ok1 = !(cf[f] & CFG_PLAIN) && fp[2 * f + 1].pp_line == NONE && fp[2 * f + 1].lex_pos == NONE;
+        if (c == 1 && ok0 && ok1) {
+          vf[v] = (u32)f; vp[v] = 3;
+          fp[2 * f].view = v; fp[2 * f + 1].view = v;
+          ve[2 * v] = fp[2 * f].eof_line; ve[2 * v + 1] = fp[2 * f].eof_col;
+          vcnt[v] = s0[tf1] - s0[tf0];
+          vd[v] = vcnt[v] == tf1 - tf0 ? tf0 : NONE;
+          return;
+        }
+        for (u32 p = 0; p < 2; p++) {
+          bool okp = p ? ok1 : ok0;
+          if (!okp) continue;
+          vf[v] = (u32)f; vp[v] = (u8)(1u << p);
+          fp[2 * f + p].view = v;
+          ve[2 * v] = fp[2 * f + p].eof_line; ve[2 * v + 1] = fp[2 * f + p].eof_col;
+          vcnt[v] = p ? (s1[tf1] - s1[tf0]) : (s0[tf1] - s0[tf0]);
+          vd[v] = vcnt[v] == tf1 - tf0 ? tf0 : NONE;
+          v++;
+        }
+      }, st);
+    }
+    h2d(vcnt + V, "\0\0\0\0", 4, st);
+    excl_scan_u32(vcnt, P.vbase, V + 1, sc, st);
+    P.VT = get1(P.vbase + V, st);
+    VT = P.VT;
+    P.vtok = dalloc<u32>(VT + 1);
+    P.vview = dalloc<u32>(VT + 1);
+    P.vkid = dalloc<u16>(VT + 1);
+    {
+      const Tok* tk = L.toks; const FP* fp = L.fp; const u32* ft = L.ftok;
+      const u32* vb = P.vbase; const u8* vp = P.vpass; u32* vt = P.vtok; u32* vv = P.vview;
+      u16* vkd = P.vkid;
+      par_for(T, [=] EXS_HD (i64 t) {
+        u32 f = tk[t].file;
+        u8 m = tk[t].mask;
+        u32 tf0 = ft[f];
+        for (u32 p = 0; p < 2; p++) {
+          u32 v = fp[2 * f + p].view;
+          if (v == NONE) continue;
+          if (p == 1 && vp[v] == 3) continue;
+          if (!((m >> p) & 1)) continue;
+          u32 i = vb[v] + (p ? (s1[t] - s1[tf0]) : (s0[t] - s0[tf0]));
+          vt[i] = (u32)t;
+          vv[i] = v;
+          vkd[i] = (u16)(((u32)tk[t].kind << 8) | tk[t].id);
+        }
+      }, st);
+    }
+    sync(st);
+    dfree(s0); dfree(s1); dfree(vcnt); dfree(fvc); dfree(fvb); dfree(split);
   }
-  {
-    FP* fp = L.fp; const u8* cf = L.cfg; const u32* ft = L.ftok;
-    u32* vf = P.vfile; u8* vp = P.vpass; u32* ve = P.veof; u32* vd = P.vdirect;
-    par_for(F, [=] EXS_HD (i64 f) {
-      u32 v = fvb[f];
-      u32 c = fvc[f];
-      if (!c) return;
-      u32 tf0 = ft[f], tf1 = ft[f + 1];
-      bool ok0 = fp[2 * f].pp_line == NONE && fp[2 * f].lex_pos == NONE;
-      bool ok1 = !(cf[f] & CFG_PLAIN) && fp[2 * f + 1].pp_line == NONE && fp[2 * f + 1].lex_pos == NONE;
-      if (c == 1 && ok0 && ok1) {
-        vf[v] = (u32)f; vp[v] = 3;
-        fp[2 * f].view = v; fp[2 * f + 1].view = v;
-        ve[2 * v] = fp[2 * f].eof_line; ve[2 * v + 1] = fp[2 * f].eof_col;
-        vcnt[v] = s0[tf1] - s0[tf0];
-        vd[v] = vcnt[v] == tf1 - tf0 ? tf0 : NONE;
-        return;
-      }
-      for (u32 p = 0; p < 2; p++) {
-        bool okp = p ? ok1 : ok0;
-        if (!okp) continue;
-        vf[v] = (u32)f; vp[v] = (u8)(1u << p);
-        fp[2 * f + p].view = v;
-        ve[2 * v] = fp[2 * f + p].eof_line; ve[2 * v + 1] = fp[2 * f + p].eof_col;
-        vcnt[v] = p ? (s1[tf1] - s1[tf0]) : (s0[tf1] - s0[tf0]);
-        vd[v] = vcnt[v] == tf1 - tf0 ? tf0 : NONE;
-        v++;
-      }
-    }, st);
-  }
-  h2d(vcnt + V, "\0\0\0\0", 4, st);
-  excl_scan_u32(vcnt, P.vbase, V + 1, sc, st);
-  P.VT = get1(P.vbase + V, st);
-  const u32 VT = P.VT;
-  P.vtok = dalloc<u32>(VT + 1);
-  P.vview = dalloc<u32>(VT + 1);
-  P.vkid = dalloc<u16>(VT + 1);
-  {
-    const Tok* tk = L.toks; const FP* fp = L.fp; const u32* ft = L.ftok;
-    const u32* vb = P.vbase; const u8* vp = P.vpass; u32* vt = P.vtok; u32* vv = P.vview;
-    u16* vkd = P.vkid;
-    par_for(T, [=] EXS_HD (i64 t) {
-      u32 f = tk[t].file;
-      u8 m = tk[t].mask;
-      u32 tf0 = ft[f];
-      for (u32 p = 0; p < 2; p++) {
-        u32 v = fp[2 * f + p].view;
-        if (v == NONE) continue;
-        if (p == 1 && vp[v] == 3) continue;
-        if (!((m >> p) & 1)) continue;
-        u32 i = vb[v] + (p ? (s1[t] - s1[tf0]) : (s0[t] - s0[tf0]));
-        vt[i] = (u32)t;
-        vv[i] = v;
-        vkd[i] = (u16)(((u32)tk[t].kind << 8) | tk[t].id);
-      }
-    }, st);
-  }
-  sync(st);
-  dfree(s0); dfree(s1); dfree(vcnt); dfree(fvc); dfree(fvb); dfree(split);
   // 3. segmentation: depth scan and item starts (depth over ( ) { })
   i64* depth_after = nullptr;
   {

@@ -20,6 +20,7 @@ constexpr u32 CNT_STRIDE = 32;
 
 struct WalkState {
   u32 cap_inst = 0, n_inst = 0, levels = 0;
+  u32 buf_scale = 1;  // multiplier of the creation-log estimate (grows on overflow)
   u64 n_edges = 0, edge_cap = 0, callsites = 0;
   IKey* slots = nullptr;
   u32* sid = nullptr;
@@ -185,8 +186,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   dzero(W.main_key, 8ull * (NW + 1), st);
   u64 edge_cap = 0, pend_cap = 0, seed_cap = 0, log_cap = 0;
   W.edges = nullptr; W.pend = nullptr; W.seeds = nullptr; W.log = nullptr;
-  // roots need log capacity 2 per decl and walk
-  grow(W.log, log_cap, 4ull * NF + 64, 0, st);
+  // roots log only their non-inserting creators (duplicate decls): few
+  grow(W.log, log_cap, std::min<u64>(4ull * NF, ((u64)NF / 8 + 65536) * W.buf_scale) + 64, 0, st);
   grow(W.pend, pend_cap, 1024, 0, st);
   grow(W.seeds, seed_cap, 2048, 0, st);
   grow(W.edges, edge_cap, 1024, 0, st);
@@ -333,6 +334,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       dfree(fr_tmp);
     }
     prev_n = n_now;
+    const u32 nnew_prev = nnew;  // new instances per level track the next level's
     if (!nf) break;
     prof_mark(st);
     // edge bases: scan of call-site counts
@@ -346,14 +348,16 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     u64 S_level = get1(eb + nf, st);
     W.callsites += S_level;
     grow(W.edges, edge_cap, edges_used + S_level + 1, edges_used, st);
-    grow(W.log, log_cap, 2 * S_level + 64, 0, st);
+    // the creation log holds the creators that did not insert (several creators
+    // of one instance in one level) -- few; it grows on overflow (buf_scale)
+    grow(W.log, log_cap, std::min<u64>(2ull * S_level, ((u64)S_level / 8 + 65536) * W.buf_scale) + 64, 0, st);
     u32 npend = cnt[CNT_PEND], nseeds = cnt[CNT_SEEDS];
     grow(W.pend, pend_cap, (u64)npend + S_level + 64, npend, st);
     grow(W.seeds, seed_cap, 2ull * (nseeds + S_level) + 64, 2ull * nseeds, st);
-    // typically <= one new instance per call site (exact for deep chains, C3);
-    // the rarer second instance of an nvcc native-side call can still overflow,
-    // which the caller handles with a walk-only retry
-    grow_inst(W, (u64)n_now + S_level + S_level / 8 + 64, n_now, st);
+    // a level creates at most ~one new instance per call site (exact for deep
+    // chains, C3) and about as many as the previous level did (C4: calls hit
+    // existing roots); an overflow is handled by the caller's walk-only retry
+    grow_inst(W, (u64)n_now + std::min<u64>(S_level, 2ull * nnew_prev) + S_level / 8 + 65536, n_now, st);
     B = bufs();
     B.lvl_base = n_now;
     {

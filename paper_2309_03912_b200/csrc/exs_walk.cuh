@@ -299,12 +299,14 @@ struct Walker {
       inst_publish(*B, slot, id);
     }
     if (id >= B->lvl_base) {
-      // a creator in this level: the minimum creation key wins.  The inserter's
-      // location and decl are already in the record, so only the other
-      // creators are logged (the post-level fixup applies the log entry whose
-      // key is the minimum; none matches when the inserter holds it)
-      at_min64(&B->sck[slot], ck);
-      if (inserted) return id;
+      // a creator in this level: the minimum creation key wins.  A creator
+      // logs (ckey, location, decl) only if it lowered the minimum when it
+      // arrived -- the final winner always did -- and not if it inserted (the
+      // record already holds its data).  The post-level fixup applies the log
+      // entry whose key equals the final minimum; none matches when the
+      // inserter holds it.
+      const unsigned long long old = at_min64(&B->sck[slot], ck);
+      if (inserted || old < ck) return id;
       u32 li = at_inc_agg(B->n_log);
       if (li < B->cap_log) {
         CreateLog& L = B->log[li];

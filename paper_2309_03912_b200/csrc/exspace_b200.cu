@@ -28,6 +28,7 @@ struct BlockCache {
   std::multimap<std::pair<cudaStream_t, size_t>, void*> free_;
   std::map<void*, std::pair<cudaStream_t, size_t>> live;
   size_t cached = 0;
+  size_t live_bytes = 0, peak_bytes = 0;
 };
 static BlockCache g_cache;
 
@@ -55,10 +56,21 @@ void* cache_alloc(size_t bytes) {
         }
       }
       cudaStreamSynchronize(g_alloc_stream);
-      CK(cudaMallocAsync(&p, bytes, g_alloc_stream));
+      e = cudaMallocAsync(&p, bytes, g_alloc_stream);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        char msg[256];
+        snprintf(msg, sizeof msg,
+                 "device out of memory: %.1f MiB requested with %.1f MiB live (peak %.1f MiB) in this "
+                 "process's pipelines; split the batch",
+                 bytes / 1048576.0, g_cache.live_bytes / 1048576.0, g_cache.peak_bytes / 1048576.0);
+        throw std::runtime_error(msg);
+      }
     }
   }
   g_cache.live[p] = {g_alloc_stream, bytes};
+  g_cache.live_bytes += bytes;
+  if (g_cache.live_bytes > g_cache.peak_bytes) g_cache.peak_bytes = g_cache.live_bytes;
   return p;
 }
 
@@ -68,6 +80,7 @@ void cache_free(void* p) {
   if (it == g_cache.live.end()) { cudaFreeAsync(p, g_alloc_stream); return; }
   g_cache.free_.insert({it->second, p});
   g_cache.cached += it->second.second;
+  g_cache.live_bytes -= it->second.second;
   g_cache.live.erase(it);
 }
 
@@ -376,10 +389,12 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     prof_mark(st);
     Timer t3(st);
     u32 walk_ovf = 0;
+    u32 buf_scale = 1;
     while (true) {
       H.W.free_all();
       H.W = WalkState();
       H.W.cap_inst = cap_inst;
+      H.W.buf_scale = buf_scale;
       bool ok = run_walk(L, H.P, H.S, H.W, B0, H.sc, st, cap_diags);
       if (ok && (any_div || H.want_demands)) run_demands(H, any_div);
       walk_ovf = get1(H.W.ctr(CNT_OVF), st);
@@ -404,6 +419,7 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       } else if (walk_ovf & 2) {
         break;  // the earlier stages overflowed too: outer loop
       }
+      if (walk_ovf & 4) buf_scale = std::min<u32>(buf_scale * 4, 1u << 20);  // creation log
       if (walk_ovf & 1) {
         u32 n_now = get1(H.W.ctr(CNT_INST), st);
         cap_inst = (u32)std::min<u64>(std::max<u64>(8ull * cap_inst, 2ull * n_now), 0x7FFFFFFFull);

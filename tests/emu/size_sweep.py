@@ -24,4 +24,4 @@ for n in ns:
     mb = st["bytes"] / 1e6
     print(f"n={n:6d} {mb:8.1f} MB  total {st['ms_total']:8.2f} ms  = {mb / st['ms_total']:.2f} GB/s |"
           + " ".join(f"{k[3:]} {1e3 * st[k] / mb:6.1f}" for k in ("ms_lex", "ms_parse", "ms_sema", "ms_walk"))
-          + " us/MB", flush=True)
+          + f" us/MB, retries {st['retries']}", flush=True)

@@ -84,6 +84,55 @@ typedef struct {
   uint8_t bkind[2], bvx[2], pad2[4]; /* bkind 1 type 2 hdc; bvx: type targ / hdc */
 } exs_desc;
 
+/* ---- walk materialisation: the arrays behind Analysis.walks[side].instances /
+ * .demands / .edges (spacecheck.py:183-221,239-346,585).  All refer to the last
+ * run on the handle; a host renders the reference's canonical keys from them. */
+
+/* one function declaration (sema.py FunctionDecl; order = _all_decls order) */
+typedef struct {
+  uint32_t node, view, rec, order;  /* FN node; struct record (0xFFFFFFFF free) */
+  uint32_t ncalls, flags;           /* call-site slots of an instance's edges; 1 DUP 2 OWNER 4 MEMBER */
+} exs_decl;
+
+/* one struct declaration */
+typedef struct {
+  uint32_t node, view;
+} exs_struct;
+
+/* a value bound in an instance key: k 1 = type (struct record rec, or builtin
+ * bt 1 void 2 int 3 bool 4 HDC; targ 1..3 = HDC argument Hst/Dev/HstDev),
+ * k 2 = HDC value (x = 1 Hst, 2 Dev, 3 HstDev), k 0 = none */
+typedef struct {
+  uint8_t k, targ, bt, pad;
+  uint32_t rec;
+  uint64_t x;
+} exs_val;
+
+/* one instance (spacecheck.py Instance): creating decl, walk (2*file + pass),
+ * side (0 host 1 device), first-creation token, bindings and owner type,
+ * legal edges: slots [ebase, ebase + decl.ncalls) of the edge array */
+typedef struct {
+  uint32_t decl, walk, side, at;
+  uint32_t ebase, ecnt, flags, pad;
+  uint64_t ckey;                    /* creation order (level, parent rank, statement, ordinal) */
+  exs_val tb, hb, ot;
+} exs_inst;
+
+/* AST node (32 bytes, csrc/exs_common.cuh Node) */
+typedef struct {
+  uint8_t kind, sub;
+  uint16_t n;
+  uint32_t tok, c0, c1, c2, next;
+  uint64_t hv;
+} exs_node;
+
+int exs_get_decls(exs_handle h, exs_decl* out, uint64_t cap, uint64_t* n);
+int exs_get_structs(exs_handle h, exs_struct* out, uint64_t cap, uint64_t* n);
+int exs_get_instances(exs_handle h, exs_inst* out, uint64_t cap, uint64_t* n);
+int exs_get_edges(exs_handle h, uint32_t* out, uint64_t cap, uint64_t* n);   /* callee ids, 0xFFFFFFFF empty */
+int exs_get_nodes(exs_handle h, exs_node* out, uint64_t cap, uint64_t* n);
+int exs_get_token_range(exs_handle h, uint64_t first, uint64_t count, exs_token* out);
+
 int exs_create(int device, exs_handle* out);
 int exs_destroy(exs_handle h);
 const char* exs_last_error(void);

@@ -58,7 +58,21 @@ EXPORTS = [
     "exs_create", "exs_destroy", "exs_last_error", "exs_run", "exs_run_device", "exs_get_stats",
     "exs_get_diags", "exs_diags_view", "exs_get_arena", "exs_get_pass_status", "exs_get_tokens",
     "exs_get_walk_stats", "exs_describe", "exs_set_option", "exs_stage_times", "exs_profile_text",
+    "exs_get_decls", "exs_get_structs", "exs_get_instances", "exs_get_edges", "exs_get_nodes",
+    "exs_get_token_range",
 ]
+
+
+DECL_DTYPE = np.dtype([("node", "<u4"), ("view", "<u4"), ("rec", "<u4"), ("order", "<u4"),
+                       ("ncalls", "<u4"), ("flags", "<u4")])
+STRUCT_DTYPE = np.dtype([("node", "<u4"), ("view", "<u4")])
+_VAL = [("k", "u1"), ("targ", "u1"), ("bt", "u1"), ("pad", "u1"), ("rec", "<u4"), ("x", "<u8")]
+INST_DTYPE = np.dtype([("decl", "<u4"), ("walk", "<u4"), ("side", "<u4"), ("at", "<u4"),
+                       ("ebase", "<u4"), ("ecnt", "<u4"), ("flags", "<u4"), ("pad", "<u4"),
+                       ("ckey", "<u8")] + [(f"{v}_{n}", t) for v in ("tb", "hb", "ot") for n, t in _VAL])
+NODE_DTYPE = np.dtype([("kind", "u1"), ("sub", "u1"), ("n", "<u2"), ("tok", "<u4"), ("c0", "<u4"),
+                       ("c1", "<u4"), ("c2", "<u4"), ("next", "<u4"), ("hv", "<u8")])
+assert DECL_DTYPE.itemsize == 24 and INST_DTYPE.itemsize == 88 and NODE_DTYPE.itemsize == 32
 
 
 class NativeError(RuntimeError):
@@ -82,6 +96,9 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     lib.exs_get_stats.argtypes = [vp, C.POINTER(Stats)]
     lib.exs_get_diags.argtypes = [vp, vp, C.c_uint64, u64p]
     lib.exs_diags_view.argtypes = [vp, C.POINTER(C.c_void_p), u64p]
+    for fn in ("exs_get_decls", "exs_get_structs", "exs_get_instances", "exs_get_edges", "exs_get_nodes"):
+        getattr(lib, fn).argtypes = [vp, vp, C.c_uint64, u64p]
+    lib.exs_get_token_range.argtypes = [vp, C.c_uint64, C.c_uint64, vp]
     lib.exs_get_arena.argtypes = [vp, vp, C.c_uint64, u64p]
     lib.exs_get_pass_status.argtypes = [vp, vp, C.c_uint64]
     lib.exs_get_tokens.argtypes = [vp, C.c_uint32, vp, C.c_uint64, u64p]
@@ -161,6 +178,37 @@ class Handle:
         view = raw.view(DIAG_DTYPE)
         view.flags.writeable = False
         return view
+
+    def _records(self, fn: str, dtype) -> np.ndarray:
+        n = C.c_uint64()
+        f = getattr(self.lib, fn)
+        self._check(f(self.h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=dtype)
+        if n.value:
+            self._check(f(self.h, _ptr(out), n.value, C.byref(n)))
+        return out
+
+    # walk materialisation (include/exspace_b200.h): arrays of the last run
+    def decls(self) -> np.ndarray:
+        return self._records("exs_get_decls", DECL_DTYPE)
+
+    def structs(self) -> np.ndarray:
+        return self._records("exs_get_structs", STRUCT_DTYPE)
+
+    def instances(self) -> np.ndarray:
+        return self._records("exs_get_instances", INST_DTYPE)
+
+    def edges(self) -> np.ndarray:
+        return self._records("exs_get_edges", np.dtype("<u4"))
+
+    def nodes(self) -> np.ndarray:
+        return self._records("exs_get_nodes", NODE_DTYPE)
+
+    def token_range(self, first: int, count: int) -> np.ndarray:
+        out = np.zeros(count, dtype=TOKEN_DTYPE)
+        if count:
+            self._check(self.lib.exs_get_token_range(self.h, first, count, _ptr(out)))
+        return out
 
     def arena(self) -> bytes:
         n = C.c_uint64()

@@ -718,6 +718,102 @@ int exs_get_walk_stats(exs_handle x, exs_walk_stats* out, uint64_t cap) {
   API_END
 }
 
+// ---- walk materialisation (the arrays behind Analysis.walks)
+static_assert(sizeof(exs_val) == sizeof(Val), "exs_val mirrors Val");
+static_assert(sizeof(exs_node) == sizeof(Node), "exs_node mirrors Node");
+static_assert(sizeof(exs_token) == sizeof(Tok), "exs_token mirrors Tok");
+
+int exs_get_decls(exs_handle x, exs_decl* out, uint64_t cap, uint64_t* n) {
+  API_TRY
+  Handle& H = x->h;
+  bind_stream(H);
+  const u32 NF = H.S.fns ? H.S.NF : 0;
+  *n = NF;
+  const u64 m = std::min<u64>(cap, NF);
+  if (out && m) {
+    std::vector<FnRec> fr(m);
+    d2h(fr.data(), H.S.fns, sizeof(FnRec) * m, H.st);
+    sync(H.st);
+    for (u64 i = 0; i < m; i++) {
+      out[i].node = fr[i].node; out[i].view = fr[i].view; out[i].rec = fr[i].rec;
+      out[i].order = fr[i].order; out[i].ncalls = fr[i].ncalls;
+      out[i].flags = fr[i].flags & (FR_DUP | FR_OWNER | FR_MEMBER);
+    }
+  }
+  API_END
+}
+
+int exs_get_structs(exs_handle x, exs_struct* out, uint64_t cap, uint64_t* n) {
+  API_TRY
+  Handle& H = x->h;
+  bind_stream(H);
+  const u32 NR = H.S.recs ? H.S.NR : 0;
+  *n = NR;
+  const u64 m = std::min<u64>(cap, NR);
+  if (out && m) {
+    std::vector<RecRec> rr(m);
+    d2h(rr.data(), H.S.recs, sizeof(RecRec) * m, H.st);
+    sync(H.st);
+    for (u64 i = 0; i < m; i++) { out[i].node = rr[i].node; out[i].view = rr[i].view; }
+  }
+  API_END
+}
+
+int exs_get_instances(exs_handle x, exs_inst* out, uint64_t cap, uint64_t* n) {
+  API_TRY
+  Handle& H = x->h;
+  bind_stream(H);
+  const u32 NI = H.W.inst ? H.W.n_inst : 0;
+  *n = NI;
+  const u64 m = std::min<u64>(cap, NI);
+  if (out && m) {
+    std::vector<Inst> in(m);
+    d2h(in.data(), H.W.inst, sizeof(Inst) * m, H.st);
+    sync(H.st);
+    for (u64 i = 0; i < m; i++) {
+      exs_inst& o = out[i];
+      o.decl = in[i].fn; o.walk = in[i].walk; o.side = in[i].side; o.at = in[i].at;
+      o.ebase = in[i].ebase; o.ecnt = in[i].ecnt; o.flags = in[i].flags; o.pad = 0;
+      o.ckey = in[i].ckey;
+      memcpy(&o.tb, &in[i].tb, sizeof(Val));
+      memcpy(&o.hb, &in[i].hb, sizeof(Val));
+      memcpy(&o.ot, &in[i].ot, sizeof(Val));
+    }
+  }
+  API_END
+}
+
+int exs_get_edges(exs_handle x, uint32_t* out, uint64_t cap, uint64_t* n) {
+  API_TRY
+  Handle& H = x->h;
+  bind_stream(H);
+  const u64 NE = H.W.edges ? H.W.n_edges : 0;
+  *n = NE;
+  const u64 m = std::min<u64>(cap, NE);
+  if (out && m) { d2h(out, H.W.edges, 4ull * m, H.st); sync(H.st); }
+  API_END
+}
+
+int exs_get_nodes(exs_handle x, exs_node* out, uint64_t cap, uint64_t* n) {
+  API_TRY
+  Handle& H = x->h;
+  bind_stream(H);
+  const u64 NN = H.P.nodes ? H.P.n_nodes : 0;
+  *n = NN;
+  const u64 m = std::min<u64>(cap, NN);
+  if (out && m) { d2h(out, H.P.nodes, sizeof(Node) * m, H.st); sync(H.st); }
+  API_END
+}
+
+int exs_get_token_range(exs_handle x, uint64_t first, uint64_t count, exs_token* out) {
+  API_TRY
+  Handle& H = x->h;
+  bind_stream(H);
+  if (first > H.L.T || count > H.L.T - first) throw Err("token range out of bounds");
+  if (count) { d2h(out, H.L.toks + first, sizeof(Tok) * count, H.st); sync(H.st); }
+  API_END
+}
+
 int exs_describe(exs_handle x, const uint32_t* ids, const uint8_t* kinds, uint32_t n, exs_desc* out) {
   API_TRY
   Handle& H = x->h;

@@ -17,6 +17,7 @@ from typing import Iterable, Optional
 import numpy as np
 
 from . import _native
+from .walks import BatchWalks
 from .messages import CODES, Renderer, stray_text
 
 
@@ -238,11 +239,38 @@ def legality(caller_side, callee_space, kind: str = "direct", *, caller_from_hd:
 
 @dataclass
 class WalkSummary:
-    """What the GPU walk exposes per native side (Analysis.walks)."""
+    """One walk of an analysis (spacecheck.py _Walk): counts, and -- rendered from
+    the GPU arrays on first access -- the instance, demand and edge maps keyed by
+    the reference's keys in canonical text form (walks.py)."""
     native: ExecSpace
     n_instances: int
     n_edges: int
     n_demands: int
+    _batch: object = field(default=None, repr=False, compare=False)
+    _where: tuple = field(default=(0, 0), repr=False, compare=False)
+    _maps: Optional[tuple] = field(default=None, repr=False, compare=False)
+
+    def _get(self, i: int):
+        if self._maps is None:
+            if self._batch is None:
+                raise RuntimeError("walk keys need an analysis run with want_walks=True")
+            self._maps = self._batch.walk(*self._where)
+        return self._maps[i]
+
+    @property
+    def instances(self) -> dict:
+        """{instance key: walks.InstanceInfo} in creation (FIFO) order."""
+        return self._get(0)
+
+    @property
+    def demands(self) -> dict:
+        """{demand key: (display name, (line, col) of the first demand)}."""
+        return self._get(1)
+
+    @property
+    def edges(self) -> dict:
+        """{caller instance key: [callee instance keys in post-order]} (legal edges)."""
+        return self._get(2)
 
 
 @dataclass
@@ -291,10 +319,16 @@ class Engine:
             walks = self.handle.walk_stats(len(units)) if want_walks else None
             status = self.handle.pass_status(len(units)) if want_walks else None
             ren = Renderer(data.tobytes(), offsets.tolist(), arena, self.handle.describe)
-            out = self._assemble(units, recs, ren, walks, status)
+            batch = None
+            if want_walks:
+                # the walk arrays stay valid until the next run on this engine:
+                # snapshot them now (lazily rendered afterwards)
+                batch = BatchWalks(self.handle, ren, status, [u[3] for u in units])
+                batch._load()
+            out = self._assemble(units, recs, ren, walks, status, batch)
         return out
 
-    def _assemble(self, units, recs, ren: Renderer, walks, status):
+    def _assemble(self, units, recs, ren: Renderer, walks, status, batch=None):
         per_file: list = [[] for _ in units]
         for r in recs:
             f = int(r["file"])
@@ -312,7 +346,7 @@ class Engine:
                     w = walks[2 * f + p]
                     if w["exists"]:
                         a.walks[side] = WalkSummary(side, int(w["instances"]), int(w["edges"]),
-                                                    int(w["demands"]))
+                                                    int(w["demands"]), batch, (f, p))
                 for p, kind in enumerate(u[2].pass_kinds()):
                     s = status[2 * f + p]
                     a.passes[kind] = {"pp_line": int(s["pp_line"]), "lex_line": int(s["lex_line"]),

@@ -163,3 +163,25 @@ def test_diagnostic_overflow_regrows_inside_the_walk(X, eng):
     assert eng.last_stats["retries"] >= 1
     rows, _, _ = _oracle_rows(text, "sound")
     assert as_rows(a) == rows
+
+
+@pytest.mark.parametrize("group", GOLDEN_GROUPS)
+def test_walk_keys_match_the_reference(X, eng, group):
+    """Analysis.walks[side].instances / .demands / .edges (spacecheck.py:239-346,585),
+    rendered from the GPU arrays, equal the reference's keys (canonical text form,
+    with demand display names and first-demand locations, edges in post-order)."""
+    cases = [c for c in load_golden(group) if any("instances" in e for e in c["walks"].values())]
+    res = eng.run_batch([unit_of(X, c) for c in cases], want_walks=True)
+    bad = []
+    for c, a in zip(cases, res):
+        for side, ent in c["walks"].items():
+            if "instances" not in ent:
+                continue
+            w = a.walks[X.ExecSpace(side)]
+            if sorted(w.instances) != ent["instances"]:
+                bad.append((c["name"], side, "instances"))
+            if sorted([k, d, l[0], l[1]] for k, (d, l) in w.demands.items()) != ent["demands"]:
+                bad.append((c["name"], side, "demands"))
+            if sorted([k, v] for k, v in w.edges.items()) != ent["edges"]:
+                bad.append((c["name"], side, "edges"))
+    assert not bad, bad[:5]

@@ -110,10 +110,12 @@ typedef struct {
 
 /* one instance (spacecheck.py Instance): creating decl, walk (2*file + pass),
  * side (0 host 1 device), first-creation token, bindings and owner type,
- * legal edges: slots [ebase, ebase + decl.ncalls) of the edge array */
+ * legal edges: slots [ebase, ebase + decl.ncalls) of the edge array;
+ * spaces = the instance's execution spaces, bits 1 host 2 device 4 global
+ * (spacecheck.py Instance.spaces, GLOBAL = {__global__}) */
 typedef struct {
   uint32_t decl, walk, side, at;
-  uint32_t ebase, ecnt, flags, pad;
+  uint32_t ebase, ecnt, flags, spaces;
   uint64_t ckey;                    /* creation order (level, parent rank, statement, ordinal) */
   exs_val tb, hb, ot;
 } exs_inst;

@@ -68,7 +68,7 @@ DECL_DTYPE = np.dtype([("node", "<u4"), ("view", "<u4"), ("rec", "<u4"), ("order
 STRUCT_DTYPE = np.dtype([("node", "<u4"), ("view", "<u4")])
 _VAL = [("k", "u1"), ("targ", "u1"), ("bt", "u1"), ("pad", "u1"), ("rec", "<u4"), ("x", "<u8")]
 INST_DTYPE = np.dtype([("decl", "<u4"), ("walk", "<u4"), ("side", "<u4"), ("at", "<u4"),
-                       ("ebase", "<u4"), ("ecnt", "<u4"), ("flags", "<u4"), ("pad", "<u4"),
+                       ("ebase", "<u4"), ("ecnt", "<u4"), ("flags", "<u4"), ("spaces", "<u4"),
                        ("ckey", "<u8")] + [(f"{v}_{n}", t) for v in ("tb", "hb", "ot") for n, t in _VAL])
 NODE_DTYPE = np.dtype([("kind", "u1"), ("sub", "u1"), ("n", "<u2"), ("tok", "<u4"), ("c0", "<u4"),
                        ("c1", "<u4"), ("c2", "<u4"), ("next", "<u4"), ("hv", "<u8")])

@@ -773,7 +773,7 @@ int exs_get_instances(exs_handle x, exs_inst* out, uint64_t cap, uint64_t* n) {
     for (u64 i = 0; i < m; i++) {
       exs_inst& o = out[i];
       o.decl = in[i].fn; o.walk = in[i].walk; o.side = in[i].side; o.at = in[i].at;
-      o.ebase = in[i].ebase; o.ecnt = in[i].ecnt; o.flags = in[i].flags; o.pad = 0;
+      o.ebase = in[i].ebase; o.ecnt = in[i].ecnt; o.flags = in[i].flags; o.spaces = in[i].spaces;
       o.ckey = in[i].ckey;
       memcpy(&o.tb, &in[i].tb, sizeof(Val));
       memcpy(&o.hb, &in[i].hb, sizeof(Val));

@@ -17,7 +17,7 @@ from typing import Iterable, Optional
 import numpy as np
 
 from . import _native
-from .walks import BatchWalks
+from .walks import GLOBAL, BatchWalks, StructInfo
 from .messages import CODES, Renderer, stray_text
 
 
@@ -282,10 +282,23 @@ class Analysis:
     all_diagnostics: list = field(default_factory=list)
     walks: dict = field(default_factory=dict)
     passes: dict = field(default_factory=dict)  # pass kind -> status dict
+    _batch: object = field(default=None, repr=False, compare=False)
+    _file: int = field(default=0, repr=False, compare=False)
 
     @property
     def has_errors(self) -> bool:
         return any(d.is_error for d in self.diagnostics)
+
+    def structs(self, pass_index: int = 0) -> list:
+        """The struct declarations of one compile pass's AST, in source order
+        (walks.StructInfo: name, struct-level specifiers, member functions) --
+        the StructDecl items of ``parse(preprocess(text, profile.passes()[i]))``
+        (test_acceptance.py:132-135) as far as the classification needs them.
+        This is the AST the analysis walks: under the plain profile with
+        erase_specifiers its specifiers are erased (spacecheck.py:697-699)."""
+        if self._batch is None:
+            raise RuntimeError("struct declarations need an analysis run with want_walks=True")
+        return self._batch.structs_of(self._file, pass_index)
 
 
 # ---------------------------------------------------------------------------
@@ -340,7 +353,8 @@ class Engine:
         out = []
         for f, u in enumerate(units):
             ordered = finish_diagnostics(per_file[f])
-            a = Analysis(u[1], u[2], u[3], [d for d in ordered if not d.suppressed], ordered)
+            a = Analysis(u[1], u[2], u[3], [d for d in ordered if not d.suppressed], ordered,
+                         _batch=batch, _file=f)
             if walks is not None:
                 for p, side in ((0, HOST), (1, DEVICE)):
                     w = walks[2 * f + p]
@@ -393,14 +407,45 @@ def analyze_corpus(units: Iterable, profile: CompileProfile = CompileProfile(),
     return get_engine(device).run_batch(packed, want_walks=want_walks)
 
 
+def declared_spaces(spec: int) -> frozenset:
+    """sema.py:627-635 on specifier bits (1 host, 2 device; global counts as host)."""
+    out = {sp for b, sp in ((1, HOST), (2, DEVICE)) if spec & b}
+    return frozenset(out or {HOST})
+
+
+def propagate_spaces(analysis: Analysis) -> dict:
+    """Instance display name -> effective spaces over all walks (spacecheck.py:770-782)."""
+    out: dict = {}
+    for walk in analysis.walks.values():
+        for inst in walk.instances.values():
+            acc = out.setdefault(inst.display, set())
+            if inst.spaces == GLOBAL:
+                acc.add(ExecSpace.Global)
+            else:
+                acc.update(inst.spaces)
+    return {k: frozenset(v) for k, v in out.items()}
+
+
+def struct_member_spaces(struct: StructInfo) -> dict:
+    """Declared member spaces with the struct-level decoration distributed to
+    undecorated members (spacecheck.py:785-793)."""
+    out = {}
+    for name, spec in struct.members:
+        if not spec & 7 and struct.spec & 7:
+            spec = struct.spec
+        out[name] = declared_spaces(spec)
+    return out
+
+
 def stray_set(analysis: Analysis) -> list:
     """The stray-coded subset of the ordered diagnostics."""
     return [d for d in analysis.diagnostics if d.code in STRAY_CODES]
 
 
 __all__ = [
-    "Analysis", "CODE_REGISTRY", "CompileProfile", "Diagnostic", "Engine", "ExecSpace", "Mode",
-    "Severity", "SrcLoc", "TraitConfig", "Verdict", "analyze", "analyze_corpus", "check_unit",
-    "finish_diagnostics", "format_diagnostic", "get_engine", "legality", "stray_set",
-    "stray_text",
+    "Analysis", "CODE_REGISTRY", "CompileProfile", "Diagnostic", "Engine", "ExecSpace", "GLOBAL",
+    "Mode", "Severity", "SrcLoc", "StructInfo", "TraitConfig", "Verdict", "analyze",
+    "analyze_corpus", "check_unit", "declared_spaces", "finish_diagnostics", "format_diagnostic",
+    "get_engine", "legality", "propagate_spaces", "stray_set", "stray_text",
+    "struct_member_spaces",
 ]

@@ -25,6 +25,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Optional
 
+import numpy as np
+
 NONE = 0xFFFFFFFF
 # csrc/exs_common.cuh NodeKind
 (N_INT, N_STR, N_BOOL, N_HDCV, N_ARCH, N_NAME, N_TMP, N_TRAIT, N_MCONST, N_CALL, N_MCALL, N_SCALL,
@@ -49,6 +51,24 @@ class InstanceInfo:
     side: str
     display: str
     first_loc: tuple  # (line, col) of the first creation
+    spaces: object = None  # effective spaces: GLOBAL or frozenset of ExecSpace (Instance.spaces)
+
+
+GLOBAL = "global"  # sema.py GLOBAL: the spaces of a __global__ instance
+
+
+@dataclass
+class StructInfo:
+    """One struct declaration of a pass's AST (nodes.py StructDecl): the name, the
+    struct-level specifier bits (1 host, 2 device, 4 global) and the member
+    functions as (name, specifier bits) in declaration order."""
+    name: str
+    spec: int
+    members: list
+    line: int
+
+    def member_functions(self) -> list:
+        return [m for m, _ in self.members]
 
 
 class BatchWalks:
@@ -213,7 +233,7 @@ class BatchWalks:
         instances {key: InstanceInfo}; demands {key: (display, (line, col))};
         edges {caller key: [callee keys in post-order]}."""
         self._load()
-        from .exspace import Mode
+        from .exspace import DEVICE, HOST, Mode
         p2 = self.modes[f] is Mode.PROPOSAL2
         w = 2 * f + p
         view = int(self.status[w]["view"])
@@ -235,7 +255,10 @@ class BatchWalks:
             t = self.toks[int(r["at"])]
             loc = (int(t["line"]), int(t["col"]))
             disp = self.ren.display(i, 2)
-            instances[key] = InstanceInfo(key, dk, int(r["decl"]), SIDES[int(r["side"])], disp, loc)
+            sp = int(r["spaces"])
+            spaces = GLOBAL if sp & 4 else frozenset(s for b, s in ((1, HOST), (2, DEVICE)) if sp & b)
+            instances[key] = InstanceInfo(key, dk, int(r["decl"]), SIDES[int(r["side"])], disp, loc,
+                                          spaces)
             fn = self.nodes[int(self.decls[int(r["decl"])]["node"])]
             if int(fn["c0"]) != NONE or int(r["ot_k"]) == V_TYPE:  # spacecheck.py:345-346
                 demands.setdefault(dk, (disp, loc))
@@ -248,3 +271,21 @@ class BatchWalks:
             if callees:
                 edges[self.inst_keys(i, p2)[0]] = callees
         return instances, demands, edges
+
+    def structs_of(self, f: int, p: int) -> list:
+        """The struct declarations of (file f, pass p) in source order, each with
+        its member functions (sema.py _all_decls records owned by the struct)."""
+        self._load()
+        view = int(self.status[2 * f + p]["view"])
+        out, by_rec = [], {}
+        for r in range(len(self.structs)):
+            if int(self.structs[r]["view"]) == view:
+                nd = self.nodes[int(self.structs[r]["node"])]
+                t = self.toks[int(nd["tok"])]
+                by_rec[r] = StructInfo(self._text(int(nd["tok"])), int(nd["n"]) & 7, [], int(t["line"]))
+                out.append(by_rec[r])
+        if by_rec:
+            for d in np.nonzero(np.isin(self.decls["rec"], list(by_rec)))[0]:
+                fn = self.nodes[int(self.decls[d]["node"])]
+                by_rec[int(self.decls[d]["rec"])].members.append((self._text(int(fn["tok"])), int(fn["n"]) & 7))
+        return out

@@ -185,3 +185,27 @@ def test_walk_keys_match_the_reference(X, eng, group):
             if sorted([k, v] for k, v in w.edges.items()) != ent["edges"]:
                 bad.append((c["name"], side, "edges"))
     assert not bad, bad[:5]
+
+
+def test_classification_exports_match_the_reference(X, eng):
+    """propagate_spaces (spacecheck.py:770-782) over every walk, and
+    struct_member_spaces (spacecheck.py:785-793) of each struct of the first
+    pass's AST, equal the reference's on the golden units (classify.json.gz,
+    made by tests/golden/make_classify.py)."""
+    cases = load_golden("classify")
+    res = eng.run_batch([unit_of(X, c) for c in cases], want_walks=True)
+    bad, n_structs = [], 0
+    for c, a in zip(cases, res):
+        got = {k: sorted(s.value for s in v) for k, v in X.propagate_spaces(a).items()}
+        if got != c["spaces"]:
+            bad.append((c["name"], "spaces", got, c["spaces"]))
+        first = a.profile.pass_kinds()[0]
+        if c["structs"] is None or a.passes[first]["parse_failed"]:
+            continue
+        mine = [[s.name, {m: sorted(x.value for x in v) for m, v in X.struct_member_spaces(s).items()}]
+                for s in a.structs(0)]
+        n_structs += len(mine)
+        if mine != c["structs"]:
+            bad.append((c["name"], "structs", mine, c["structs"]))
+    assert not bad, bad[:3]
+    assert len(cases) > 800 and n_structs > 1000

@@ -193,6 +193,13 @@ void par_for_walk(i64 n, F f, cudaStream_t s, const char* fn = __builtin_FUNCTIO
     cudaEventRecord(pr.a, s);
   }
   if (pr.line == 0) nvtxRangePushA(pr.fn);  // named launches are NVTX ranges (ncu --nvtx-include)
+#ifdef EXS_WALK_CARVEOUT
+  static bool carve = false;  // per kernel instance: prefer L1 over shared memory
+  if (!carve) {
+    CK(cudaFuncSetAttribute(k_for_walk<F>, cudaFuncAttributePreferredSharedMemoryCarveout, EXS_WALK_CARVEOUT));
+    carve = true;
+  }
+#endif
   k_for_walk<<<grid, 128, 0, s>>>(f, n);
   if (pr.line == 0) nvtxRangePop();
   CK(cudaGetLastError());

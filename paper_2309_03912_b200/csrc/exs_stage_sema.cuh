@@ -19,6 +19,7 @@ struct SemaState {
   u64* siga_k = nullptr; u32* siga_v = nullptr; u32 siga_mask = 0; // walk-visible sig reps
   u32* fcand = nullptr, *fcand_cnt = nullptr;
   u32 NS = 0;                                  // top-level statements of all bodies
+  u64 NCS = 0;                                 // call sites of all bodies
   u32* stmt_node = nullptr, *stmt_cs = nullptr;  // per statement: node, call sites before it
   Tables tab;
   void free_all() {
@@ -455,7 +456,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       FnRec& r = fr[i];
       if (r.nstmts) r.ncalls = cpre[r.stmt_base + r.nstmts] - cpre[r.stmt_base];
     }, st);
-    sync(st);
+    S.NCS = get1(cpre + NSt, st);
     dfree(ns);
     dfree(sb);
     dfree(sfn);

@@ -378,7 +378,14 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     Timer t2(st);
     run_sema(L, H.P, H.S, B0, H.sc, st);
     H.t_stage[2] = t2.stop();
-    if (!cap_inst) cap_inst = (u32)std::min<u64>(std::max<u64>(65536, 4ull * H.S.NF + 1024), 0x7FFFFFFFull);
+    // roots (<= 2 per decl) plus the first level's growth bound of run_walk
+    // (one instance per call site, at most twice the roots): the table is not
+    // rehashed on the common two-level corpora
+    if (!cap_inst) {
+      const u64 nf4 = 4ull * H.S.NF;
+      cap_inst = (u32)std::min<u64>(std::max<u64>(65536, nf4 + std::min<u64>(H.S.NCS, nf4) + H.S.NCS / 8 + 65536 + 1024),
+                                    0x7FFFFFFFull);
+    }
     // the walk is retried alone (bigger instance table) after restoring the
     // diagnostics emitted by the earlier stages
     u32 nd0 = get1(H.d_ndiags, st);

@@ -67,6 +67,15 @@ struct WalkCfg {
   const FP* fp;
 };
 
+// a root candidate (run_walk roots): decl, walk, owner type, specifier inputs
+struct RootCand {
+  u32 i, p, file, walk;
+  u8 mode, cfg;
+  bool fast, free_main;  // fast: no specifier needs evaluation
+  u16 sf;                // specifier bits of the owning struct
+  Val ot;
+};
+
 // build a walker for an existing instance
 EXS_HD inline void walker_for(Walker& w, const WalkCfg& C, const WalkBufs& B, u32 id, u64 rank) {
   const Inst& I = B.inst[id];
@@ -239,16 +248,117 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       dfree(key);
     }
     const u32* rcc = rcand;
-    EXS_TAG("walk_roots");
-    par_for_walk(NRC, [=] EXS_HD (i64 kk) {
-      const u32 x = rcc[kk];
-      u32 i = x >> 1, p = x & 1;
-      const FnRec& r = fr[i];
-      u32 file = vf[r.view];
-      u32 walk = 2 * file + p;
+    // a root candidate: its decl, walk, owner type and (when no specifier
+    // needs evaluation) its sides
+    // rot: the canonical owner record per candidate, found once (step 1)
+    u32* rot = dalloc<u32>((u64)NRC + 1);
+    const u32* rotc = rot;
+    auto cand = [=] EXS_HD (u32 x, u32 kk, bool find_owner) -> RootCand {
+      RootCand q;
+      q.i = x >> 1; q.p = x & 1;
+      const FnRec& r = fr[q.i];
+      q.file = vf[r.view];
+      q.walk = 2 * q.file + q.p;
       const Node& fn = nd[r.node];
-      u8 c = cfgs[file];
-      u8 mode = c & CFG_MODE_MASK;
+      q.cfg = cfgs[q.file];
+      q.mode = q.cfg & CFG_MODE_MASK;
+      q.ot = vnone();
+      if (r.rec != NONE) {
+        q.ot.k = V_TYPE; q.ot.x = rr[r.rec].name;
+        q.ot.rec = find_owner ? tab->smap.find(vkey(r.view, rr[r.rec].name)) : rotc[kk];
+        q.ot.bt = BT_NONE; q.ot.targ = 0;
+      }
+      q.fast = !(q.mode == MODE_P1 && (fn.n & (FF_HPRED | FF_DPRED)));
+      q.free_main = tk[fn.tok].id == W_MAIN && r.rec == NONE;
+      q.sf = r.rec != NONE ? nd[rr[r.rec].node].n : 0;
+      return q;
+    };
+    // 1. candidates whose specifiers need no evaluation: insert the keys, keep
+    // the minimum creation key (decl order x side order, spacecheck.py:272-283)
+    // and log lowering non-inserters by SLOT; ids come from a scan (no shared
+    // counter: at this rate one counter serialises the kernel)
+    u32* rslot = dalloc<u32>(2ull * NRC + 1);
+    const u32 nlog0 = get1(B.n_log, st);
+    {
+      u32* rs = rslot;
+      EXS_TAG("walk_roots");
+      u32* ro = rot;
+      par_for_walk(NRC, [=] EXS_HD (i64 kk) {
+        rs[2 * kk] = rs[2 * kk + 1] = NONE;
+        const RootCand q = cand(rcc[kk], (u32)kk, true);
+        ro[kk] = q.ot.rec;
+        if (!q.fast) { rs[2 * kk] = NONE - 1; return; }  // evaluated in step 3
+        const FnRec& r = fr[q.i];
+        const u16 fl = nd[r.node].n;
+        const u8 sides = (fl & FF_G) ? 2 : (static_spaces(fl, q.free_main, q.sf, q.mode, 0) & 3);
+        u32 k = 0;
+        for (u8 sd = 0; sd < 2; sd++) {
+          if (!((sides >> sd) & 1)) continue;
+          const unsigned long long ck = ((unsigned long long)(q.i & 0x3FFFFFFu) << 28) | k++;
+          const IKey key = make_ikey(r.sig_rep, vnone(), vnone(), q.ot, q.walk, sd);
+          bool inserted;
+          const u32 slot = slot_insert(B, key, inserted);
+          if (slot == NONE) return;
+          if (inserted) rs[2 * kk + sd] = slot;
+          const unsigned long long old = at_min64(&B.sck[slot], ck);
+          if (inserted || old < ck) continue;
+          const u32 li = at_inc_agg(B.n_log);
+          if (li < B.cap_log) {
+            CreateLog& L = B.log[li];
+            L.ckey = ck; L.inst = slot; L.at = nd[r.node].tok; L.fn = q.i;
+          } else {
+            at_or(B.overflow, 4);
+          }
+        }
+      }, st);
+    }
+    // 2. ids in candidate order, records, published ids
+    {
+      const u32 NS2 = 2 * NRC;
+      u32* ins = dalloc<u32>(NS2 + 1);
+      u32* ids = dalloc<u32>(NS2 + 1);
+      const u32* rs = rslot;
+      par_for(NS2 + 1, [=] EXS_HD (i64 j) { ins[j] = j < NS2 && rs[j] < NONE - 1; }, st);
+      excl_scan_u32(ins, ids, NS2 + 1, sc, st);
+      const u32 total = get1(ids + NS2, st);
+      const u32* id_of = ids;
+      par_for(NS2, [=] EXS_HD (i64 j) {
+        const u32 slot = rs[j];
+        if (slot >= NONE - 1) return;
+        const u32 id = id_of[j];
+        if (id >= B.cap_inst) { at_or(B.overflow, 1u); return; }
+        const RootCand q = cand(rcc[j >> 1], (u32)(j >> 1), false);
+        const u8 sd = (u8)(j & 1);
+        const FnRec& r = fr[q.i];
+        const Node& fn = nd[r.node];
+        const IKey key = make_ikey(r.sig_rep, vnone(), vnone(), q.ot, q.walk, sd);
+        fill_instance(B.inst[id], tab, key, q.i, vnone(), vnone(), sd, r.rec, q.ot, fn.tok, q.walk,
+                      static_spaces(fn.n, q.free_main, q.sf, q.mode, sd), 0, slot);
+        B.sid[slot] = id;
+      }, st);
+      u32* ni = B.n_inst;
+      par_for(1, [=] EXS_HD (i64) { *ni = total; }, st);
+      // log entries of step 1 hold slots: resolve them to ids
+      const u32 nlog1 = get1(B.n_log, st);
+      const u32 lo = nlog0, hi = nlog1 < B.cap_log ? nlog1 : B.cap_log;
+      if (hi > lo) {
+        CreateLog* lg = B.log; const u32* sid = B.sid;
+        par_for(hi - lo, [=] EXS_HD (i64 j) { lg[lo + j].inst = sid[lg[lo + j].inst]; }, st);
+      }
+      sync(st);
+      dfree(ins);
+      dfree(ids);
+    }
+    // 3. proposal1 conditional specifiers: evaluated by a walker
+    const u32* rs3 = rslot;
+    par_for_walk(NRC, [=] EXS_HD (i64 kk) {
+      if (rs3[2 * kk] != NONE - 1) return;
+      const RootCand q = cand(rcc[kk], (u32)kk, false);
+      const u32 i = q.i, p = q.p, file = q.file, walk = q.walk;
+      const FnRec& r = fr[i];
+      const Node& fn = nd[r.node];
+      const u8 c = q.cfg, mode = q.mode;
+      const Val ot = q.ot;
       Walker w;
       w.S.init(tab, r.view, c);
       w.B = &B; w.T = tab; w.file = file; w.walk = walk; w.inst_id = NONE;
@@ -258,11 +368,6 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       w.parent_rank = i; w.contract = false;
       w.stmt_k = 0; w.stmt_ord = 0; w.stmt_cs_base = 0; w.cs_ord = 0;
       w.silent = false; w.asp = 0; w.nloc = 0; w.wdepth = 0; w.ebase = 0; w.ecnt = 0;
-      Val ot = vnone();
-      if (r.rec != NONE) {
-        u32 canon = w.S.struct_of(rr[r.rec].name);
-        ot.k = V_TYPE; ot.rec = canon; ot.x = rr[r.rec].name; ot.bt = BT_NONE; ot.targ = 0;
-      }
       Env none; none.clear();
       u8 sides;
       if (fn.n & FF_G) sides = 2;
@@ -284,6 +389,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     }, st);
     sync(st);
     dfree(rcand);
+    dfree(rslot);
+    dfree(rot);
   }
   prof_mark(st);
   // ---- levels
@@ -316,15 +423,23 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     u32 nnew = n_now - prev_n;
     if (!nnew) break;
     prof_mark(st);
-    // frontier: new instances with bodies, ordered by creation key
+    // frontier: new instances with bodies, ordered by creation key.  A body
+    // with no statements and no parameters has nothing to walk (no calls, no
+    // parameter types to resolve): it is left out.  Creation keys only order
+    // the creators among themselves, so dropping non-creators keeps them.
     grow(front, front_cap, nnew + 1, 0, st);
     u32 nf;
     {
       const Inst* in = W.inst;
+      const FnRec* fns = S.fns; const Node* nd = P.nodes;
       u32 base = prev_n;
       u32* fr_tmp = dalloc<u32>(nnew + 1);
-      nf = select_idx(nnew, [=] EXS_HD (u32 j) -> bool { return (in[base + j].flags & IF_BODY) != 0; },
-                      fr_tmp, L.cnt, sc, st);
+      nf = select_idx(nnew, [=] EXS_HD (u32 j) -> bool {
+        const Inst& I = in[base + j];
+        if (!(I.flags & IF_BODY)) return false;
+        const FnRec& r = fns[I.fn];
+        return r.nstmts != 0 || nd[r.node].c1 != NONE;
+      }, fr_tmp, L.cnt, sc, st);
       u64* keys = dalloc<u64>(nf + 1);
       par_for(nf, [=] EXS_HD (i64 j) { fr_tmp[j] += base; keys[j] = in[fr_tmp[j]].ckey; }, st);
       sort_pairs(keys, fr_tmp, nf, sc, st);

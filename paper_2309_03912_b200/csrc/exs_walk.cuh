@@ -167,6 +167,97 @@ EXS_HD inline void inst_publish(const WalkBufs& B, u32 slot, u32 id) {
   *(volatile u32*)&B.sid[slot] = id;
 }
 
+// instance key and record (spacecheck.py:325-341)
+EXS_HD inline IKey make_ikey(u32 sig_rep, const Val& tb, const Val& hb, const Val& ot, u32 walk, u8 side) {
+  IKey k;
+  k.a = ((u64)sig_rep << 32) | tcode(tb);
+  k.b = (1ull << 63) | ((u64)tcode(ot) << 32) | ((u64)walk << 3) |
+        ((u64)(hb.k == V_HDC ? hb.x : 0) << 1) | side;
+  return k;
+}
+EXS_HD inline void fill_instance(Inst& I, const Tables* T, const IKey& k, u32 fi, const Val& tb, const Val& hb,
+                                 u8 side, u32 orec, const Val& ot, u32 at_tok, u32 walk, u8 sp, u8 clevel,
+                                 u32 slot) {
+  const FnRec& fr = T->fns[fi];
+  const Node& fnn = T->nodes[fr.node];
+  I.ka = k.a; I.kb = k.b;
+  I.ckey = ~0ull; I.fn = fi; I.orec = orec; I.walk = walk; I.at = at_tok;
+  I.ebase = 0; I.ecnt = 0;
+  I.tb = tb; I.hb = hb; I.ot = ot;
+  I.side = side; I.spaces = sp; I.level = clevel; I.slot = slot;
+  I.flags = (fnn.n & FF_BODY) ? IF_BODY : 0;
+  if (T->toks[fnn.tok].id == W_MAIN && !(fr.flags & FR_OWNER)) I.flags |= IF_MAIN;
+}
+// key insertion without an id (the level-0 roots allocate ids by a scan
+// afterwards instead of one shared counter): the slot, NONE if the table is full
+EXS_HD inline u32 slot_insert(const WalkBufs& B, const IKey& k, bool& inserted) {
+  u32 h = (u32)mix64(k.a ^ mix64(k.b)) & B.mask;
+  inserted = false;
+  for (u32 probes = 0; probes <= B.mask; probes++) {
+    IKey old;
+    if (ikey_cas(&B.slots[h], k, old)) { inserted = true; return h; }
+    if (old.a == k.a && old.b == k.b) return h;
+    h = (h + 1) & B.mask;
+  }
+  at_or(B.overflow, 1u);
+  return NONE;
+}
+
+// The part of _instantiate (spacecheck.py:312-351) after effective_spaces:
+// look up or insert the key, fill a new record, and keep the minimum creation
+// key of this level (with a log entry for a non-inserting creator that lowered
+// it; the post-level fixup applies the entry whose key equals the minimum).
+EXS_HD EXS_FI u32 create_instance(const WalkBufs& B, const Tables* T, u32 fi, const Val& tb, const Val& hb,
+                                  u8 want_side, u32 orec, const Val& ot, u32 at_tok, u32 walk, u8 sp,
+                                  u8 clevel, unsigned long long ck) {
+  const FnRec& fr = T->fns[fi];
+  const IKey k = make_ikey(fr.sig_rep, tb, hb, ot, walk, want_side);
+  bool inserted;
+  u32 slot;
+  u32 id = inst_lookup_or_insert(B, k, inserted, slot);
+  if (id == NONE) return NONE;
+  if (inserted) {
+    fill_instance(B.inst[id], T, k, fi, tb, hb, want_side, orec, ot, at_tok, walk, sp, clevel, slot);
+    inst_publish(B, slot, id);
+  }
+  if (id >= B.lvl_base) {
+    // a creator in this level: the minimum creation key wins.  A creator
+    // logs (ckey, location, decl) only if it lowered the minimum when it
+    // arrived -- the final winner always did -- and not if it inserted (the
+    // record already holds its data).  The post-level fixup applies the log
+    // entry whose key equals the final minimum; none matches when the
+    // inserter holds it.
+    const unsigned long long old = at_min64(&B.sck[slot], ck);
+    if (inserted || old < ck) return id;
+    u32 li = at_inc_agg(B.n_log);
+    if (li < B.cap_log) {
+      CreateLog& L = B.log[li];
+      L.ckey = ck; L.inst = id; L.at = at_tok; L.fn = fi;
+    } else {
+      at_or(B.overflow, 4);
+    }
+  }
+  return id;
+}
+
+// effective_spaces (sema.py:670-703) of a declaration whose specifiers need no
+// evaluation (everything but proposal1 conditional specifiers): 1 H 2 D 3 HD 4 G.
+// sf: specifier bits of the owning struct (0 for free functions).
+EXS_HD inline u8 static_spaces(u16 fl, bool free_main, u16 sf, u8 mode, u8 side) {
+  if (fl & FF_G) return 4;
+  if (mode == MODE_P2) {
+    if (free_main) return 1;
+    if (!(fl & (FF_H | FF_D | FF_G))) {
+      if (sf & (SF_H | SF_D | SF_G)) fl = sf;
+      else return (u8)(1u << side);
+    }
+  }
+  u8 sp = 0;
+  if (fl & FF_H) sp |= 1;
+  if (fl & FF_D) sp |= 2;
+  return sp ? sp : 1;
+}
+
 // ---------------------------------------------------------------------------
 
 // verdict table (spacecheck.py:86-132) for direct calls; callee 1=H 2=D
@@ -268,54 +359,16 @@ struct Walker {
   EXS_HD EXS_FI u32 instantiate(u32 fi, const Val& tb, const Val& hb, u8 want_side, u32 orec,
                          const Env& obinds, const Val& ot, u32 at_tok) {
     u32 my_local = (stmt_k << 12) | (stmt_ord++ & 0xFFFu);
-    const Node& fnn = N(T->fns[fi].node);
     u8 sp;
     S.depth = 0;
     u8 st = S.spaces(fi, &obinds, tb, hb, want_side, at_tok, orec, sp);
     if (S.contract) { contract = true; return NONE; }
     if (st == ST_SEMA) { emit_err(); return NONE; }
     if (st == ST_SUBST) { emit_tok(C_E0001, at_tok, M_W_PRED_CONST); return NONE; }
-    const FnRec& fr = T->fns[fi];
-    IKey k;
-    k.a = ((u64)fr.sig_rep << 32) | tcode(tb);
-    k.b = (1ull << 63) | ((u64)tcode(ot) << 32) | ((u64)walk << 3) |
-          ((u64)(hb.k == V_HDC ? hb.x : 0) << 1) | want_side;
-    bool inserted;
-    u32 slot;
-    u32 id = inst_lookup_or_insert(*B, k, inserted, slot);
-    if (id == NONE) return NONE;
     unsigned long long ck = ((unsigned long long)clevel << 54) |
                             ((unsigned long long)(parent_rank & 0x3FFFFFFull) << 28) |
                             (my_local & 0xFFFFFFFu);
-    if (inserted) {
-      Inst& I = B->inst[id];
-      I.ka = k.a; I.kb = k.b;
-      I.ckey = ~0ull; I.fn = fi; I.orec = orec; I.walk = walk; I.at = at_tok;
-      I.ebase = 0; I.ecnt = 0;
-      I.tb = tb; I.hb = hb; I.ot = ot;
-      I.side = want_side; I.spaces = sp; I.level = clevel; I.slot = slot;
-      I.flags = (fnn.n & FF_BODY) ? IF_BODY : 0;
-      if (K(fnn.tok).id == W_MAIN && !(fr.flags & FR_OWNER)) I.flags |= IF_MAIN;
-      inst_publish(*B, slot, id);
-    }
-    if (id >= B->lvl_base) {
-      // a creator in this level: the minimum creation key wins.  A creator
-      // logs (ckey, location, decl) only if it lowered the minimum when it
-      // arrived -- the final winner always did -- and not if it inserted (the
-      // record already holds its data).  The post-level fixup applies the log
-      // entry whose key equals the final minimum; none matches when the
-      // inserter holds it.
-      const unsigned long long old = at_min64(&B->sck[slot], ck);
-      if (inserted || old < ck) return id;
-      u32 li = at_inc_agg(B->n_log);
-      if (li < B->cap_log) {
-        CreateLog& L = B->log[li];
-        L.ckey = ck; L.inst = id; L.at = at_tok; L.fn = fi;
-      } else {
-        at_or(B->overflow, 4);
-      }
-    }
-    return id;
+    return create_instance(*B, T, fi, tb, hb, want_side, orec, ot, at_tok, walk, sp, clevel, ck);
   }
 
   EXS_HD void add_binds(const Node& fnn, const Val& tb, const Val& hb, Env& e) const {

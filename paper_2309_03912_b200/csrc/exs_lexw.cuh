@@ -83,6 +83,11 @@ struct SRec {
   u8 pad;
 };
 
+// per-word masks of phases 1-2, written by the count pass for the emit pass
+struct alignas(16) WordMasks {
+  u32 f, lsb, nl, own, starts, err, idst, DGc, IDc, qs, qt, sm, pst, pad[3];
+};
+
 struct LexW {
   const u8* src; u32 n; bool vec;  // vec: 16-byte aligned source, vector loads allowed
   const u32* sp; const u32* fs;    // splice / file-start bitmaps
@@ -96,6 +101,7 @@ struct LexW {
   u32 ns;                          // special lines recorded
   // emit pass
   const u32* fdir; const DirRec* dirs; const u8* dlive; FP* fp;
+  WordMasks* wm;                   // count pass writes, emit pass reads (nullptr: recompute)
 };
 
 EXS_HD inline u32 upper_file(const u32* foff, u32 F, u32 p) {
@@ -294,10 +300,19 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
     gnl0 = (u32)e.lc;
   }
   const u32 st0 = st;
+  u32 f, fend, sm, sbb, nl, lsb, own, IDc, DGc, idst, qs, qt, pst, starts, err;
+  if (EMIT && X.wm) {
+    // the count pass left the word's masks (phases 1-2 are not redone)
+    const WordMasks M = X.wm[w];
+    f = M.f; lsb = M.lsb; nl = M.nl; own = M.own; starts = M.starts; err = M.err; idst = M.idst;
+    DGc = M.DGc; IDc = M.IDc; qs = M.qs; qt = M.qt; sm = M.sm; pst = M.pst; sbb = 0;
+    fend = X.foff[f + 1];
+  } else {
   bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
   // ---- phase 1
-  u32 bl = 0, sm = 0, sbb = 0, nl = 0, lsb = 0;
-  u32 id = 0, dg = 0, ws = 0, ps = 0, sg = 0, qt = 0, sl = 0;
+  u32 bl = 0;
+  sm = 0; sbb = 0; nl = 0; lsb = 0; qt = 0;
+  u32 id = 0, dg = 0, ws = 0, ps = 0, sg = 0, sl = 0;
 #pragma unroll
   for (u32 j = 0; j < 32; j++) {
     const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
@@ -323,7 +338,8 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
   }
   lsb &= valid; nl &= valid;
   // ---- special lines: bytes excluded from the plain tokenizer; owned ones
-  u32 spm = 0, own = 0;
+  u32 spm = 0;
+  own = 0;
   {
     u32 li = li0, seg = 0, rest = lsb;
     bool cur = li != NONE && X.special[li] != 0;
@@ -340,8 +356,8 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
     spm &= valid;
   }
   // file of the word's first byte
-  u32 f = upper_file(X.foff, X.F, base);
-  u32 fend = X.foff[f + 1];
+  f = upper_file(X.foff, X.F, base);
+  fend = X.foff[f + 1];
   // end of the file holding the word's last byte (look-ahead past the word)
   const u32 fe_last = (fsw & ~1u) ? X.foff[upper_file(X.foff, X.F, base + m - 1) + 1] : fend;
   // ---- phase 2: code characters and token starts
@@ -351,7 +367,8 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
     const u8 nx = q < fe_last ? X.src[q] : 0;
     if (nx == '/' || nx == '*') code &= ~0x80000000u;
   }
-  const u32 IDc = id & code, DGc = dg & code, ALc = IDc & ~DGc;
+  IDc = id & code; DGc = dg & code;
+  const u32 ALc = IDc & ~DGc;
   u32 cin_id = 0, cin_num = 0, cin_ps = 0, pskip = 0;
   if ((code & 1u) && !(lsb & 1u) && base > 0 && st0 == S_CODE) {
     const u8 pc = X.src[base - 1];
@@ -388,11 +405,12 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
       rest &= rest - 1;
     }
   }
-  const u32 idst = rs | (ALc & ((P << 1) | cin_num));
-  const u32 qs = qt & code;
+  idst = rs | (ALc & ((P << 1) | cin_num));
+  qs = qt & code;
   const u32 sgs = sg & code;
   const u32 PSc = ps & code;
-  u32 pst = 0, perr = 0;
+  pst = 0;
+  u32 perr = 0;
   {
     u32 runs = PSc & ~(((PSc << 1) | cin_ps) & ~fsw);
     if (cin_ps && pskip < 32 && ((PSc >> pskip) & 1u)) runs |= 1u << pskip;
@@ -415,9 +433,16 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
       }
     }
   }
-  const u32 starts = idst | qs | sgs | pst;
+  starts = idst | qs | sgs | pst;
+  err = (code & ~(id | ws | ps | sg | qt | sl)) | (sl & code) | perr;
+  if (!EMIT && X.wm) {
+    WordMasks M;
+    M.f = f; M.lsb = lsb; M.nl = nl; M.own = own; M.starts = starts; M.err = err; M.idst = idst;
+    M.DGc = DGc; M.IDc = IDc; M.qs = qs; M.qt = qt; M.sm = sm; M.pst = pst; M.pad[0] = M.pad[1] = M.pad[2] = 0;
+    X.wm[w] = M;
+  }
+  }
   u32 ntok = EMIT ? 0 : popc32(starts);
-  const u32 err = (code & ~(id | ws | ps | sg | qt | sl)) | (sl & code) | perr;
   // ---- phase 3: events in source order
   u32 fnl0 = X.fnl[f];
   u8 fmask = 0, live = 3;

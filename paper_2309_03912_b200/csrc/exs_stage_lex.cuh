@@ -152,6 +152,8 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
   SRec* srec = dalloc<SRec>(srcap);
   X.srec = srec; X.nsrec = S.cnt + 4; X.srcap = srcap;
   u32* wcnt = dalloc<u32>(W + 1);
+  WordMasks* wmask = dalloc<WordMasks>(W + 1);  // 64 B per word, read back by lex_emit
+  X.wm = wmask;
   {
     const LexW Xc = X;
     EXS_TAG("lex_count");
@@ -292,6 +294,9 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
     EXS_TAG("lex_emit");
     par_for(W, [=] EXS_HD (i64 w) { lex_word<true>(Xc, (u32)w, tk + wt[w], wt[w]); }, st);
   }
+  sync(st);
+  dfree(wmask);
+  X.wm = nullptr;
   if (S.NS) {
     const u8* s = S.src; const u32* sp = S.splice; const u32* fo = S.foff; const SRec* sr = S.srec;
     Tok* tk = S.toks; FP* fp = S.fp;

@@ -35,13 +35,13 @@ def main():
             kern = {}
             for ln in h.lib.exs_profile_text().decode().splitlines():
                 p = ln.split()
-                if len(p) >= 4 and not p[0].startswith("[") and ":" not in p[0]:
+                if len(p) >= 4 and not p[0].startswith("["):
                     kern[p[0]] = kern.get(p[0], 0.0) + float(p[1])
             h.set_option(2, 0)
             if best is None or st["ms_total"] < best["ms_total"]:
                 best, kbest = st, kern
         st = best
-        ks = " ".join(f"{k}={v:.1f}" for k, v in sorted(kbest.items(), key=lambda kv: -kv[1])[:8])
+        ks = " ".join(f"{k}={v:.1f}" for k, v in sorted(kbest.items(), key=lambda kv: -kv[1])[:int(os.environ.get("TOPK", "8"))])
         print(f"{Path(lib).name}: {st['ms_total']:.1f} ms = {mb / st['ms_total']:.2f} GB/s | lex {st['ms_lex']:.1f}"
               f" parse {st['ms_parse']:.1f} sema {st['ms_sema']:.1f} walk {st['ms_walk']:.1f} | diags"
               f" {st['diagnostics']} inst {st['instances']} retries {st['retries']} | {ks}", flush=True)

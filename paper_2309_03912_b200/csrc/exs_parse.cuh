@@ -51,6 +51,7 @@ struct Parser {
 
   u32 defer_open, defer_close;  // view positions of a body parsed separately (or NONE)
   bool deferred;
+  u32 block_stmts;              // statements of the last block parsed
 
   EXS_HD void init(const PView& view, Node* nd, u32 base, u32 cap, u32 start) {
     v = view; nodes = nd; nbase = base; nused = 0; ncap = cap; pos = start;
@@ -410,6 +411,7 @@ struct Parser {
     }
     u32 body = NONE;
     bool has_body = false;
+    u32 nst = 0;
     if (at_p(P_LBRACE) && pos == defer_open) {
       // a large body: its statements are parsed in parallel afterwards and
       // linked under this FN node (run_parse step 4b)
@@ -419,6 +421,7 @@ struct Parser {
     } else if (at_p(P_LBRACE)) {
       if (!block(body)) return NONE;
       has_body = true;
+      nst = block_stmts;
     } else if (!need_p(P_SEMI, EX_FN_BODY)) {
       return NONE;
     }
@@ -438,6 +441,7 @@ struct Parser {
     f.sub = (u8)params.count;
     Node& x = N(xid);
     x.c0 = req; x.c1 = hp; x.c2 = dp; x.next = ret;
+    x.hv = nst;  // top-level statements of the body (a deferred body: set when linked)
     return id;
   }
 
@@ -512,13 +516,16 @@ struct Parser {
     if (!enter()) return false;
     if (!need_p(P_LBRACE, EX_LBRACE)) return false;
     ListB l;
+    u32 cnt = 0;
     while (!at_p(P_RBRACE)) {
       u32 s = stmt();
       if (s == NONE) return false;
       push(l, s);
+      cnt++;
     }
     if (!need_p(P_RBRACE, EX_RBRACE)) return false;
     out = l.head;
+    block_stmts = cnt;
     depth--;
     return true;
   }

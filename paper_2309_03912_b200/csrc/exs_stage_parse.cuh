@@ -30,10 +30,11 @@ struct ParseState {
   u32* fitem_view = nullptr;
   Node* nodes = nullptr;
   u64 n_nodes = 0;
+  u32* seg_root = nullptr;  // statement node of each split-body segment (FNX.hv >> 32 - 1 indexes it)
   void free_all() {
     void* ps[] = {vbase, vfile, vpass, veof, vtok, vview, item_start, item_view, item_root,
                   item_end, item_stat, item_err, vfirst, vbad, vstat, vfb_base, vfb_cnt,
-                  fb_items, vfi, fitems, fitem_view, nodes, vdirect, vkid};
+                  fb_items, vfi, fitems, fitem_view, nodes, vdirect, vkid, seg_root};
     for (void* p : ps) dfree(p);
   }
 };
@@ -475,10 +476,18 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       bool first = k == 0 || ssc[k - 1] < is[j];
       bool last = !(k + 1 < NSSc && ssc[k + 1] < inext);
       nd[sroot[k]].next = last ? NONE : sroot[k + 1];
-      if (first) nd[ir[j]].c2 = sroot[k];
+      if (first) {
+        nd[ir[j]].c2 = sroot[k];
+        u32 lo2 = k, hi2 = NSSc;  // the body's statements: segments [k, first segment >= inext)
+        while (lo2 < hi2) { u32 mid = (lo2 + hi2) / 2; if (ssc[mid] < inext) lo2 = mid + 1; else hi2 = mid; }
+        // FNX: statement count, and (first segment + 1) << 32: the statement
+        // list of this body is seg_root[k, k + count)
+        nd[ir[j] + 1].hv = ((u64)(k + 1) << 32) | (lo2 - (u32)k);
+      }
     }, st);
     sync(st);
-    dfree(sroot); dfree(sbad); dfree(sstat); dfree(serr); dfree(sperm);
+    P.seg_root = sroot;
+    dfree(sbad); dfree(sstat); dfree(serr); dfree(sperm);
   }
   dfree(ss);
   dfree(titem);

@@ -252,6 +252,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
     Node* nd = P.nodes; const u32* fit = P.fitems; const u32* fiv = P.fitem_view;
     const u32* ifn = S.item_fn; const u32* irc = S.item_rec; FnRec* fr = S.fns; RecRec* rr = S.recs;
     const Tok* tk = L.toks;
+    EXS_TAG("sema_decl_records");
     par_for(FI, [=] EXS_HD (i64 i) {
       Node& n = nd[fit[i]];
       u32 v = fiv[i];
@@ -259,7 +260,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       auto put = [&](u32 node, u32 rec) {
         FnRec& r = fr[f];
         r.node = node; r.view = v; r.rec = rec; r.order = f;
-        r.name = tk[nd[node].tok].hv; r.sig = 0; r.sig_rep = f; r.ncalls = 0;
+        r.name = nd[node].hv; r.sig = 0; r.sig_rep = f; r.ncalls = 0;
         r.flags = rec == NONE ? 0 : FR_MEMBER;
         nd[node + 1].tok = f;  // FNX.tok -> decl record
         f++;
@@ -268,7 +269,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       else if (n.kind == N_STRUCT) {
         u32 r = irc[i];
         RecRec& q = rr[r];
-        q.node = fit[i]; q.view = v; q.order = r; q.dup = 0; q.name = tk[n.tok].hv;
+        q.node = fit[i]; q.view = v; q.order = r; q.dup = 0; q.name = n.hv;
         n.c2 = r;
         for (u32 m = n.c1; m != NONE; m = nd[m].next) if (nd[m].kind == N_FN) put(m, r);
       }
@@ -403,6 +404,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
     FnRec* fr = S.fns;
     // bodies are scanned statement-parallel (BodyScan carries no state across
     // top-level statements): count, tabulate, scan each statement once
+    EXS_TAG("sema_body_count");
     par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
       r.nstmts = 0; r.ncalls = 0;
@@ -414,8 +416,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
         const Tok& t = tk[n.tok];
         emit_diag(B, mkdiag(vf[r.view], t.line, t.col, C_E0001, M_S_COND_SPEC_MODE));
       }
-      if (n.n & FF_BODY)
-        for (u32 s = n.c2; s != NONE; s = nd[s].next) r.nstmts++;
+      r.nstmts = (n.n & FF_BODY) ? (u32)(nd[r.node + 1].hv & 0xFFFFFFFFu) : 0;  // counted by the parser
     }, st);
     // per-statement tables: statements of a body are walked in parallel (K6)
     u32* ns = dalloc<u32>(NF + 1);
@@ -430,16 +431,32 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
     u32* scnt = dalloc<u32>(NSt + 1);
     u32* cpre = dalloc<u32>(NSt + 1);
     u32* sn = S.stmt_node; u32* scs = S.stmt_cs;
+    const u32* sroot = P.seg_root;
+    EXS_TAG("sema_body_table");
     par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
       r.stmt_base = sb[i];
       if (!r.nstmts) return;
       u32 k = sb[i];
-      for (u32 s = nd[r.node].c2; s != NONE; s = nd[s].next, k++) {
-        sn[k] = s;
-        sfn[k] = (u32)i;
-        if (nd[s].kind == N_SVAR) r.flags |= FR_VARDECL;
+      bool var = false;
+      const u64 x = nd[r.node + 1].hv;
+      if (x >> 32) {
+        // a split body: its statements are listed by segment (no list walk)
+        const u32* sg = sroot + ((x >> 32) - 1);
+        for (u32 t = 0; t < r.nstmts; t++) {
+          const u32 s = sg[t];
+          sn[k + t] = s;
+          sfn[k + t] = (u32)i;
+          var |= nd[s].kind == N_SVAR;
+        }
+      } else {
+        for (u32 s = nd[r.node].c2; s != NONE; s = nd[s].next, k++) {
+          sn[k] = s;
+          sfn[k] = (u32)i;
+          var |= nd[s].kind == N_SVAR;
+        }
       }
+      if (var) r.flags |= FR_VARDECL;
     }, st);
     EXS_TAG("sema_bodyscan");
     par_for_walk(NSt + 1, [=] EXS_HD (i64 k) {

@@ -54,12 +54,19 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   u32* split = dalloc<u32>(F + 2);
   dzero(split, (F + 2) * 4, st);
   u32* irr = split + F + 1;  // some token is not live in all its file's passes, or a pass failed
+  // the one pass over the token records also fills the per-position file and
+  // kind/id arrays of the common one-view-per-file layout (dropped otherwise)
+  u32* tview = dalloc<u32>((u64)T + 1);
+  u16* tkid = dalloc<u16>((u64)T + 1);
   {
     const Tok* tk = L.toks; const u8* cf = L.cfg;
     par_for(T, [=] EXS_HD (i64 t) {
-      const u8 m = tk[t].mask;
-      if (m == 1 || m == 2) at_or(&split[tk[t].file], 1u);
-      if (m != ((cf[tk[t].file] & CFG_PLAIN) ? 1 : 3)) at_or(irr, 1u);
+      const Tok& k = tk[t];
+      const u8 m = k.mask;
+      tview[t] = k.file;
+      tkid[t] = (u16)(((u32)k.kind << 8) | k.id);
+      if (m == 1 || m == 2) at_or(&split[k.file], 1u);
+      if (m != ((cf[k.file] & CFG_PLAIN) ? 1 : 3) && !ld_volatile(irr)) at_or(irr, 1u);
     }, st);
   }
   // 2. views per file
@@ -104,20 +111,17 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       }, st);
     }
     P.vtok = dalloc<u32>(VT + 1);
-    P.vview = dalloc<u32>(VT + 1);
-    P.vkid = dalloc<u16>(VT + 1);
+    P.vview = tview;
+    P.vkid = tkid;
     {
-      const Tok* tk = L.toks; u32* vt = P.vtok; u32* vv = P.vview; u16* vkd = P.vkid;
-      par_for(T, [=] EXS_HD (i64 t) {
-        const Tok& k = tk[t];
-        vt[t] = (u32)t;
-        vv[t] = k.file;
-        vkd[t] = (u16)(((u32)k.kind << 8) | k.id);
-      }, st);
+      u32* vt = P.vtok;
+      par_for(T, [=] EXS_HD (i64 t) { vt[t] = (u32)t; }, st);
     }
     sync(st);
     dfree(fvc); dfree(fvb); dfree(split);
   } else {
+    dfree(tview);
+    dfree(tkid);
     prof_mark(st);
     excl_scan_u32(fvc, fvb, F + 1, sc, st);
     P.V = get1(fvb + F, st);
@@ -213,13 +217,15 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   {
     i64* el = dalloc<i64>(VT + 1);
     i64* inc = dalloc<i64>(VT + 1);
-    const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vv = P.vview; const u32* vb = P.vbase;
+    const u32* vv = P.vview; const u32* vb = P.vbase;
+    const u16* vk = P.vkid;  // 2-byte kind/id per view position (not the 32-byte token)
     par_for(VT, [=] EXS_HD (i64 i) {
-      const Tok& t = tk[vt[i]];
+      const u16 t = vk[i];
       i64 d = 0;
-      if (t.kind == TK_PUNCT) {
-        if (t.id == P_LPAREN || t.id == P_LBRACE) d = 1;
-        else if (t.id == P_RPAREN || t.id == P_RBRACE) d = -1;
+      if ((t >> 8) == TK_PUNCT) {
+        const u8 id = (u8)t;
+        if (id == P_LPAREN || id == P_LBRACE) d = 1;
+        else if (id == P_RPAREN || id == P_RBRACE) d = -1;
       }
       bool head = vb[vv[i]] == (u32)i;
       el[i] = (d & 0xFFFFFFFFll) | (head ? (1ll << 40) : 0);
@@ -229,13 +235,13 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     prof_mark(st);
     u8* endf = (u8*)el;  // reuse as end flags (VT bytes)
     par_for(VT, [=] EXS_HD (i64 i) {
-      const Tok& t = tk[vt[i]];
+      const u16 t = vk[i];
       int dep = (int)(u32)(inc[i] & 0xFFFFFFFFll);
       bool e = false;
-      if (dep == 0 && t.kind == TK_PUNCT) {
-        if (t.id == P_SEMI) e = true;
-        else if (t.id == P_RBRACE) {
-          bool semi_next = (u32)i + 1 < vb[vv[i] + 1] && tk[vt[i + 1]].kind == TK_PUNCT && tk[vt[i + 1]].id == P_SEMI;
+      if (dep == 0 && (t >> 8) == TK_PUNCT) {
+        if ((u8)t == P_SEMI) e = true;
+        else if ((u8)t == P_RBRACE) {
+          bool semi_next = (u32)i + 1 < vb[vv[i] + 1] && vk[i + 1] == (u16)((TK_PUNCT << 8) | P_SEMI);
           e = !semi_next;
         }
       }
@@ -286,7 +292,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   u32* ss = nullptr;                // statement-segment starts
   u32* titem = nullptr;             // item of every view position (kept through step 4b)
   {
-    const Tok* tk = L.toks; const u32* vt = P.vtok; const u32* vb = P.vbase;
+    const u32* vb = P.vbase; const u16* vk = P.vkid;
     const u32* is = P.item_start; const u32* iv = P.item_view; const i64* da = depth_after;
     par_for(I, [=] EXS_HD (i64 j) {
       u32 v = iv[j];
@@ -294,15 +300,14 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       ibody[j] = NONE;
       if (next - is[j] < BIG) return;
       // last token must be the body's '}' returning to depth 0
-      const Tok& last = tk[vt[next - 1]];
-      if (!(last.kind == TK_PUNCT && last.id == P_RBRACE && (u32)(da[next - 1] & 0xFFFFFFFFll) == 0)) return;
+      if (!(vk[next - 1] == (u16)((TK_PUNCT << 8) | P_RBRACE) && (u32)(da[next - 1] & 0xFFFFFFFFll) == 0)) return;
       for (u32 i = is[j]; i < next; i++) {
-        const Tok& t = tk[vt[i]];
+        const u16 t = vk[i];
         int dep_before = i == vb[v] ? 0 : (int)(u32)(da[i - 1] & 0xFFFFFFFFll);
         if (dep_before != 0) continue;
-        if (t.kind == TK_IDENT && (t.id == W_STRUCT || t.id == W_CLASS || t.id == W_ENUM ||
-                                   t.id == W_STATIC_ASSERT)) return;
-        if (t.kind == TK_PUNCT && t.id == P_LBRACE) { ibody[j] = i; return; }
+        const u8 kind = (u8)(t >> 8), id = (u8)t;
+        if (kind == TK_IDENT && (id == W_STRUCT || id == W_CLASS || id == W_ENUM || id == W_STATIC_ASSERT)) return;
+        if (kind == TK_PUNCT && id == P_LBRACE) { ibody[j] = i; return; }
       }
     }, st);
     ss = dalloc<u32>(VT + 1);
@@ -323,15 +328,16 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       u32 next = (lo + 1 < Ic && iv[lo + 1] == v) ? is[lo + 1] : vb[v + 1];
       if (i >= next - 1) return false;  // the closing '}'
       if (i == bo + 1) return true;
-      const Tok& pt = tk[vt[i - 1]];
-      if ((u32)(da[i - 1] & 0xFFFFFFFFll) != 1 || pt.kind != TK_PUNCT) return false;
-      if (pt.id == P_SEMI) return true;
-      if (pt.id == P_RBRACE) {
+      const u16 pt = vk[i - 1];
+      if ((u32)(da[i - 1] & 0xFFFFFFFFll) != 1 || (pt >> 8) != TK_PUNCT) return false;
+      if ((u8)pt == P_SEMI) return true;
+      if ((u8)pt == P_RBRACE) {
         // a block ends a statement unless 'else' or an operator follows (a
         // brace-initialised temporary: D{}.call(), D{} == x, f(D{}, ...))
-        const Tok& t = tk[vt[i]];
-        if (t.kind == TK_IDENT) return t.id != W_ELSE;
-        if (t.kind == TK_PUNCT) return t.id == P_LBRACE || t.id == P_RBRACE || t.id == P_LPAREN || t.id == P_BANG;
+        const u16 t = vk[i];
+        const u8 kind = (u8)(t >> 8), id = (u8)t;
+        if (kind == TK_IDENT) return id != W_ELSE;
+        if (kind == TK_PUNCT) return id == P_LBRACE || id == P_RBRACE || id == P_LPAREN || id == P_BANG;
         return true;
       }
       return false;
@@ -363,8 +369,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
         u32 len = (ib[j] != NONE ? ib[j] + 1 : next) - is[j];  // tokens this thread parses
         u32 lb = 0;
         while ((1u << lb) < len && lb < 31) lb++;
-        const Tok& t = tk[vt[is[j]]];
-        key[j] = ((u64)lb << 16) | ((u64)t.kind << 8) | t.id;
+        key[j] = ((u64)lb << 16) | vk[is[j]];
         iperm[j] = (u32)j;
       }, st);
       prof_mark(st);
@@ -424,8 +429,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     {
       u64* key = dalloc<u64>(NSS + 1);
       par_for(NSS, [=] EXS_HD (i64 k) {
-        const Tok& t = tk[vt[ssc[k]]];
-        key[k] = ((u64)t.kind << 8) | t.id;
+        key[k] = vk[ssc[k]];
         sperm[k] = (u32)k;
       }, st);
       sort_pairs(key, sperm, NSS, sc, st, 16);

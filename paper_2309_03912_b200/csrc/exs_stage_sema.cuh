@@ -261,6 +261,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
         FnRec& r = fr[f];
         r.node = node; r.view = v; r.rec = rec; r.order = f;
         r.name = nd[node].hv; r.sig = 0; r.sig_rep = f; r.ncalls = 0;
+        r.nstmts = (nd[node].n & FF_BODY) ? (u32)(nd[node + 1].hv & 0xFFFFFFFFu) : 0;  // counted by the parser
         r.flags = rec == NONE ? 0 : FR_MEMBER;
         nd[node + 1].tok = f;  // FNX.tok -> decl record
         f++;
@@ -347,10 +348,17 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       map_insert_min(ka, va, mask, vkey(r.view, r.sig), (u32)i);
     }, st);
     Map ma{ka, va, mask};
+    const u8* cfgs = L.cfg;
     par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
       u32 rep = ma.find(vkey(r.view, r.sig));
       r.sig_rep = rep == NONE ? (u32)i : rep;
+      if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) { r.nstmts = 0; return; }  // not in the struct any more
+      const Node& n = nd[r.node];
+      if ((n.n & (FF_HPRED | FF_DPRED)) && (cfgs[vf[r.view]] & CFG_MODE_MASK) != MODE_P1) {
+        const Tok& t = tk[n.tok];
+        emit_diag(B, mkdiag(vf[r.view], t.line, t.col, C_E0001, M_S_COND_SPEC_MODE));
+      }
     }, st);
   }
   // 5. overload sets of free functions, in item order
@@ -404,20 +412,9 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
     FnRec* fr = S.fns;
     // bodies are scanned statement-parallel (BodyScan carries no state across
     // top-level statements): count, tabulate, scan each statement once
-    EXS_TAG("sema_body_count");
-    par_for(NF, [=] EXS_HD (i64 i) {
-      FnRec& r = fr[i];
-      r.nstmts = 0; r.ncalls = 0;
-      if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) return;  // not in the struct any more
-      u8 c = cfgs[vf[r.view]];
-      u8 mode = c & CFG_MODE_MASK;
-      const Node& n = nd[r.node];
-      if (mode != MODE_P1 && (n.n & (FF_HPRED | FF_DPRED))) {
-        const Tok& t = tk[n.tok];
-        emit_diag(B, mkdiag(vf[r.view], t.line, t.col, C_E0001, M_S_COND_SPEC_MODE));
-      }
-      r.nstmts = (n.n & FF_BODY) ? (u32)(nd[r.node + 1].hv & 0xFFFFFFFFu) : 0;  // counted by the parser
-    }, st);
+    // statement counts: set with the decl records (the parser counted them);
+    // removed members were zeroed and conditional specifiers outside proposal1
+    // reported with the signature representatives (step 4)
     // per-statement tables: statements of a body are walked in parallel (K6)
     u32* ns = dalloc<u32>(NF + 1);
     u32* sb = dalloc<u32>(NF + 1);

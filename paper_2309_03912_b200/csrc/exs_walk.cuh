@@ -139,8 +139,7 @@ EXS_HD inline u32 inst_lookup_or_insert(const WalkBufs& B, const IKey& k, bool& 
   u32 h = (u32)mix64(k.a ^ mix64(k.b)) & B.mask;
   inserted = false;
   // the table holds 2x the id capacity, so probing stays short even past an
-  // overflow; the flag word sits on its own cache line
-  if (ld_volatile(B.overflow) & 1u) return NONE;
+  // overflow (then every insert fails to get an id and the walk is re-run)
   for (u32 probes = 0; probes <= B.mask; probes++) {
     IKey old;
     if (ikey_cas(&B.slots[h], k, old)) {

@@ -166,6 +166,18 @@ struct ByteCursor {
   }
 };
 
+// bit k (k < 4) set where byte k of x equals c
+EXS_HD inline u32 byte_eq_mask(u32 x, u8 c) {
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  const u32 e = __vcmpeq4(x, 0x01010101u * c);  // 0xFF per equal byte
+  return (e & 1u) | ((e >> 7) & 2u) | ((e >> 14) & 4u) | ((e >> 21) & 8u);
+#else
+  u32 o = 0;
+  for (u32 k = 0; k < 4; k++) o |= (((x >> (8 * k)) & 0xFFu) == c ? 1u : 0u) << k;
+  return o;
+#endif
+}
+
 EXS_HD inline void load_word(const LexW& X, u32 base, u32 r[8]) {
 #if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
   if (X.vec && base + 32 <= X.n) {

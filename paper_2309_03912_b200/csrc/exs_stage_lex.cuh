@@ -89,12 +89,32 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
     u32* sp = S.splice;
     const u8* s = S.src;
     EXS_TAG("lex_splice");
+    LexW Xs{};
+    Xs.src = S.src; Xs.n = N; Xs.vec = (((uintptr_t)S.src) & 15) == 0;
     par_for(W, [=] EXS_HD (i64 w) {
-      u32 bits = 0;
-      u32 base = (u32)w * 32;
-      for (u32 j = 0; j < 32 && base + j < N; j++) {
-        u8 c = s[base + j];
-        if ((c == '\\' || c == '\n') && compute_spliced(v, base + j)) bits |= 1u << j;
+      const u32 base = (u32)w * 32;
+      if (base >= N) { sp[w] = 0; return; }
+      u32 r[8];
+      load_word(Xs, base, r);
+      // candidates: backslashes and newlines of the word (byte-parallel compares)
+      u32 bsm = 0, nlm = 0;
+      const u32 m = N - base < 32 ? N - base : 32;
+#pragma unroll
+      for (u32 k = 0; k < 8; k++) {
+        bsm |= byte_eq_mask(r[k], '\\') << (4 * k);
+        nlm |= byte_eq_mask(r[k], '\n') << (4 * k);
+      }
+      const u32 valid = m == 32 ? ~0u : ((1u << m) - 1);
+      bsm &= valid; nlm &= valid;
+      // a newline is spliced only after a backslash (possibly through a run of
+      // newlines): none in the word and none carried in from the byte before
+      const u8 prev = base ? s[base - 1] : 0;
+      if (!bsm && prev != '\\' && prev != '\n') { sp[w] = 0; return; }
+      u32 bits = 0, cand = bsm | nlm;
+      while (cand) {
+        const u32 j = ffs32(cand);
+        cand &= cand - 1;
+        if (compute_spliced(v, base + j)) bits |= 1u << j;
       }
       sp[w] = bits;
     }, st);

@@ -540,7 +540,11 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         walker_for(w, Cc, B, fl[j], (u64)j);
         const FnRec& r = fr[w.fn];
         u32 k0 = c * KCH, k1 = k0 + KCH < r.nstmts ? k0 + KCH : r.nstmts;
+#ifdef EXS_EXP_NOWALK  // timing experiment only: walker set-up without the statements
+        if (w.ecnt == 12345) w.run_chunk(sn, scs, r.stmt_base, k0, k1);
+#else
         w.run_chunk(sn, scs, r.stmt_base, k0, k1);
+#endif
         if (w.ecnt) at_add(&B.inst[fl[j]].ecnt, w.ecnt);
         if (w.contract) at_or(&ct[w.file], 1);
       }, st);

@@ -528,7 +528,7 @@ struct Walker {
     const Node& n = N(s);
     if (n.kind == N_SEXPR || (n.kind == N_SRET && n.c0 != NONE)) {
       if (++wdepth > MAX_WALK_DEPTH) { contract = true; wdepth--; return; }
-      expr_(n.c0);
+      expr_<1>(n.c0);
       wdepth--;
     } else if (n.kind != N_SRET) {
       stmt(s);
@@ -537,11 +537,14 @@ struct Walker {
 
   EXS_HD Val expr(u32 e) {
     if (++wdepth > MAX_WALK_DEPTH) { contract = true; wdepth--; return vnone(); }
-    Val r = expr_(e);
+    Val r = expr_<0>(e);
     wdepth--;
     return r;
   }
 
+  // TOP = 1: the copy inlined into a work item's top-level statement (not
+  // recursive itself: sub-expressions go through expr); TOP = 0: expr's body
+  template <int TOP>
   EXS_HD EXS_FI Val expr_(u32 e) {
     const Node& n = N(e);
     switch (n.kind) {

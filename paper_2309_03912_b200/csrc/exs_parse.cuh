@@ -537,7 +537,7 @@ struct Parser {
       take();
       u32 ex = NONE;
       if (!at_p(P_SEMI)) {
-        ex = expr();
+        ex = expr_t<1>();
         if (ex == NONE) return NONE;
       }
       if (!need_p(P_SEMI, EX_SEMI)) return NONE;
@@ -584,7 +584,7 @@ struct Parser {
       if (matched) return s;
     }
     (void)tpos;
-    u32 ex = expr();
+    u32 ex = expr_t<1>();
     if (ex == NONE) return NONE;
     if (!need_p(P_SEMI, EX_SEMI)) return NONE;
     u32 id = mk(N_SEXPR, t);
@@ -668,12 +668,17 @@ struct Parser {
   }
 
   // ------------------------------------------------------------ expressions
-  EXS_HD u32 expr() {
+  // expression grammar; TOP = 1 is the copy inlined into stmt() (its own
+  // recursion goes through the out-of-line expr()/unary(), TOP = 0)
+  EXS_HD u32 expr() { return expr_t<0>(); }
+  EXS_HD u32 unary() { return unary_t<0>(); }
+  template <int TOP>
+  EXS_HD EXS_FI u32 expr_t() {
     if (!enter()) return NONE;
-    u32 lhs = conj();
+    u32 lhs = conj<TOP>();
     while (lhs != NONE && at_p(P_OR)) {
       u32 op = take();
-      u32 rhs = conj();
+      u32 rhs = conj<TOP>();
       if (rhs == NONE) return NONE;
       u32 id = mk(N_BIN, op);
       if (id == NONE) return NONE;
@@ -683,11 +688,12 @@ struct Parser {
     depth--;
     return lhs;
   }
+  template <int TOP>
   EXS_HD EXS_FI u32 conj() {
-    u32 lhs = cmp();
+    u32 lhs = cmp<TOP>();
     while (lhs != NONE && at_p(P_AND)) {
       u32 op = take();
-      u32 rhs = cmp();
+      u32 rhs = cmp<TOP>();
       if (rhs == NONE) return NONE;
       u32 id = mk(N_BIN, op);
       if (id == NONE) return NONE;
@@ -696,13 +702,14 @@ struct Parser {
     }
     return lhs;
   }
+  template <int TOP>
   EXS_HD EXS_FI u32 cmp() {
-    u32 lhs = unary();
+    u32 lhs = unary_t<TOP>();
     if (lhs == NONE) return NONE;
     if (at_p(P_EQ) || at_p(P_NE)) {
       u8 o = tid();
       u32 op = take();
-      u32 rhs = unary();
+      u32 rhs = unary_t<TOP>();
       if (rhs == NONE) return NONE;
       u32 id = mk(N_BIN, op);
       if (id == NONE) return NONE;
@@ -711,7 +718,8 @@ struct Parser {
     }
     return lhs;
   }
-  EXS_HD u32 unary() {
+  template <int TOP>
+  EXS_HD EXS_FI u32 unary_t() {
     if (at_p(P_BANG)) {
       if (!enter()) return NONE;
       u32 op = take();

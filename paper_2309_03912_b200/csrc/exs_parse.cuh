@@ -530,7 +530,11 @@ struct Parser {
     return true;
   }
 
-  EXS_HD u32 stmt() {
+  // TOP = 1: the copy inlined into the statement-parallel kernel (run_parse
+  // step 4b); nested statements go through the out-of-line stmt()
+  EXS_HD u32 stmt() { return stmt_t<0>(); }
+  template <int TOP>
+  EXS_HD EXS_FI u32 stmt_t() {
     u32 tpos = pos;
     u32 t = gtok(pos);
     if (at_w(W_RETURN)) {

@@ -453,7 +453,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       p.init(pv, nd, (u32)(2ull * i0 + 4ull * j), 2 * (stop - i0), i0 - vb[v]);
       p.v_src = s; p.v_splice = sp;
       p.depth = 1;  // inside the body's block (parser depth limit)
-      u32 r = p.stmt();
+      u32 r = p.stmt_t<1>();
       sroot[k] = r;
       u8 stt = p.failed ? (p.overflow ? 2 : 1) : 0;
       if (!stt && vb[v] + p.pos != stop) stt = 3;  // statements do not chain: sequential repair

@@ -423,23 +423,17 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     u32 nnew = n_now - prev_n;
     if (!nnew) break;
     prof_mark(st);
-    // frontier: new instances with bodies, ordered by creation key.  A body
-    // with no statements and no parameters has nothing to walk (no calls, no
-    // parameter types to resolve): it is left out.  Creation keys only order
-    // the creators among themselves, so dropping non-creators keeps them.
+    // frontier: new instances with a body to walk (IF_BODY: an empty,
+    // parameterless body is left out -- creation keys only order the creators
+    // among themselves, so dropping non-creators keeps them), by creation key
     grow(front, front_cap, nnew + 1, 0, st);
     u32 nf;
     {
       const Inst* in = W.inst;
-      const FnRec* fns = S.fns; const Node* nd = P.nodes;
       u32 base = prev_n;
       u32* fr_tmp = dalloc<u32>(nnew + 1);
-      nf = select_idx(nnew, [=] EXS_HD (u32 j) -> bool {
-        const Inst& I = in[base + j];
-        if (!(I.flags & IF_BODY)) return false;
-        const FnRec& r = fns[I.fn];
-        return r.nstmts != 0 || nd[r.node].c1 != NONE;
-      }, fr_tmp, L.cnt, sc, st);
+      nf = select_idx(nnew, [=] EXS_HD (u32 j) -> bool { return (in[base + j].flags & IF_BODY) != 0; },
+                      fr_tmp, L.cnt, sc, st);
       u64* keys = dalloc<u64>(nf + 1);
       par_for(nf, [=] EXS_HD (i64 j) { fr_tmp[j] += base; keys[j] = in[fr_tmp[j]].ckey; }, st);
       sort_pairs(keys, fr_tmp, nf, sc, st);

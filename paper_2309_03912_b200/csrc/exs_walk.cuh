@@ -184,7 +184,9 @@ EXS_HD inline void fill_instance(Inst& I, const Tables* T, const IKey& k, u32 fi
   I.ebase = 0; I.ecnt = 0;
   I.tb = tb; I.hb = hb; I.ot = ot;
   I.side = side; I.spaces = sp; I.level = clevel; I.slot = slot;
-  I.flags = (fnn.n & FF_BODY) ? IF_BODY : 0;
+  // IF_BODY: a body to walk -- statements or parameter types to resolve (an
+  // empty, parameterless body creates nothing and reports nothing)
+  I.flags = ((fnn.n & FF_BODY) && (fr.nstmts || fnn.c1 != NONE)) ? IF_BODY : 0;
   if (T->toks[fnn.tok].id == W_MAIN && !(fr.flags & FR_OWNER)) I.flags |= IF_MAIN;
 }
 // key insertion without an id (the level-0 roots allocate ids by a scan

@@ -22,9 +22,7 @@ struct WalkState {
   u32 cap_inst = 0, n_inst = 0, levels = 0;
   u32 buf_scale = 1;  // multiplier of the creation-log estimate (grows on overflow)
   u64 n_edges = 0, edge_cap = 0, callsites = 0;
-  IKey* slots = nullptr;
-  u32* sid = nullptr;
-  unsigned long long* sck = nullptr;
+  Slot* slots = nullptr;
   u32 mask = 0;
   Inst* inst = nullptr;
   u32* edges = nullptr;
@@ -49,9 +47,9 @@ struct WalkState {
     return out;
   }
   void free_all() {
-    void* ps[] = {slots, sid, sck, inst, edges, pend, seeds, log, main_inst, main_key, counters, visited};
+    void* ps[] = {slots, inst, edges, pend, seeds, log, main_inst, main_key, counters, visited};
     for (void* p : ps) dfree(p);
-    slots = nullptr; sid = nullptr; sck = nullptr; inst = nullptr; edges = nullptr; pend = nullptr; seeds = nullptr;
+    slots = nullptr; inst = nullptr; edges = nullptr; pend = nullptr; seeds = nullptr;
     log = nullptr; main_inst = nullptr; main_key = nullptr; counters = nullptr; visited = nullptr;
   }
 };
@@ -113,7 +111,7 @@ EXS_HD inline void walker_for(Walker& w, const WalkCfg& C, const WalkBufs& B, u3
 inline WalkBufs make_bufs(WalkState& W, u32* n_diags, Diag* diags, u32 cap_diags, u64* dset,
                           u32 dmask, u32* contract) {
   WalkBufs B;
-  B.slots = W.slots; B.sid = W.sid; B.sck = W.sck; B.mask = W.mask; B.inst = W.inst;
+  B.slots = W.slots; B.mask = W.mask; B.inst = W.inst;
   B.n_inst = W.ctr(CNT_INST); B.cap_inst = W.cap_inst; B.lvl_base = 0;
   B.edges = W.edges;
   B.pend = W.pend; B.n_pend = W.ctr(CNT_PEND); B.cap_pend = W.cap_pend;
@@ -143,30 +141,36 @@ void grow(T*& p, u64& cap_or_dummy, u64 need, u64 used, cudaStream_t st) {
 // creates at most two instances per call site (spacecheck.py:591-596) and
 // usually at most one; growing before each level replaces the overflow-and-
 // rerun of the whole walk.
+// an empty instance hash table (mask + 1 slots)
+inline Slot* alloc_slots(u32 mask, cudaStream_t st) {
+  Slot* sl = dalloc<Slot>((u64)mask + 1);
+  par_for((i64)mask + 1, [=] EXS_HD (i64 h) {
+    Slot e;
+    e.k.a = 0; e.k.b = 0; e.sid = NONE; e.pad = 0; e.sck = ~0ull;
+    sl[h] = e;
+  }, st);
+  return sl;
+}
+
 inline void grow_inst(WalkState& W, u64 need, u32 n, cudaStream_t st) {
   if (need <= W.cap_inst) return;
   const u32 cap = (u32)std::min<u64>(std::max<u64>(need + need / 2, 2ull * W.cap_inst), 0x7FFFFFFFull);
   Inst* in = dalloc<Inst>(cap);
   if (n) d2d(in, W.inst, sizeof(Inst) * (u64)n, st);
   const u32 mask = (u32)(pow2_at_least(2ull * cap) - 1);
-  IKey* slots = dalloc<IKey>((u64)mask + 1);
-  u32* sid = dalloc<u32>((u64)mask + 1);
-  unsigned long long* sck = dalloc<unsigned long long>((u64)mask + 1);
-  dzero(slots, sizeof(IKey) * ((u64)mask + 1), st);
-  dfill_ff(sid, 4ull * ((u64)mask + 1), st);
-  dfill_ff(sck, 8ull * ((u64)mask + 1), st);
+  Slot* slots = alloc_slots(mask, st);
   par_for(n, [=] EXS_HD (i64 i) {
     Inst& I = in[i];
     IKey k; k.a = I.ka; k.b = I.kb;
     u32 h = (u32)mix64(k.a ^ mix64(k.b)) & mask;
     IKey old;
-    while (!ikey_cas(&slots[h], k, old)) h = (h + 1) & mask;
-    sid[h] = (u32)i;
+    while (!ikey_cas(&slots[h].k, k, old)) h = (h + 1) & mask;
+    slots[h].sid = (u32)i;
     I.slot = h;
   }, st);
   sync(st);
-  dfree(W.inst); dfree(W.slots); dfree(W.sid); dfree(W.sck);
-  W.inst = in; W.slots = slots; W.sid = sid; W.sck = sck;
+  dfree(W.inst); dfree(W.slots);
+  W.inst = in; W.slots = slots;
   W.cap_inst = cap; W.mask = mask;
 }
 
@@ -180,12 +184,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   WalkCfg C{dtab, S.fns, S.recs, P.nodes, L.toks, P.vfile, L.cfg, L.fp};
   // buffers
   W.mask = pow2_at_least(2ull * W.cap_inst) - 1;
-  W.slots = dalloc<IKey>((u64)W.mask + 1);
-  W.sid = dalloc<u32>((u64)W.mask + 1);
-  W.sck = dalloc<unsigned long long>((u64)W.mask + 1);
-  dzero(W.slots, sizeof(IKey) * ((u64)W.mask + 1), st);
-  dfill_ff(W.sid, 4ull * ((u64)W.mask + 1), st);
-  dfill_ff(W.sck, 8ull * ((u64)W.mask + 1), st);
+  W.slots = alloc_slots(W.mask, st);
   W.inst = dalloc<Inst>(W.cap_inst);
   W.counters = dalloc<u32>(CNT_N * CNT_STRIDE);
   dzero(W.counters, 4ull * CNT_N * CNT_STRIDE, st);
@@ -300,7 +299,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
           const u32 slot = slot_insert(B, key, inserted);
           if (slot == NONE) return;
           if (inserted) rs[2 * kk + sd] = slot;
-          const unsigned long long old = at_min64(&B.sck[slot], ck);
+          const unsigned long long old = at_min64(&B.slots[slot].sck, ck);
           if (inserted || old < ck) continue;
           const u32 li = at_inc_agg(B.n_log);
           if (li < B.cap_log) {
@@ -334,7 +333,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         const IKey key = make_ikey(r.sig_rep, vnone(), vnone(), q.ot, q.walk, sd);
         fill_instance(B.inst[id], tab, key, q.i, vnone(), vnone(), sd, r.rec, q.ot, fn.tok, q.walk,
                       static_spaces(fn.n, q.free_main, q.sf, q.mode, sd), 0, slot);
-        B.sid[slot] = id;
+        B.slots[slot].sid = id;
       }, st);
       u32* ni = B.n_inst;
       par_for(1, [=] EXS_HD (i64) { *ni = total; }, st);
@@ -342,8 +341,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       const u32 nlog1 = get1(B.n_log, st);
       const u32 lo = nlog0, hi = nlog1 < B.cap_log ? nlog1 : B.cap_log;
       if (hi > lo) {
-        CreateLog* lg = B.log; const u32* sid = B.sid;
-        par_for(hi - lo, [=] EXS_HD (i64 j) { lg[lo + j].inst = sid[lg[lo + j].inst]; }, st);
+        CreateLog* lg = B.log; const Slot* sl = B.slots;
+        par_for(hi - lo, [=] EXS_HD (i64 j) { lg[lo + j].inst = sl[lg[lo + j].inst].sid; }, st);
       }
       sync(st);
       dfree(ins);
@@ -408,8 +407,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     // creation keys of this level's instances (min over creators), then the
     // first creator's location (spacecheck.py:331-337)
     {
-      Inst* in = W.inst; const unsigned long long* sk = W.sck; const u32 base = prev_n;
-      par_for(n_now - prev_n, [=] EXS_HD (i64 j) { Inst& I = in[base + j]; I.ckey = sk[I.slot]; }, st);
+      Inst* in = W.inst; const Slot* sl = W.slots; const u32 base = prev_n;
+      par_for(n_now - prev_n, [=] EXS_HD (i64 j) { Inst& I = in[base + j]; I.ckey = sl[I.slot].sck; }, st);
     }
     {
       const CreateLog* lg = W.log; Inst* in = W.inst;

@@ -15,6 +15,15 @@ struct alignas(16) IKey {
   u64 a, b;
 };
 
+// one slot of the instance hash table: key (128-bit CAS), published id and
+// the creation-key minimum of the current level share one 32-byte sector, so
+// a creator's probe, id read and atomicMin touch one line
+struct alignas(32) Slot {
+  IKey k;
+  u32 sid, pad;
+  unsigned long long sck;
+};
+
 struct Inst {
   u64 ka, kb;
   unsigned long long ckey;  // min creation key (level<<52 | parent rank<<24 | local)
@@ -37,9 +46,7 @@ struct CreateLog {
 
 struct WalkBufs {
   // instance table
-  IKey* slots;
-  u32* sid;
-  unsigned long long* sck;  // per slot: min creation key of the current level (atomicMin)
+  Slot* slots;              // key, published id, min creation key of the current level
   u32 mask;
   Inst* inst;
   u32* n_inst;
@@ -142,7 +149,7 @@ EXS_HD inline u32 inst_lookup_or_insert(const WalkBufs& B, const IKey& k, bool& 
   // overflow (then every insert fails to get an id and the walk is re-run)
   for (u32 probes = 0; probes <= B.mask; probes++) {
     IKey old;
-    if (ikey_cas(&B.slots[h], k, old)) {
+    if (ikey_cas(&B.slots[h].k, k, old)) {
       u32 id = at_inc_agg(B.n_inst);
       if (id >= B.cap_inst) { at_or(B.overflow, 1u); id = NONE; }
       inserted = true;
@@ -151,7 +158,7 @@ EXS_HD inline u32 inst_lookup_or_insert(const WalkBufs& B, const IKey& k, bool& 
     }
     if (old.a == k.a && old.b == k.b) {
       u32 id;
-      while ((id = ld_volatile(&B.sid[h])) == NONE) {
+      while ((id = ld_volatile(&B.slots[h].sid)) == NONE) {
         if (ld_volatile(B.overflow) & 1u) return NONE;
       }
       slot = h;
@@ -163,7 +170,7 @@ EXS_HD inline u32 inst_lookup_or_insert(const WalkBufs& B, const IKey& k, bool& 
   return NONE;
 }
 EXS_HD inline void inst_publish(const WalkBufs& B, u32 slot, u32 id) {
-  *(volatile u32*)&B.sid[slot] = id;
+  *(volatile u32*)&B.slots[slot].sid = id;
 }
 
 // instance key and record (spacecheck.py:325-341)
@@ -196,7 +203,7 @@ EXS_HD inline u32 slot_insert(const WalkBufs& B, const IKey& k, bool& inserted) 
   inserted = false;
   for (u32 probes = 0; probes <= B.mask; probes++) {
     IKey old;
-    if (ikey_cas(&B.slots[h], k, old)) { inserted = true; return h; }
+    if (ikey_cas(&B.slots[h].k, k, old)) { inserted = true; return h; }
     if (old.a == k.a && old.b == k.b) return h;
     h = (h + 1) & B.mask;
   }
@@ -228,7 +235,7 @@ EXS_HD EXS_FI u32 create_instance(const WalkBufs& B, const Tables* T, u32 fi, co
     // record already holds its data).  The post-level fixup applies the log
     // entry whose key equals the final minimum; none matches when the
     // inserter holds it.
-    const unsigned long long old = at_min64(&B.sck[slot], ck);
+    const unsigned long long old = at_min64(&B.slots[slot].sck, ck);
     if (inserted || old < ck) return id;
     u32 li = at_inc_agg(B.n_log);
     if (li < B.cap_log) {

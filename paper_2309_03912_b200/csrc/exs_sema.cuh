@@ -52,18 +52,22 @@ struct RecRec {
   u64 name;
 };
 
-// open-addressing u64 -> u32 map (keys never 0)
+// open-addressing u64 -> u32 map (keys never 0); key and value share one
+// 16-byte entry, so a probe touches one line
+struct alignas(16) MapEnt {
+  u64 k;
+  u32 v, pad;
+};
 struct Map {
-  u64* keys;
-  u32* vals;
+  MapEnt* e;
   u32 mask;
   EXS_HD u32 find(u64 k) const {
-    if (!keys) return NONE;
+    if (!e) return NONE;
     u32 h = (u32)mix64(k) & mask;
     while (true) {
-      u64 kk = keys[h];
-      if (kk == k) return vals[h];
-      if (kk == 0) return NONE;
+      const MapEnt x = e[h];
+      if (x.k == k) return x.v;
+      if (x.k == 0) return NONE;
       h = (h + 1) & mask;
     }
   }
@@ -71,11 +75,11 @@ struct Map {
 EXS_HD inline u64 nz(u64 k) { return k ? k : 0x9E3779B97F4A7C15ull; }
 EXS_HD inline u64 vkey(u32 view, u64 h) { return nz(hcombine((u64)view + 0x51ED27ull, h)); }
 
-EXS_HD inline void map_insert_min(u64* keys, u32* vals, u32 mask, u64 k, u32 v) {
+EXS_HD inline void map_insert_min(MapEnt* e, u32 mask, u64 k, u32 v) {
   u32 h = (u32)mix64(k) & mask;
   while (true) {
-    unsigned long long prev = at_cas64((unsigned long long*)&keys[h], 0ull, (unsigned long long)k);
-    if (prev == 0ull || prev == k) { at_min(&vals[h], v); return; }
+    unsigned long long prev = at_cas64((unsigned long long*)&e[h].k, 0ull, (unsigned long long)k);
+    if (prev == 0ull || prev == k) { at_min(&e[h].v, v); return; }
     h = (h + 1) & mask;
   }
 }

@@ -13,23 +13,30 @@ struct SemaState {
   RecRec* recs = nullptr;
   u32* item_fn = nullptr;   // FI+1 exclusive scan of fn counts per item
   u32* item_rec = nullptr;
-  u64* smap_k = nullptr; u32* smap_v = nullptr; u32 smap_mask = 0;
-  u64* fmap_k = nullptr; u32* fmap_v = nullptr; u32 fmap_mask = 0;
-  u64* sig_k = nullptr; u32* sig_v = nullptr; u32 sig_mask = 0;    // resolve duplicates
-  u64* siga_k = nullptr; u32* siga_v = nullptr; u32 siga_mask = 0; // walk-visible sig reps
+  MapEnt* smap = nullptr; u32 smap_mask = 0;
+  MapEnt* fmap = nullptr; u32 fmap_mask = 0;
+  MapEnt* sigm = nullptr; u32 sig_mask = 0;    // resolve duplicates
+  MapEnt* sigam = nullptr; u32 siga_mask = 0;  // walk-visible sig reps
   u32* fcand = nullptr, *fcand_cnt = nullptr;
   u32 NS = 0;                                  // top-level statements of all bodies
   u64 NCS = 0;                                 // call sites of all bodies
   u32* stmt_node = nullptr, *stmt_cs = nullptr;  // per statement: node, call sites before it
   Tables tab;
   void free_all() {
-    void* ps[] = {fns, recs, item_fn, item_rec, smap_k, smap_v, fmap_k, fmap_v, sig_k, sig_v,
-                  siga_k, siga_v, fcand, fcand_cnt, stmt_node, stmt_cs};
+    void* ps[] = {fns, recs, item_fn, item_rec, smap, fmap, sigm, sigam, fcand, fcand_cnt, stmt_node,
+                  stmt_cs};
     for (void* p : ps) dfree(p);
   }
 };
 
 // ---------------------------------------------------------------------------
+// an empty map of mask + 1 entries (keys 0, values NONE)
+inline MapEnt* alloc_map(u32 mask, cudaStream_t st) {
+  MapEnt* e = dalloc<MapEnt>((u64)mask + 1);
+  par_for((i64)mask + 1, [=] EXS_HD (i64 h) { MapEnt x; x.k = 0; x.v = NONE; x.pad = 0; e[h] = x; }, st);
+  return e;
+}
+
 // canonical printer as a hash stream (nodes.py:336-383)
 
 struct HashPrinter {
@@ -278,14 +285,11 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
   }
   // 2. struct table: first definition wins (sema.py:176-184)
   S.smap_mask = pow2_at_least(2ull * NR + 2) - 1;
-  S.smap_k = dalloc<u64>(S.smap_mask + 1);
-  S.smap_v = dalloc<u32>(S.smap_mask + 1);
-  dzero(S.smap_k, 8ull * (S.smap_mask + 1), st);
-  dfill_ff(S.smap_v, 4ull * (S.smap_mask + 1), st);
+  S.smap = alloc_map(S.smap_mask, st);
   {
-    u64* k = S.smap_k; u32* vv = S.smap_v; u32 mask = S.smap_mask; RecRec* rr = S.recs;
-    par_for(NR, [=] EXS_D (i64 r) { map_insert_min(k, vv, mask, vkey(rr[r].view, rr[r].name), (u32)r); }, st);
-    Map m{k, vv, mask};
+    MapEnt* me = S.smap; u32 mask = S.smap_mask; RecRec* rr = S.recs;
+    par_for(NR, [=] EXS_D (i64 r) { map_insert_min(me, mask, vkey(rr[r].view, rr[r].name), (u32)r); }, st);
+    Map m{me, mask};
     const Node* nd = P.nodes; const Tok* tk = L.toks; const u32* vf = P.vfile; WalkBufs B = WB;
     par_for(NR, [=] EXS_HD (i64 r) {
       RecRec& q = rr[r];
@@ -311,24 +315,18 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
   }
   // 4. duplicates among free functions and members of kept structs (sema.py:161-195)
   S.sig_mask = pow2_at_least(2ull * NF + 2) - 1;
-  S.sig_k = dalloc<u64>(S.sig_mask + 1);
-  S.sig_v = dalloc<u32>(S.sig_mask + 1);
+  S.sigm = alloc_map(S.sig_mask, st);
   S.siga_mask = S.sig_mask;
-  S.siga_k = dalloc<u64>(S.sig_mask + 1);
-  S.siga_v = dalloc<u32>(S.sig_mask + 1);
-  dzero(S.sig_k, 8ull * (S.sig_mask + 1), st);
-  dfill_ff(S.sig_v, 4ull * (S.sig_mask + 1), st);
-  dzero(S.siga_k, 8ull * (S.sig_mask + 1), st);
-  dfill_ff(S.siga_v, 4ull * (S.sig_mask + 1), st);
+  S.sigam = alloc_map(S.sig_mask, st);
   {
     FnRec* fr = S.fns; const RecRec* rr = S.recs;
-    u64* k = S.sig_k; u32* vv = S.sig_v; u32 mask = S.sig_mask;
+    MapEnt* me = S.sigm; u32 mask = S.sig_mask;
     par_for(NF, [=] EXS_D (i64 i) {
       const FnRec& r = fr[i];
       if (r.rec != NONE && rr[r.rec].dup) return;  // members of duplicate structs are never checked
-      map_insert_min(k, vv, mask, vkey(r.view, r.sig), (u32)i);
+      map_insert_min(me, mask, vkey(r.view, r.sig), (u32)i);
     }, st);
-    Map m{k, vv, mask};
+    Map m{me, mask};
     const Node* nd = P.nodes; const Tok* tk = L.toks; const u32* vf = P.vfile; WalkBufs B = WB;
     par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
@@ -341,13 +339,13 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
         emit_diag(B, mkdiag(vf[r.view], t.line, t.col, C_E0102, M_S_DUP, ((u64)t.pos << 32) | (t.end - t.pos), osp));
       }
     }, st);
-    u64* ka = S.siga_k; u32* va = S.siga_v;
+    MapEnt* mea = S.sigam;
     par_for(NF, [=] EXS_D (i64 i) {
       const FnRec& r = fr[i];
       if ((r.flags & FR_DUP) && (r.flags & FR_OWNER)) return;  // removed from the struct
-      map_insert_min(ka, va, mask, vkey(r.view, r.sig), (u32)i);
+      map_insert_min(mea, mask, vkey(r.view, r.sig), (u32)i);
     }, st);
-    Map ma{ka, va, mask};
+    Map ma{mea, mask};
     const u8* cfgs = L.cfg;
     par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
@@ -374,25 +372,22 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
     S.fcand = idx;
     S.fcand_cnt = dalloc<u32>(NC + 1);
     S.fmap_mask = pow2_at_least(2ull * NC + 2) - 1;
-    S.fmap_k = dalloc<u64>(S.fmap_mask + 1);
-    S.fmap_v = dalloc<u32>(S.fmap_mask + 1);
-    dzero(S.fmap_k, 8ull * (S.fmap_mask + 1), st);
-    dfill_ff(S.fmap_v, 4ull * (S.fmap_mask + 1), st);
-    u32* cnt = S.fcand_cnt; u64* fk = S.fmap_k; u32* fv = S.fmap_v; u32 mask = S.fmap_mask;
+    S.fmap = alloc_map(S.fmap_mask, st);
+    u32* cnt = S.fcand_cnt; MapEnt* fme = S.fmap; u32 mask = S.fmap_mask;
     par_for(NC, [=] EXS_D (i64 i) {
       if (i > 0 && keys[i - 1] == keys[i]) return;
       u32 j = (u32)i;
       while (j < NC && keys[j] == keys[i]) j++;
       cnt[i] = j - (u32)i;
-      map_insert_min(fk, fv, mask, keys[i], (u32)i);
+      map_insert_min(fme, mask, keys[i], (u32)i);
     }, st);
     sync(st);
     dfree(keys);
   }
   // tables for the evaluator
   S.tab.nodes = P.nodes; S.tab.toks = L.toks; S.tab.fns = S.fns; S.tab.recs = S.recs;
-  S.tab.smap = Map{S.smap_k, S.smap_v, S.smap_mask};
-  S.tab.fmap = Map{S.fmap_k, S.fmap_v, S.fmap_mask};
+  S.tab.smap = Map{S.smap, S.smap_mask};
+  S.tab.fmap = Map{S.fmap, S.fmap_mask};
   S.tab.fcand = S.fcand; S.tab.fcand_cnt = S.fcand_cnt;
   S.tab.src = L.src; S.tab.splice = L.splice;
   // 6. mode-gated syntax (sema.py:221-248), call sites, undefined names

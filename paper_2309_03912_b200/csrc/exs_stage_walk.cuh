@@ -635,7 +635,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
           if (vis[c]) continue;
           vis[c] = 1;
 #endif
-          u32 k = at_add(&qn[1], 1);
+          u32 k = at_inc_agg(&qn[1]);  // warp-aggregated: one atomic per warp
           qb[k] = c;
         }
       }, st);

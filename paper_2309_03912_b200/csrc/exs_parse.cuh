@@ -628,6 +628,28 @@ struct Parser {
     u32 nm = take();
     u32 targs = NONE;
     if (at_p(P_LT)) {
+      // look ahead to the '>' closing the template arguments (their grammar
+      // has no bare '<' or '>' besides nested lists): unless a launch '<<<' or a
+      // declared name follows, the statement is an expression -- back off now
+      // instead of parsing the list twice
+      u32 q = pos, dep = 0;
+      bool known = false;
+      while (q < v.n) {
+        const u16 kq = v.vkid[v.vbase + q];
+        if ((kq >> 8) == TK_PUNCT) {
+          const u8 pq = (u8)kq;
+          if (pq == P_LT) dep++;
+          else if (pq == P_GT) { if (--dep == 0) { known = true; break; } }
+          else if (pq == P_LLL || pq == P_GGG || pq == P_SEMI || pq == P_LBRACE || pq == P_RBRACE) break;
+        }
+        q++;
+      }
+      if (known) {
+        const u16 kn = q + 1 < v.n ? v.vkid[v.vbase + q + 1] : (u16)(TK_EOF << 8);
+        const bool launch = kn == (u16)((TK_PUNCT << 8) | P_LLL);
+        const bool decl = (kn >> 8) == TK_IDENT && !((u8)kn >= 1 && (u8)kn <= W_LAST_KEYWORD);
+        if (!launch && !decl) { pos = mark; return NONE; }
+      }
       int save_depth = depth;
       bool ok = targ_list(targs);
       if (!ok) {

@@ -323,11 +323,15 @@ inline void sort_pairs(u64* keys, u32* vals, i64 n, Scratch& sc, cudaStream_t s,
 #ifndef EXS_EMU
   u64* k2 = dalloc<u64>(n);
   u32* v2 = dalloc<u32>(n);
+  // double-buffered: the passes ping-pong between the two buffers and the
+  // result is copied back only when it ends in the scratch pair
+  cub::DoubleBuffer<u64> dk(keys, k2);
+  cub::DoubleBuffer<u32> dv(vals, v2);
   size_t tb = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, k2, vals, v2, (int)n, 0, end_bit, s));
-  CK(cub::DeviceRadixSort::SortPairs(sc.get(tb), tb, keys, k2, vals, v2, (int)n, 0, end_bit, s));
-  CK(cudaMemcpyAsync(keys, k2, n * 8, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(vals, v2, n * 4, cudaMemcpyDeviceToDevice, s));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)n, 0, end_bit, s));
+  CK(cub::DeviceRadixSort::SortPairs(sc.get(tb), tb, dk, dv, (int)n, 0, end_bit, s));
+  if (dk.Current() != keys) CK(cudaMemcpyAsync(keys, dk.Current(), n * 8, cudaMemcpyDeviceToDevice, s));
+  if (dv.Current() != vals) CK(cudaMemcpyAsync(vals, dv.Current(), n * 4, cudaMemcpyDeviceToDevice, s));
   sync(s);
   dfree(k2);
   dfree(v2);

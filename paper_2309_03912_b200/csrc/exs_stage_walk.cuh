@@ -435,7 +435,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
                       fr_tmp, L.cnt, sc, st);
       u64* keys = dalloc<u64>(nf + 1);
       par_for(nf, [=] EXS_HD (i64 j) { fr_tmp[j] += base; keys[j] = in[fr_tmp[j]].ckey; }, st);
-      sort_pairs(keys, fr_tmp, nf, sc, st);
+      sort_pairs(keys, fr_tmp, nf, sc, st, 54);  // bits 54+ hold the level: equal in a frontier
       d2d(front, fr_tmp, 4ull * nf, st);
       sync(st);
       dfree(keys);

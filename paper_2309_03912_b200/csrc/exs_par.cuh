@@ -304,6 +304,23 @@ u32 select_idx(i64 n, P pred, u32* out, u32* d_count, Scratch& sc, cudaStream_t 
 #ifndef EXS_EMU
   cub::CountingInputIterator<u32> it(0);
   size_t tb = 0;
+#ifndef EXS_SELECT_FLAGGED_MIN
+#define EXS_SELECT_FLAGGED_MIN (1ll << 22)
+#endif
+  if (n >= EXS_SELECT_FLAGGED_MIN) {
+    // large selections: the predicate runs once in a coalesced pass (one
+    // thread per index, 1-byte flag out) and the compaction reads only the
+    // flags; inside DeviceSelect::If each thread evaluates a run of
+    // consecutive indices, so a predicate that gathers strides its loads
+    u8* fl = dalloc<u8>((size_t)n);
+    par_for(n, [=] EXS_HD (i64 i) { fl[i] = pred((u32)i) ? 1 : 0; }, s, 256, "select_flags", 1);
+    CK(cub::DeviceSelect::Flagged(nullptr, tb, it, fl, out, d_count, (int)n, s));
+    CK(cub::DeviceSelect::Flagged(sc.get(tb), tb, it, fl, out, d_count, (int)n, s));
+    g_launches += 2;
+    const u32 c = get1(d_count, s);
+    dfree(fl);
+    return c;
+  }
   CK(cub::DeviceSelect::If(nullptr, tb, it, out, d_count, (int)n, pred, s));
   CK(cub::DeviceSelect::If(sc.get(tb), tb, it, out, d_count, (int)n, pred, s));
   g_launches += 2;

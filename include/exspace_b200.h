@@ -159,7 +159,10 @@ int exs_get_tokens(exs_handle h, uint32_t file, exs_token* out, uint64_t cap, ui
 int exs_get_walk_stats(exs_handle h, exs_walk_stats* out, uint64_t cap);
 int exs_describe(exs_handle h, const uint32_t* ids, const uint8_t* kinds, uint32_t n,
                  exs_desc* out);
-/* options: 1 = also compute per-walk demand counts (Analysis.walks parity) */
+/* options: 1 = also compute per-walk demand counts (Analysis.walks parity);
+ * 3 = statement-parallel body parsing threshold (tokens, >= 4);
+ * 4 = ordered selections of at least this many indices use a flag pass +
+ *     flagged compaction (default 4M; 0 forces it, for the parity tests) */
 int exs_set_option(exs_handle h, int key, int value);
 /* with EXS_PROFILE=1 in the environment: per-launch-site device times of the last run */
 const char* exs_profile_text(void);

@@ -147,6 +147,12 @@ struct ProfRec { const char* fn; int line; cudaEvent_t a, b; };
 extern bool g_profile;
 extern std::vector<ProfRec> g_prof;
 extern thread_local const char* g_tag;  // name of the next launch (EXS_TAG)
+// select_idx switches to a flag pass + DeviceSelect::Flagged at this many indices
+// (set per run from the handle: exs_set_option key 4)
+#ifndef EXS_SELECT_FLAGGED_MIN
+#define EXS_SELECT_FLAGGED_MIN (1ll << 22)
+#endif
+extern thread_local i64 g_select_flagged_min;
 #define EXS_TAG(name) (::exs::g_tag = (name))
 #endif
 
@@ -304,10 +310,7 @@ u32 select_idx(i64 n, P pred, u32* out, u32* d_count, Scratch& sc, cudaStream_t 
 #ifndef EXS_EMU
   cub::CountingInputIterator<u32> it(0);
   size_t tb = 0;
-#ifndef EXS_SELECT_FLAGGED_MIN
-#define EXS_SELECT_FLAGGED_MIN (1ll << 22)
-#endif
-  if (n >= EXS_SELECT_FLAGGED_MIN) {
+  if (n >= g_select_flagged_min) {
     // large selections: the predicate runs once in a coalesced pass (one
     // thread per index, 1-byte flag out) and the compaction reads only the
     // flags; inside DeviceSelect::If each thread evaluates a run of

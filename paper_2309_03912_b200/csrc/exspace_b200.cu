@@ -19,6 +19,7 @@ thread_local cudaStream_t g_alloc_stream = 0;
 bool g_profile = getenv("EXS_PROFILE") != nullptr;
 std::vector<ProfRec> g_prof;
 thread_local const char* g_tag = nullptr;
+thread_local i64 g_select_flagged_min = EXS_SELECT_FLAGGED_MIN;
 static std::string g_prof_text;
 
 // size-exact block cache (see exs_par.cuh); keyed per stream so handles on
@@ -165,6 +166,7 @@ struct Handle {
   float t_stage[4] = {0, 0, 0, 0};
   bool want_demands = false;
   u32 split_min = 16;  // statement-parallel body parsing threshold (tokens; C2 1 GB best)
+  long long select_flagged_min = EXS_SELECT_FLAGGED_MIN;  // select_idx flag-pass threshold (indices)
 
   void reset() {
     L.free_all(); L = LexState();
@@ -328,6 +330,9 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
   if (n_bytes >= (1ull << 31)) throw Err("batch larger than 2 GiB; split into batches");
   cudaStream_t st = H.st;
   H.reset();
+#ifndef EXS_EMU
+  g_select_flagged_min = H.select_flagged_min;
+#endif
   u64 launches0 = g_launches;
   Timer total(st);
   bool any_div = false;
@@ -625,6 +630,7 @@ int exs_set_option(exs_handle x, int key, int value) {
   else if (key == 2) g_profile = value != 0;  // per-launch device timing of later runs
 #endif
   else if (key == 3) x->h.split_min = value < 4 ? 4u : (u32)value;  // statement-split threshold (tokens)
+  else if (key == 4) x->h.select_flagged_min = value < 0 ? 0 : value;  // flag-pass selection threshold
   else throw Err("unknown option");
   API_END
 }

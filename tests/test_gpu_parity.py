@@ -45,6 +45,16 @@ def eng_split(X):
     return e
 
 
+@pytest.fixture(scope="module")
+def eng_flag(X):
+    """An engine whose ordered selections all take the flag pass + flagged
+    compaction (csrc/exs_par.cuh select_idx), which by default only inputs of
+    >= 4M indices reach."""
+    e = X.Engine(0)
+    e.handle.set_option(4, 0)
+    return e
+
+
 @pytest.mark.parametrize("split", [False, True], ids=["items", "stmt_split"])
 @pytest.mark.parametrize("group", GOLDEN_GROUPS)
 def test_golden_vectors(X, eng, eng_split, group, split):
@@ -105,25 +115,33 @@ def _check_against_oracle(X, eng, texts, modes):
     assert callsites == want_calls
 
 
-def test_c2_files_vs_oracle(X, eng):
+@pytest.mark.parametrize("flagged", [False, True], ids=["select_if", "select_flagged"])
+def test_c2_files_vs_oracle(X, eng, eng_flag, flagged):
+    eng = eng_flag if flagged else eng
     from paper_2309_03912_b200 import synth
     texts = [synth.gen_c2_file(1000 + s, 15000) for s in range(8)]
     _check_against_oracle(X, eng, texts, ["classic", "sound", "fidelity", "proposal1"] * 2)
 
 
-def test_c5_stressors_vs_oracle(X, eng):
+@pytest.mark.parametrize("flagged", [False, True], ids=["select_if", "select_flagged"])
+def test_c5_stressors_vs_oracle(X, eng, eng_flag, flagged):
+    eng = eng_flag if flagged else eng
     from paper_2309_03912_b200 import synth
     texts = [synth.gen_c5_file(500 + s, 12000, 0.5) for s in range(10)]
     _check_against_oracle(X, eng, texts, ["classic", "sound", "proposal2", "fidelity", "proposal1"] * 2)
 
 
-def test_c3_chain_vs_oracle(X, eng):
+@pytest.mark.parametrize("flagged", [False, True], ids=["select_if", "select_flagged"])
+def test_c3_chain_vs_oracle(X, eng, eng_flag, flagged):
+    eng = eng_flag if flagged else eng
     from paper_2309_03912_b200 import synth
     text = synth.gen_chain(24, 48)
     _check_against_oracle(X, eng, [text, text], ["classic", "sound"])
 
 
-def test_c4_callgraph_vs_oracle(X, eng):
+@pytest.mark.parametrize("flagged", [False, True], ids=["select_if", "select_flagged"])
+def test_c4_callgraph_vs_oracle(X, eng, eng_flag, flagged):
+    eng = eng_flag if flagged else eng
     from paper_2309_03912_b200 import synth
     text = synth.gen_callgraph(2000, 10, 7)
     _check_against_oracle(X, eng, [text], ["sound"])
@@ -209,3 +227,20 @@ def test_classification_exports_match_the_reference(X, eng):
             bad.append((c["name"], "structs", mine, c["structs"]))
     assert not bad, bad[:3]
     assert len(cases) > 800 and n_structs > 1000
+
+
+def test_select_paths_agree_at_scale(X, eng):
+    """At ~24 MB (about 6M view tokens) the default engine's parser selections
+    take the flag pass; an engine that never takes it must report the same
+    diagnostics for every unit, in the same order."""
+    from paper_2309_03912_b200 import synth
+    texts = [synth.gen_c2_file(7000 + s, 100_000) for s in range(240)]
+    units = [(t, f"s{i}.cu", X.CompileProfile(), X.Mode.CLASSIC, X.TraitConfig()) for i, t in enumerate(texts)]
+    flagged = eng.run_batch(units)
+    assert eng.last_stats["view_tokens"] >= 1 << 22
+    e_if = X.Engine(0)
+    e_if.handle.set_option(4, 2**31 - 1)
+    plain = e_if.run_batch(units)
+    assert sum(len(a.all_diagnostics) for a in flagged) > 0
+    for a, b in zip(flagged, plain):
+        assert as_rows(a) == as_rows(b)

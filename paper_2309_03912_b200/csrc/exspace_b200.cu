@@ -591,10 +591,9 @@ int exs_run(exs_handle x, const uint8_t* bytes, uint64_t n_bytes, const uint64_t
   CK(cudaSetDevice(H.device));
 #endif
   Timer th(H.st);
-  if (!H.d_src_owned || true) {
-    dfree(H.d_src_owned);
-    H.d_src_owned = dalloc<u8>(n_bytes + 64);
-  }
+  // size-exact block cache: a repeated batch size gets its block back
+  dfree(H.d_src_owned);
+  H.d_src_owned = dalloc<u8>(n_bytes + 64);
   h2d(H.d_src_owned, bytes, n_bytes, H.st);
   dzero(H.d_src_owned + n_bytes, 64, H.st);
   sync(H.st);

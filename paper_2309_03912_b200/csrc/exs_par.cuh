@@ -7,6 +7,10 @@
 #include <stdexcept>
 #include <string>
 
+// select_idx flag-pass threshold default (both builds)
+#ifndef EXS_SELECT_FLAGGED_MIN
+#define EXS_SELECT_FLAGGED_MIN (1ll << 22)
+#endif
 #ifndef EXS_EMU
 #include <cub/cub.cuh>
 #include <nvtx3/nvToolsExt.h>
@@ -149,9 +153,6 @@ extern std::vector<ProfRec> g_prof;
 extern thread_local const char* g_tag;  // name of the next launch (EXS_TAG)
 // select_idx switches to a flag pass + DeviceSelect::Flagged at this many indices
 // (set per run from the handle: exs_set_option key 4)
-#ifndef EXS_SELECT_FLAGGED_MIN
-#define EXS_SELECT_FLAGGED_MIN (1ll << 22)
-#endif
 extern thread_local i64 g_select_flagged_min;
 #define EXS_TAG(name) (::exs::g_tag = (name))
 #endif

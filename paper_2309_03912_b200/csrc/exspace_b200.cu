@@ -470,10 +470,42 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     u64* k = dalloc<u64>(nd + 1);
     u32* ix = dalloc<u32>(nd + 1);
     const Diag* dd = H.d_diags;
-    par_for(nd, [=] EXS_HD (i64 i) { ix[i] = (u32)i; k[i] = ((u64)dd[i].col << 8) | dd[i].code; }, st);
-    sort_pairs(k, ix, nd, H.sc, st);
-    par_for(nd, [=] EXS_HD (i64 i) { k[i] = ((u64)dd[ix[i]].file << 32) | dd[ix[i]].line; }, st);
-    sort_pairs(k, ix, nd, H.sc, st);
+    // field widths (OR of every value: its top bit is the maximum's)
+    u32* wor = dalloc<u32>(4);
+    dzero(wor, 16, st);
+    const i64 T = std::min<i64>((i64)nd, 1 << 16);
+    par_for(T, [=] EXS_HD (i64 t) {
+      u32 o[4] = {0, 0, 0, 0};
+      for (i64 i = t; i < (i64)nd; i += T) {
+        o[0] |= dd[i].file; o[1] |= dd[i].line; o[2] |= dd[i].col; o[3] |= dd[i].code;
+      }
+      for (int q = 0; q < 4; q++) {
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+        o[q] = __reduce_or_sync(__activemask(), o[q]);
+        if ((threadIdx.x & 31) != (__ffs(__activemask()) - 1)) continue;
+#endif
+        if (o[q]) at_or(&wor[q], o[q]);
+      }
+    }, st);
+    u32 wo[4] = {0, 0, 0, 0};
+    if (nd) { d2h(wo, wor, 16, st); sync(st); }
+    dfree(wor);
+    auto bits = [](u32 v) { int b = 0; while (v) { b++; v >>= 1; } return b; };
+    const int bf = bits(wo[0]), bl = bits(wo[1]), bc = bits(wo[2]), bk = bits(wo[3]);
+    if (bf + bl + bc + bk <= 64) {
+      // (file, line, col, code) in one key: one stable radix sort of bf+bl+bc+bk bits
+      const int sl = bk + bc, sf = bk + bc + bl;
+      par_for(nd, [=] EXS_HD (i64 i) {
+        ix[i] = (u32)i;
+        k[i] = (sf < 64 ? (u64)dd[i].file << sf : 0) | ((u64)dd[i].line << sl) | ((u64)dd[i].col << bk) | dd[i].code;
+      }, st);
+      sort_pairs(k, ix, nd, H.sc, st, std::max(1, bf + bl + bc + bk));
+    } else {
+      par_for(nd, [=] EXS_HD (i64 i) { ix[i] = (u32)i; k[i] = ((u64)dd[i].col << 16) | dd[i].code; }, st);
+      sort_pairs(k, ix, nd, H.sc, st, 48);
+      par_for(nd, [=] EXS_HD (i64 i) { k[i] = ((u64)dd[ix[i]].file << 32) | dd[ix[i]].line; }, st);
+      sort_pairs(k, ix, nd, H.sc, st);
+    }
     Diag* out = dalloc<Diag>(nd + 1);
     par_for(nd, [=] EXS_HD (i64 i) { out[i] = dd[ix[i]]; }, st);
     if ((u64)nd > H.diags_host_cap) {

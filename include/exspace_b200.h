@@ -162,7 +162,9 @@ int exs_describe(exs_handle h, const uint32_t* ids, const uint8_t* kinds, uint32
 /* options: 1 = also compute per-walk demand counts (Analysis.walks parity);
  * 3 = statement-parallel body parsing threshold (tokens, >= 4);
  * 4 = ordered selections of at least this many indices use a flag pass +
- *     flagged compaction (default 4M; 0 forces it, for the parity tests) */
+ *     flagged compaction (default 4M; 0 forces it, for the parity tests);
+ * 5 = nonzero: order diagnostics by two radix sorts ((col, code) then (file, line))
+ *     instead of one packed (file, line, col, code) key (for the parity tests) */
 int exs_set_option(exs_handle h, int key, int value);
 /* with EXS_PROFILE=1 in the environment: per-launch-site device times of the last run */
 const char* exs_profile_text(void);

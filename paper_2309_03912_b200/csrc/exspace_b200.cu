@@ -167,6 +167,7 @@ struct Handle {
   bool want_demands = false;
   u32 split_min = 16;  // statement-parallel body parsing threshold (tokens; C2 1 GB best)
   long long select_flagged_min = EXS_SELECT_FLAGGED_MIN;  // select_idx flag-pass threshold (indices)
+  bool diag_sort_two_pass = false;  // force the two-key diagnostic sort (parity tests)
 
   void reset() {
     L.free_all(); L = LexState();
@@ -492,7 +493,7 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     dfree(wor);
     auto bits = [](u32 v) { int b = 0; while (v) { b++; v >>= 1; } return b; };
     const int bf = bits(wo[0]), bl = bits(wo[1]), bc = bits(wo[2]), bk = bits(wo[3]);
-    if (bf + bl + bc + bk <= 64) {
+    if (bf + bl + bc + bk <= 64 && !H.diag_sort_two_pass) {
       // (file, line, col, code) in one key: one stable radix sort of bf+bl+bc+bk bits
       const int sl = bk + bc, sf = bk + bc + bl;
       par_for(nd, [=] EXS_HD (i64 i) {
@@ -662,6 +663,7 @@ int exs_set_option(exs_handle x, int key, int value) {
 #endif
   else if (key == 3) x->h.split_min = value < 4 ? 4u : (u32)value;  // statement-split threshold (tokens)
   else if (key == 4) x->h.select_flagged_min = value < 0 ? 0 : value;  // flag-pass selection threshold
+  else if (key == 5) x->h.diag_sort_two_pass = value != 0;  // diagnostic order by two sorts
   else throw Err("unknown option");
   API_END
 }

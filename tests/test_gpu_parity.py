@@ -244,3 +244,19 @@ def test_select_paths_agree_at_scale(X, eng):
     assert sum(len(a.all_diagnostics) for a in flagged) > 0
     for a, b in zip(flagged, plain):
         assert as_rows(a) == as_rows(b)
+
+
+def test_diag_sort_paths_agree(X, eng):
+    """Diagnostic order (reference: sorted by file, line, column, code) from the
+    single packed-key radix sort must equal the two-sort fallback used when the
+    fields exceed 64 bits, over a batch with thousands of diagnostics."""
+    from paper_2309_03912_b200 import synth
+    texts = [synth.gen_c2_file(9100 + s, 60_000) for s in range(64)]
+    units = [(t, f"d{i}.cu", X.CompileProfile(), X.Mode.CLASSIC, X.TraitConfig()) for i, t in enumerate(texts)]
+    packed = eng.run_batch(units)
+    e2 = X.Engine(0)
+    e2.handle.set_option(5, 1)
+    two = e2.run_batch(units)
+    assert sum(len(a.all_diagnostics) for a in packed) > 1000
+    for a, b in zip(packed, two):
+        assert as_rows(a) == as_rows(b)

@@ -358,10 +358,13 @@ inline void sort_pairs(u64* keys, u32* vals, i64 n, Scratch& sc, cudaStream_t s,
   dfree(v2);
   g_launches += 2;
 #else
-  (void)sc; (void)s; (void)end_bit;
+  (void)sc; (void)s;
+  // like CUB, order by bits [0, end_bit) only: a key with higher bits set
+  // sorts by its truncated value here too, so the emulation catches it
+  const u64 m = end_bit >= 64 ? ~0ull : ((1ull << end_bit) - 1);
   std::vector<std::pair<u64, u32>> v(n);
   for (i64 i = 0; i < n; i++) v[i] = {keys[i], vals[i]};
-  std::stable_sort(v.begin(), v.end(), [](auto& a, auto& b) { return a.first < b.first; });
+  std::stable_sort(v.begin(), v.end(), [m](auto& a, auto& b) { return (a.first & m) < (b.first & m); });
   for (i64 i = 0; i < n; i++) { keys[i] = v[i].first; vals[i] = v[i].second; }
 #endif
 }

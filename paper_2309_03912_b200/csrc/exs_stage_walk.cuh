@@ -89,14 +89,14 @@ EXS_HD inline void walker_for(Walker& w, const WalkCfg& C, const WalkBufs& B, u3
   w.native = (u8)(I.walk & 1);
   w.side = I.side;
   w.spaces = I.spaces;
-  w.clevel = (u8)(I.level + 1);
+  w.clevel = B.clevel;
   w.fn = I.fn;
   const Node& fn = C.nodes[fr.node];
   w.pragma = (fn.n & FF_PRAGMA) != 0;
   w.from_hd = I.spaces == 3;
   w.fidelity_host = (c & CFG_MODE_MASK) == MODE_FIDELITY && w.native == 0;
   w.parent_rank = rank;
-  w.stmt_k = 0; w.stmt_ord = 0; w.stmt_cs_base = 0; w.cs_ord = 0;
+  w.stmt_k = 0; w.stmt_ord = 0; w.stmt_ord_max = 0; w.stmt_cs_base = 0; w.cs_ord = 0;
   w.silent = false; w.asp = 0; w.nloc = 0; w.wdepth = 0;
   w.ebase = I.ebase;
   w.ecnt = 0;
@@ -112,7 +112,7 @@ inline WalkBufs make_bufs(WalkState& W, u32* n_diags, Diag* diags, u32 cap_diags
                           u32 dmask, u32* contract) {
   WalkBufs B;
   B.slots = W.slots; B.mask = W.mask; B.inst = W.inst;
-  B.n_inst = W.ctr(CNT_INST); B.cap_inst = W.cap_inst; B.lvl_base = 0;
+  B.n_inst = W.ctr(CNT_INST); B.cap_inst = W.cap_inst; B.lvl_base = 0; B.clevel = 0;
   B.edges = W.edges;
   B.pend = W.pend; B.n_pend = W.ctr(CNT_PEND); B.cap_pend = W.cap_pend;
   B.seeds = W.seeds; B.n_seeds = W.ctr(CNT_SEEDS); B.cap_seeds = W.cap_seeds;
@@ -233,6 +233,16 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     };
     u32* rcand = dalloc<u32>(2ull * NF + 1);
     const u32 NRC = select_idx(2ull * NF, is_root, rcand, L.cnt, sc, st);
+    // root ranks (make_ckey) are batch decl indices while they fit the rank
+    // field, else decl indices relative to the view's first decl
+    u32* vd0 = nullptr;
+    if (NF > CK_FIELD_MAX) {
+      const u32 NV = P.V;
+      vd0 = dalloc<u32>((u64)NV + 1);
+      dfill_ff(vd0, 4ull * (NV + 1), st);
+      u32* v0 = vd0;
+      par_for(NF, [=] EXS_HD (i64 i) { at_min(&v0[fr[i].view], (u32)i); }, st);
+    }
     if (NRC) {
       u64* key = dalloc<u64>(NRC);
       const u32* rcc = rcand;
@@ -293,7 +303,9 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         u32 k = 0;
         for (u8 sd = 0; sd < 2; sd++) {
           if (!((sides >> sd) & 1)) continue;
-          const unsigned long long ck = ((unsigned long long)(q.i & 0x3FFFFFFu) << 28) | k++;
+          const u32 rank = vd0 ? q.i - vd0[r.view] : q.i;  // decl order within the view
+          if (rank > CK_FIELD_MAX) { at_or(&B.contract[q.file], 1); return; }
+          const unsigned long long ck = make_ckey(0, rank, k++);
           const IKey key = make_ikey(r.sig_rep, vnone(), vnone(), q.ot, q.walk, sd);
           bool inserted;
           const u32 slot = slot_insert(B, key, inserted);
@@ -332,7 +344,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         const Node& fn = nd[r.node];
         const IKey key = make_ikey(r.sig_rep, vnone(), vnone(), q.ot, q.walk, sd);
         fill_instance(B.inst[id], tab, key, q.i, vnone(), vnone(), sd, r.rec, q.ot, fn.tok, q.walk,
-                      static_spaces(fn.n, q.free_main, q.sf, q.mode, sd), 0, slot);
+                      static_spaces(fn.n, q.free_main, q.sf, q.mode, sd), slot);
         B.slots[slot].sid = id;
       }, st);
       u32* ni = B.n_inst;
@@ -364,8 +376,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       w.native = (u8)p; w.side = 0; w.clevel = 0;  // roots are created at level 0
       w.fn = i; w.pragma = false; w.from_hd = false;
       w.fidelity_host = mode == MODE_FIDELITY && p == 0;
-      w.parent_rank = i; w.contract = false;
-      w.stmt_k = 0; w.stmt_ord = 0; w.stmt_cs_base = 0; w.cs_ord = 0;
+      w.parent_rank = vd0 ? i - vd0[r.view] : i; w.contract = false;
+      w.stmt_k = 0; w.stmt_ord = 0; w.stmt_ord_max = 2; w.stmt_cs_base = 0; w.cs_ord = 0;
       w.silent = false; w.asp = 0; w.nloc = 0; w.wdepth = 0; w.ebase = 0; w.ecnt = 0;
       Env none; none.clear();
       u8 sides;
@@ -385,11 +397,13 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         w.stmt_ord = k++;  // roots: decl order x side order (spacecheck.py:272-283)
         w.instantiate(i, vnone(), vnone(), sd, r.rec, none, ot, fn.tok);
       }
+      if (w.contract) at_or(&B.contract[file], 1);
     }, st);
     sync(st);
     dfree(rcand);
     dfree(rslot);
     dfree(rot);
+    dfree(vd0);
   }
   prof_mark(st);
   // ---- levels
@@ -435,7 +449,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
                       fr_tmp, L.cnt, sc, st);
       u64* keys = dalloc<u64>(nf + 1);
       par_for(nf, [=] EXS_HD (i64 j) { fr_tmp[j] += base; keys[j] = in[fr_tmp[j]].ckey; }, st);
-      sort_pairs(keys, fr_tmp, nf, sc, st, 54);  // bits 54+ hold the level: equal in a frontier
+      sort_pairs(keys, fr_tmp, nf, sc, st, CK_LEVEL_SHIFT);  // the level bits are equal in a frontier
       d2d(front, fr_tmp, 4ull * nf, st);
       sync(st);
       dfree(keys);
@@ -468,6 +482,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     grow_inst(W, (u64)n_now + std::min<u64>(S_level, 2ull * nnew_prev) + S_level / 8 + 65536, n_now, st);
     B = bufs();
     B.lvl_base = n_now;
+    B.clevel = level + 1;
     {
       Inst* in = W.inst; const u32* fl = front; u64 eu = edges_used;
       par_for(nf, [=] EXS_HD (i64 j) { in[fl[j]].ebase = (u32)(eu + eb[j]); }, st);
@@ -524,13 +539,33 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         dfree(key);
       }
 #endif
+      // parent ranks (make_ckey): frontier positions while they fit the rank
+      // field, else positions among the frontier entries of the same walk
+      // (creation keys are only compared within a walk)
+      u32* frank = nullptr;
+      if (nf > CK_FIELD_MAX) {
+        frank = dalloc<u32>(nf + 1);
+        u64* wk = dalloc<u64>(nf + 1);
+        u32* pos = dalloc<u32>(nf + 1);
+        u32* wfirst = dalloc<u32>((u64)NW + 1);
+        par_for(nf, [=] EXS_HD (i64 j) { wk[j] = in[fl[j]].walk; pos[j] = (u32)j; }, st);
+        int wbits = 1;
+        while (wbits < 32 && (NW >> wbits)) wbits++;
+        sort_pairs(wk, pos, nf, sc, st, wbits);  // stable: frontier order within a walk
+        par_for(nf, [=] EXS_HD (i64 p) { if (p == 0 || wk[p - 1] != wk[p]) wfirst[wk[p]] = (u32)p; }, st);
+        u32* fk = frank;
+        par_for(nf, [=] EXS_HD (i64 p) { fk[pos[p]] = (u32)p - wfirst[wk[p]]; }, st);
+        sync(st);
+        dfree(wk); dfree(pos); dfree(wfirst);
+      }
+      const u32* frk = frank;
       const u32* pm = perm;
       EXS_TAG("walk_chunks");
       par_for_walk(nwi, [=] EXS_HD (i64 ii) {
         const u32 i = pm ? pm[ii] : (u32)ii;
         const u32 j = itj[i], c = itc[i];
         Walker w;
-        walker_for(w, Cc, B, fl[j], (u64)j);
+        walker_for(w, Cc, B, fl[j], frk ? (u64)frk[j] : (u64)j);
         const FnRec& r = fr[w.fn];
         u32 k0 = c * KCH, k1 = k0 + KCH < r.nstmts ? k0 + KCH : r.nstmts;
 #ifdef EXS_EXP_NOWALK  // timing experiment only: walker set-up without the statements
@@ -545,6 +580,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       dfree(wc);
       dfree(wb);
       dfree(perm);
+      dfree(frank);
       dfree(itj);
       dfree(itc);
     }

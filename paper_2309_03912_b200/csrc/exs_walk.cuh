@@ -24,13 +24,30 @@ struct alignas(32) Slot {
   unsigned long long sck;
 };
 
+// Creation key (the reference's FIFO position, spacecheck.py:312-351):
+//   level << CK_LEVEL_SHIFT | parent rank << CK_RANK_SHIFT | local
+// level: BFS level of the created instance (roots 0); parent rank: the
+// creator's position among its walk's frontier of the previous level, by
+// creation key (roots: decl order within the view); local: the creator's
+// instantiation ordinal within its body, 2 x (call sites of the earlier
+// top-level statements) + ordinal within the statement (a call site
+// instantiates at most twice, spacecheck.py:585-596).  A field beyond its
+// width marks the unit out of contract (X9999) instead of wrapping.
+#define CK_LEVEL_SHIFT 52
+#define CK_RANK_SHIFT 26
+#define CK_FIELD_MAX ((1u << 26) - 1u)
+#define CK_LEVEL_MAX ((1u << 12) - 1u)
+EXS_HD inline unsigned long long make_ckey(u32 level, u64 rank, u32 local) {
+  return ((unsigned long long)level << CK_LEVEL_SHIFT) | ((unsigned long long)rank << CK_RANK_SHIFT) | local;
+}
+
 struct Inst {
   u64 ka, kb;
-  unsigned long long ckey;  // min creation key (level<<52 | parent rank<<24 | local)
+  unsigned long long ckey;  // min creation key (make_ckey)
   u32 fn, orec, walk, at;   // creating decl, owner struct, walk, at_loc token
   u32 ebase, ecnt;          // legal edges (callee instance ids)
   Val tb, hb, ot;           // type binding, hdc binding, owner type
-  u8 side, spaces, level, flags;
+  u8 side, spaces, pad, flags;
   u32 slot;                 // hash slot of the key (creation key lives in sck[slot] during its level)
 };
 enum { IF_BODY = 1, IF_MAIN = 2 };
@@ -52,6 +69,7 @@ struct WalkBufs {
   u32* n_inst;
   u32 cap_inst;
   u32 lvl_base;             // ids >= lvl_base were created in the level being walked
+  u32 clevel;               // level of the instances the walkers of this launch create
   // outputs
   u32* edges;
   Pending* pend;
@@ -182,15 +200,14 @@ EXS_HD inline IKey make_ikey(u32 sig_rep, const Val& tb, const Val& hb, const Va
   return k;
 }
 EXS_HD inline void fill_instance(Inst& I, const Tables* T, const IKey& k, u32 fi, const Val& tb, const Val& hb,
-                                 u8 side, u32 orec, const Val& ot, u32 at_tok, u32 walk, u8 sp, u8 clevel,
-                                 u32 slot) {
+                                 u8 side, u32 orec, const Val& ot, u32 at_tok, u32 walk, u8 sp, u32 slot) {
   const FnRec& fr = T->fns[fi];
   const Node& fnn = T->nodes[fr.node];
   I.ka = k.a; I.kb = k.b;
   I.ckey = ~0ull; I.fn = fi; I.orec = orec; I.walk = walk; I.at = at_tok;
   I.ebase = 0; I.ecnt = 0;
   I.tb = tb; I.hb = hb; I.ot = ot;
-  I.side = side; I.spaces = sp; I.level = clevel; I.slot = slot;
+  I.side = side; I.spaces = sp; I.pad = 0; I.slot = slot;
   // IF_BODY: a body to walk -- statements or parameter types to resolve (an
   // empty, parameterless body creates nothing and reports nothing)
   I.flags = ((fnn.n & FF_BODY) && (fr.nstmts || fnn.c1 != NONE)) ? IF_BODY : 0;
@@ -217,7 +234,7 @@ EXS_HD inline u32 slot_insert(const WalkBufs& B, const IKey& k, bool& inserted) 
 // it; the post-level fixup applies the entry whose key equals the minimum).
 EXS_HD EXS_FI u32 create_instance(const WalkBufs& B, const Tables* T, u32 fi, const Val& tb, const Val& hb,
                                   u8 want_side, u32 orec, const Val& ot, u32 at_tok, u32 walk, u8 sp,
-                                  u8 clevel, unsigned long long ck) {
+                                  unsigned long long ck) {
   const FnRec& fr = T->fns[fi];
   const IKey k = make_ikey(fr.sig_rep, tb, hb, ot, walk, want_side);
   bool inserted;
@@ -225,7 +242,7 @@ EXS_HD EXS_FI u32 create_instance(const WalkBufs& B, const Tables* T, u32 fi, co
   u32 id = inst_lookup_or_insert(B, k, inserted, slot);
   if (id == NONE) return NONE;
   if (inserted) {
-    fill_instance(B.inst[id], T, k, fi, tb, hb, want_side, orec, ot, at_tok, walk, sp, clevel, slot);
+    fill_instance(B.inst[id], T, k, fi, tb, hb, want_side, orec, ot, at_tok, walk, sp, slot);
     inst_publish(B, slot, id);
   }
   if (id >= B.lvl_base) {
@@ -306,11 +323,12 @@ struct Walker {
   const Tables* T;
   u32 file, walk, inst_id;
   u8 native, side, spaces;   // side 0 host 1 device; spaces bits 1 H 2 D 4 G
-  u8 clevel;                 // level of the instances this walker creates
+  u32 clevel;                // level of the instances this walker creates
   u32 fn;                    // decl of the instance
   bool pragma, from_hd, fidelity_host;
   u64 parent_rank;           // dense rank of this instance within its level
-  u32 stmt_k, stmt_ord;      // creation order: (top-level statement, ordinal within it)
+  u32 stmt_k, stmt_ord;      // top-level statement, instantiations in it so far
+  u32 stmt_ord_max;          // 2 x call sites of the statement (bound of stmt_ord)
   u32 ebase, ecnt;           // edge slots of this instance, legal edges written
   u32 stmt_cs_base, cs_ord;  // edge slot of the current statement, edges in it so far
   bool silent;               // replaying declarations of earlier chunks: no side effects
@@ -374,17 +392,21 @@ struct Walker {
   // _instantiate (spacecheck.py:312-351); returns instance id or NONE
   EXS_HD EXS_FI u32 instantiate(u32 fi, const Val& tb, const Val& hb, u8 want_side, u32 orec,
                          const Env& obinds, const Val& ot, u32 at_tok) {
-    u32 my_local = (stmt_k << 12) | (stmt_ord++ & 0xFFFu);
+    // creation order (make_ckey): a field past its width is out of contract
+    const u32 ord = stmt_ord++;
+    const u64 my_local = 2ull * stmt_cs_base + ord;
+    if (ord >= stmt_ord_max || my_local > CK_FIELD_MAX || parent_rank > CK_FIELD_MAX || clevel > CK_LEVEL_MAX) {
+      contract = true;
+      return NONE;
+    }
     u8 sp;
     S.depth = 0;
     u8 st = S.spaces(fi, &obinds, tb, hb, want_side, at_tok, orec, sp);
     if (S.contract) { contract = true; return NONE; }
     if (st == ST_SEMA) { emit_err(); return NONE; }
     if (st == ST_SUBST) { emit_tok(C_E0001, at_tok, M_W_PRED_CONST); return NONE; }
-    unsigned long long ck = ((unsigned long long)clevel << 54) |
-                            ((unsigned long long)(parent_rank & 0x3FFFFFFull) << 28) |
-                            (my_local & 0xFFFFFFFu);
-    return create_instance(*B, T, fi, tb, hb, want_side, orec, ot, at_tok, walk, sp, clevel, ck);
+    const unsigned long long ck = make_ckey(clevel, parent_rank, (u32)my_local);
+    return create_instance(*B, T, fi, tb, hb, want_side, orec, ot, at_tok, walk, sp, ck);
   }
 
   EXS_HD void add_binds(const Node& fnn, const Val& tb, const Val& hb, Env& e) const {
@@ -482,7 +504,9 @@ struct Walker {
       nviable++;
     }
     u32 first_ok = nviable ? vfi[0] : NONE;
-    if (S.mode == MODE_P2 && nviable > 1 && nviable <= 8) {
+    // the proposal2 space filter keeps the first 8 survivors: more is out of contract
+    if (S.mode == MODE_P2 && nviable > 8) { contract = true; return false; }
+    if (S.mode == MODE_P2 && nviable > 1) {
       u32 nc = 0;
       for (u32 j = 0; j < nviable; j++)
         if (S.compatible(vfi[j], ctx_side, member ? rec : NONE)) vfi[nc++] = vfi[j];
@@ -784,10 +808,12 @@ struct Walker {
       }
     }
     silent = false;
+    const FnRec& fr = T->fns[fn];
     for (u32 k = k0; k < k1 && !contract; k++) {
       stmt_k = k;
       stmt_ord = 0;
       stmt_cs_base = stmt_cs[sbase + k];
+      stmt_ord_max = 2u * ((k + 1 < fr.nstmts ? stmt_cs[sbase + k + 1] : fr.ncalls) - stmt_cs_base);
       cs_ord = 0;
       stmt_top(stmt_node[sbase + k]);
     }

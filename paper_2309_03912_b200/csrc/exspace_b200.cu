@@ -357,8 +357,10 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     L.cfg = dalloc<u8>(n_files + 1);
     if (n_files) h2d(L.cfg, cfg, n_files, st);
     // diagnostics buffers
+    // n_files slots past the capacity the stages use: the out-of-contract
+    // markers written after the last retry always fit
     H.cap_diags = cap_diags;
-    H.d_diags = dalloc<Diag>(cap_diags);
+    H.d_diags = dalloc<Diag>((u64)cap_diags + n_files);
     H.dmask = pow2_at_least(2ull * cap_diags) - 1;
     H.d_dset = dalloc<u64>((u64)H.dmask + 1);
     dzero(H.d_dset, 8ull * (H.dmask + 1), st);
@@ -418,7 +420,7 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
         // set, keep the diagnostics of the earlier stages, re-run the walk only
         const u32 nd_now = get1(H.d_ndiags, st);
         const u32 ncap = (u32)std::min<u64>(4ull * std::max(nd_now, cap_diags), 0x7FFFFFFFull);
-        Diag* ndg = dalloc<Diag>(ncap);
+        Diag* ndg = dalloc<Diag>((u64)ncap + n_files);
         if (nd0) d2d(ndg, H.d_diags, sizeof(Diag) * (u64)nd0, st);
         const u32 nmask = pow2_at_least(2ull * ncap) - 1;
         u64* nset = dalloc<u64>((u64)nmask + 1);
@@ -459,14 +461,14 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
   {
     u32* ct = H.d_contract;
     WalkBufs B{};
-    B.diags = H.d_diags; B.n_diags = H.d_ndiags; B.cap_diags = H.cap_diags; B.dset = H.d_dset;
+    B.diags = H.d_diags; B.n_diags = H.d_ndiags; B.cap_diags = H.cap_diags + n_files; B.dset = H.d_dset;
     B.dmask = H.dmask; B.overflow = H.W.ctr(CNT_OVF);
     par_for(n_files, [=] EXS_HD (i64 f) {
       if (ct[f]) emit_diag(B, mkdiag((u32)f, 1, 1, C_X9999, M_X_CONTRACT));
     }, st);
   }
   // order diagnostics by (file, line, col, code) with two stable radix passes
-  u32 nd = std::min(get1(H.d_ndiags, st), H.cap_diags);
+  u32 nd = std::min(get1(H.d_ndiags, st), H.cap_diags + n_files);
   {
     u64* k = dalloc<u64>(nd + 1);
     u32* ix = dalloc<u32>(nd + 1);

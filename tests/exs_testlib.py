@@ -8,7 +8,7 @@ ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 GOLDEN = ROOT / "tests" / "golden"
-GOLDEN_GROUPS = ["corpus", "genunit", "snippets", "synthetic", "mutations"]
+GOLDEN_GROUPS = ["corpus", "genunit", "snippets", "synthetic", "mutations", "semadiag"]
 
 from oracle import exs_oracle as O  # noqa: E402
 

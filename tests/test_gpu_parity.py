@@ -123,6 +123,41 @@ def test_c2_files_vs_oracle(X, eng, eng_flag, flagged):
     _check_against_oracle(X, eng, texts, ["classic", "sound", "fidelity", "proposal1"] * 2)
 
 
+def test_c2_100kb_files_vs_oracle(X, eng):
+    """Full-size C2 files (the bench's ~100 KB shape, seeds the bench times)."""
+    from paper_2309_03912_b200 import synth
+    texts = [synth.gen_c2_file(s, 100_000) for s in (0, 1, 4242)]
+    _check_against_oracle(X, eng, texts, ["classic", "sound", "proposal2"])
+
+
+def _ckey_unit(n, nested):
+    """g<A>() demanded on the host pass only (E1201 at its first demand), then
+    n calls, then g<A>() again: the second creator sits past the old 12-bit
+    ordinal (nested) or 16-bit statement field (top level) of the creation key
+    (exs_walk.cuh creation-key widths)."""
+    ind = "    " if nested else "  "
+    lines = ["struct A { __host__ __device__ void call() {} };", "template< typename T >",
+             "__host__ __device__ void g() { T{}.call(); }", "__host__ __device__ void h() {}",
+             "__host__ __device__ void run() {"]
+    if nested:
+        lines.append("  if ( true ) {")
+    lines += ["#ifndef __CUDA_ARCH__", ind + "g< A >();"] + [ind + "h();"] * n + [ind + "g< A >();", "#endif"]
+    if nested:
+        lines.append("  }")
+    lines += ["}", "int main() { run(); }"]
+    return "\n".join(lines) + "\n"
+
+
+@pytest.mark.parametrize("shape", ["ordinal_4096", "statement_65536"])
+def test_creation_key_fields_do_not_wrap(X, eng, shape):
+    text = _ckey_unit(4095, True) if shape == "ordinal_4096" else _ckey_unit(65535, False)
+    for m in ("sound", "proposal2"):
+        a = eng.run_batch([(text, "u.mcu", X.CompileProfile(), X.Mode(m), X.TraitConfig())])[0]
+        rows, _, _ = _oracle_rows(text, m)
+        assert as_rows(a) == rows
+        assert [r[0] for r in rows] == ["E1201"]
+
+
 @pytest.mark.parametrize("flagged", [False, True], ids=["select_if", "select_flagged"])
 def test_c5_stressors_vs_oracle(X, eng, eng_flag, flagged):
     eng = eng_flag if flagged else eng

@@ -1,21 +1,32 @@
-"""Benchmark: stray-call analysis of the C2 synthetic corpus on B200.
+"""Benchmark: stray-call analysis of synthetic CUDA corpora on B200.
 
 Metric (BASELINE.json): source GB/s scanned (+ call-graph edges/s), with the
-stray-call set bit-exact vs the CPU reference (parity is pinned by tests/).
-Workload: C2 = 10,000 seeded synthetic MiniCU files of ~100 KB (~1 GB), one
-GPU per 10,000 files (weak scaling over ranks), mode classic, profile nvcc 12.
+stray-call set bit-exact vs the CPU reference.  Default workload C2: 10,000
+seeded synthetic MiniCU files of ~100 KB (~1 GB) per GPU (weak scaling over
+ranks), mode classic, profile nvcc 12.  Other BASELINE.json configs:
+``--config c3`` (one unit of depth-64 template chains, ~1M instantiations per
+walk), ``--config c4`` (one unit, 10M functions / 100M call edges),
+``--config c5`` (lexer-stressor corpus: 8 GB per GPU, i.e. 64 GB on 8 GPUs,
+streamed through the public API in batches).
 
 A step = one full analysis of the rank's corpus: lex -> parse -> symbol join
--> instantiation fixpoint -> reachability -> ordered stray-call set.
+-> instantiation fixpoint -> reachability -> verdicts -> rendered, ordered,
+de-duplicated diagnostics (the reference's ``finish_diagnostics`` output).
   value : corpus already resident in HBM (exs_run_device), device time (CUDA
           events on the library stream), max over ranks.
-  e2e   : the public C-ABI entry exs_run with the corpus in pinned host memory
-          (H2D inside) plus the D2H read of the diagnostic records.
-Inputs (1 GB) exceed the 126 MB L2, so no L2 flush is needed between steps.
+  e2e   : the public Python API ``analyze_corpus(units)`` with the units as
+          host ``str`` objects: pack into page-locked memory, H2D, analysis,
+          message rendering, D2H of the results and the per-unit Analysis
+          objects, wall time, max over ranks.
+  parity: the oracle (CPU restatement of the reference, test infrastructure)
+          on a sample of the files timed, compared with the e2e run's output.
+Inputs (>= 1 GB) exceed the 126 MB L2, so no L2 flush is needed between steps.
 
---impl reference: the reference algorithm on the host CPU cores (the oracle
-port in oracle/exs_oracle.py, the reference being pure Python) over a bounded
-sample of the same workload, multiprocessing over all cores.
+--impl reference: the reference package itself (pip-installed unmodified into
+baseline/_ref from /root/reference; pure Python) timed on the host cores over a
+bounded sample of the same files, multiprocessing over all cores.
+
+--gpus N without torchrun re-launches itself under torch.distributed.run.
 """
 from __future__ import annotations
 
@@ -41,20 +52,62 @@ METRIC = "source GB/s scanned + call-graph edges/s, stray-call set bit-exact vs 
 PEAKS = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
 HBM_PEAK = float(PEAKS.get("hbm_gbs", 6650.0))
 HBM_PEAK_SRC = "measured" if "hbm_gbs" in PEAKS else "fallback"
+REF_DIR = ROOT / "baseline" / "_ref"
+STRAY = ("E1001", "E1002", "W1101", "W1102", "E1101", "E1102", "E1501", "W1502")
 
+
+# ---------------------------------------------------------------------------
+# workloads
 
 def _gen(args):
-    seed, size = args
-    return synth.gen_c2_file(seed, size).encode()
+    kind, seed, size = args
+    if kind == "c5":
+        return synth.gen_c5_file(seed, size, 0.01)
+    return synth.gen_c2_file(seed, size)
 
 
-def make_corpus(n_files: int, file_bytes: int, seed0: int, procs: int):
+def make_texts(kind: str, seeds, file_bytes: int, procs: int):
     with mp.Pool(procs) as pool:
-        blobs = pool.map(_gen, [(seed0 + i, file_bytes) for i in range(n_files)], chunksize=32)
-    offs = np.zeros(n_files + 1, dtype=np.uint64)
-    offs[1:] = np.cumsum([len(b) for b in blobs])
-    return blobs, offs
+        return pool.map(_gen, [(kind, s, file_bytes) for s in seeds], chunksize=16)
 
+
+class Workload:
+    """Units of one rank: (paths, texts) plus how to describe them."""
+
+    def __init__(self, a, rank: int, world: int):
+        procs = max(1, (os.cpu_count() or 8) // max(world, 1))
+        self.mode = "classic"
+        if a.config == "c2":
+            seeds = range(rank * a.files, (rank + 1) * a.files)
+            self.texts = make_texts("c2", seeds, a.file_bytes, procs)
+            self.paths = [f"c2/r{rank}/f{s:07d}.cu" for s in seeds]
+            self.desc = f"C2: {a.files} seeded MiniCU files x ~{a.file_bytes // 1000} KB per GPU, classic, nvcc 12"
+        elif a.config == "c3":
+            self.texts = [synth.gen_chain(64, a.c3_structs)]
+            self.paths = ["c3/chains.cu"]
+            self.desc = f"C3: one unit, 64-deep template chains over {a.c3_structs} structs, classic, nvcc 12"
+        elif a.config == "c4":
+            self.texts = [synth.gen_callgraph(a.c4_funcs, 10, 7 + rank)]
+            self.paths = [f"c4/r{rank}/callgraph.cu"]
+            self.mode = "sound"
+            self.desc = f"C4: one unit, {a.c4_funcs} functions x 10 random calls, sound, nvcc 12"
+        else:  # c5: a pool of distinct stressor files cycled to c5_gb per GPU
+            pool_n = a.c5_pool
+            seeds = range(rank * pool_n, (rank + 1) * pool_n)
+            pool_t = make_texts("c5", seeds, a.file_bytes, procs)
+            per = sum(len(t) for t in pool_t) / pool_n
+            n = int(a.c5_gb * 1e9 / per)
+            self.texts = [pool_t[i % pool_n] for i in range(n)]
+            self.paths = [f"c5/r{rank}/u{i:07d}.cu" for i in range(n)]
+            self.pool = pool_n
+            self.desc = (f"C5: {n} units (~{a.c5_gb:g} GB) per GPU cycling {pool_n} distinct seeded "
+                         f"lexer-stressor files (~1% malformed), classic, nvcc 12; each unit analysed "
+                         f"independently, every byte packed, copied and lexed")
+        self.nbytes = sum(len(t) for t in self.texts)
+
+
+# ---------------------------------------------------------------------------
+# NVML clocks sampled during the timed region
 
 class ClockSampler:
     """SM clocks and throttle reasons sampled during the timed region (NVML in
@@ -132,39 +185,119 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm (oracle port of the reference algorithm)
+# the reference (pure Python, installed unmodified into baseline/_ref) and the
+# oracle port (tests' checker) on host cores
 
-def _oracle_file(blob: bytes):
-    from oracle import exs_oracle as O  # the checker/baseline only
-    r = O.analyze_unit(blob.decode(), "classic")
-    return len(blob), O.edge_count(r), sum(1 for d in r.diagnostics if d[0] in (
-        "E1001", "E1002", "W1101", "W1102", "E1101", "E1102", "E1501", "W1502"))
+def _ref_import():
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import exspace  # noqa: F401
+    from exspace import spacecheck, preprocess  # noqa: F401
+    return exspace
 
 
-def cpu_reference(n_sample: int, file_bytes: int, seed0: int, cores: int):
-    """Time the reference algorithm over a bounded sample on `cores` processes."""
-    blobs, _ = make_corpus(n_sample, file_bytes, seed0, cores)
+def _ref_unit(args):
+    """One unit through the reference's own public API (spacecheck.py:687-739)."""
+    text, mode = args
+    ex = _ref_import()
+    from exspace.spacecheck import Mode, analyze
+    from exspace.syntax.preprocess import CompileProfile
     t0 = time.perf_counter()
-    with mp.Pool(cores) as pool:
-        res = pool.map(_oracle_file, blobs, chunksize=1)
+    a = analyze(text, "u.cu", CompileProfile(), Mode(mode))
+    dt = time.perf_counter() - t0
+    edges = sum(len(v) for w in a.walks.values() for v in w.edges.values())
+    _ = ex
+    return len(text.encode()), edges, sum(1 for d in a.diagnostics if d.code in STRAY), dt
+
+
+def reference_kind():
+    try:
+        _ref_import()
+        return "reference"
+    except Exception:
+        return "port"
+
+
+def _port_unit(args):
+    text, mode = args
+    from oracle import exs_oracle as O  # the checker / baseline only
+    t0 = time.perf_counter()
+    r = O.analyze_unit(text, mode)
+    dt = time.perf_counter() - t0
+    return (len(text.encode()), O.edge_count(r),
+            sum(1 for d in r.diagnostics if d[0] in STRAY), dt)
+
+
+def cpu_reference(texts, mode: str, cores: int):
+    """Time the reference over ``texts`` on ``cores`` processes."""
+    fn = _ref_unit if reference_kind() == "reference" else _port_unit
+    t0 = time.perf_counter()
+    if cores <= 1:
+        res = [fn((t, mode)) for t in texts]
+    else:
+        with mp.Pool(cores) as pool:
+            res = pool.map(fn, [(t, mode) for t in texts], chunksize=1)
     dt = time.perf_counter() - t0
     nbytes = sum(r[0] for r in res)
     edges = sum(r[1] for r in res)
+    cpu_s = sum(r[3] for r in res)
     return {"gbs": nbytes / dt / 1e9, "edges_per_s": edges / dt, "seconds": dt, "bytes": nbytes,
-            "files": n_sample}
+            "files": len(texts), "gbs_per_core": nbytes / cpu_s / 1e9 if cpu_s else None}
+
+
+def _oracle_check(args):
+    text, mode = args
+    from oracle import exs_oracle as O  # the checker only
+    return O.check(text, mode)
+
+
+def parity_sample(analyses, texts, idx, mode, procs):
+    """Compare the e2e run's ordered diagnostics of units ``idx`` with the
+    oracle (pinned to the reference's golden vectors)."""
+    with mp.Pool(procs) as pool:
+        want = pool.map(_oracle_check, [(texts[i], mode) for i in idx], chunksize=1)
+    bad = 0
+    n_d = n_s = 0
+    for i, w in zip(idx, want):
+        got = [(d.code, d.loc.line, d.loc.col, d.message) for d in analyses[i].diagnostics]
+        n_d += len(got)
+        n_s += sum(1 for g in got if g[0] in STRAY)
+        if got != w:
+            bad += 1
+    return {"files": len(idx), "mismatches": bad, "diagnostics": n_d, "stray": n_s,
+            "checker": "oracle/exs_oracle.py (pinned to the reference's golden vectors)"}
 
 
 def run_reference_arm(a, rank, world):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    # bounded sample: ~8 files per core of the same C2 shape per step (~5 s)
-    n = max(cores * 8, 32)
+    kind = reference_kind()
+    n = max(cores * 8, 32) if a.config in ("c2", "c5") else 1
     vals = []
-    for i in range(a.warmup + a.steps):
-        r = cpu_reference(n, a.file_bytes, 10_000 + i * n, cores)
-        if i >= a.warmup:
-            vals.append(r)
+    if a.config in ("c2", "c5"):
+        # the files the GPU arm times (rank 0's seeds), a window per step
+        pool = a.files if a.config == "c2" else a.c5_pool
+        for i in range(a.warmup + a.steps):
+            seeds = [(i * n + j) % pool for j in range(n)]
+            texts = make_texts(a.config, seeds, a.file_bytes, cores)
+            r = cpu_reference(texts, "classic", cores)
+            if i >= a.warmup:
+                vals.append(r)
+        sample = (f"{n} of the timed {a.config.upper()} files (~{n * a.file_bytes / 1e6:.1f} MB) per step, "
+                  f"{'the reference package (baseline/_ref) exspace.analyze' if kind == 'reference' else 'oracle port'}"
+                  f" over {cores} processes")
+        workload = f"{a.config.upper()} sample of the GPU arm's files, classic, nvcc 12"
+    else:
+        small = {"c3": synth.gen_chain(64, 512), "c4": synth.gen_callgraph(100_000, 10, 7)}[a.config]
+        mode = "sound" if a.config == "c4" else "classic"
+        for i in range(max(1, min(a.steps, 2))):
+            vals.append(cpu_reference([small], mode, 1))
+        sample = ({"c3": "one unit of 64-deep chains over 512 structs",
+                   "c4": "one unit of 100k functions x 10 calls (C4 scaled down 100x)"}[a.config] +
+                  f", {'reference package' if kind == 'reference' else 'oracle port'} on 1 core")
+        workload = f"{a.config.upper()} scaled-down sample, 1 core"
+        cores = 1
     gbs = statistics.mean(v["gbs"] for v in vals)
     eps = statistics.mean(v["edges_per_s"] for v in vals)
     ms = statistics.mean(v["seconds"] for v in vals) * 1e3
@@ -172,13 +305,11 @@ def run_reference_arm(a, rank, world):
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (seeded C2 generator, paper_2309_03912_b200/synth.py)",
-        "config": {"workload": "C2 sample: ~100 KB seeded MiniCU files, classic, nvcc 12",
-                   "files_per_step": n, "file_bytes": a.file_bytes},
+        "data": "synthetic (seeded generators, paper_2309_03912_b200/synth.py)",
+        "config": {"workload": workload, "files_per_step": n, "file_bytes": a.file_bytes},
         "edges_per_s": eps,
-        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} C2 files (~{n * a.file_bytes / 1e6:.1f} MB) per step, "
-                                   f"oracle/exs_oracle.py over {cores} processes"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
+                         "gbs_per_core": statistics.mean(v["gbs_per_core"] or 0 for v in vals)},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -190,75 +321,88 @@ def run_reference_arm(a, rank, world):
 def run_gpu_arm(a, rank, world, local):
     import torch
     from paper_2309_03912_b200 import _native
+    from paper_2309_03912_b200 import exspace as X
 
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    procs = max(1, (os.cpu_count() or 8) // max(world, 1))
-    blobs, offs = make_corpus(a.files, a.file_bytes, rank * a.files, procs)
-    host = torch.frombuffer(bytearray(b"".join(blobs)), dtype=torch.uint8).pin_memory()
-    nbytes = host.numel()
-    dev = host.to(f"cuda:{local}", non_blocking=False)
-    torch.cuda.synchronize()
-    cfg = np.zeros(a.files, dtype=np.uint8)  # classic, nvcc 12
-    h = _native.Handle(local)
+    W = Workload(a, rank, world)
+    mode = W.mode
+    prof = X.CompileProfile()
+    cfgb = X.cfg_byte(prof, X.Mode(mode), X.TraitConfig())
+    eng = X.Engine(local, batch_mib=a.batch_mib)
+    h = eng.handle
+    nbytes = W.nbytes
+    resident = a.config != "c5"  # C5 (8 GB per GPU) is measured end to end only
+    if resident:
+        blob = b"".join(t.encode() for t in W.texts)
+        offs = np.zeros(len(W.texts) + 1, dtype=np.uint64)
+        offs[1:] = np.cumsum([len(t) for t in W.texts])
+        dev = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(f"cuda:{local}")
+        del blob
+        cfg = np.full(len(W.texts), cfgb, dtype=np.uint8)
+        torch.cuda.synchronize()
 
     def run_resident():
         h.run_device(dev.data_ptr(), nbytes, offs, cfg)
         return h.stats()
 
+    units = list(zip(W.paths, W.texts))
+
     def run_e2e():
         t0 = time.perf_counter()
-        h.lib.exs_run(h.h, _native.C.c_void_p(host.data_ptr()), nbytes, _native._ptr(offs),
-                      a.files, _native._ptr(cfg))
-        recs = h.diags(copy=False)  # D2H into pinned host memory inside exs_run; zero-copy view
-        return time.perf_counter() - t0, recs.nbytes
+        res = X.analyze_corpus(units, prof, X.Mode(mode), device=local, engine=eng)
+        return time.perf_counter() - t0, res
 
-    for _ in range(a.warmup):
-        st = run_resident()
+    steps, kern = [], {}
+    clk_sum = None
+    if resident:
+        for _ in range(a.warmup):
+            run_resident()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        h.set_option(2, 1)
+        with ClockSampler(local) as clk:
+            for _ in range(a.steps):
+                steps.append(run_resident())
+                for ln in h.lib.exs_profile_text().decode().splitlines():
+                    parts = ln.split()
+                    if len(parts) >= 4 and not parts[0].startswith("[") and ":" not in parts[0]:
+                        k = kern.setdefault(parts[0], [0.0, 0])
+                        k[0] += float(parts[1])
+                        k[1] += int(parts[3].lstrip("x"))
+        h.set_option(2, 0)
+        clk_sum = clk.summary()
+        torch.cuda.synchronize()
+    # e2e through the public API with host str units
+    for _ in range(1 if a.config == "c5" else max(1, min(a.warmup, 2))):
+        run_e2e()
     if dist:
         dist.barrier()
-    torch.cuda.synchronize()
-    steps = []
-    kern = {}  # tag -> [total ms, launches] over the timed steps (CUDA events, library stream)
-    h.set_option(2, 1)
-    with ClockSampler(local) as clk:
-        for _ in range(a.steps):
-            steps.append(run_resident())
-            for ln in h.lib.exs_profile_text().decode().splitlines():
-                parts = ln.split()
-                if len(parts) >= 4 and not parts[0].startswith("[") and ":" not in parts[0]:
-                    k = kern.setdefault(parts[0], [0.0, 0])
-                    k[0] += float(parts[1])
-                    k[1] += int(parts[3].lstrip("x"))
-    h.set_option(2, 0)
-    torch.cuda.synchronize()
-    ms = [s["ms_total"] for s in steps]
-    lex_ms = [s["ms_lex"] for s in steps]
-    mean_ms = statistics.mean(ms)
-    # e2e through the public C ABI with host buffers
-    e2e_t = []
-    d2h_b = 0
-    run_e2e()  # warm-up of the host-buffer path (its device staging buffer), untimed
-    for _ in range(max(1, min(a.steps, 3))):
-        t, d2h_b = run_e2e()
-        e2e_t.append(t)
+    e2e_t, res = [], None
+    e2e_stats = []
+    with ClockSampler(local) as clk2:
+        for _ in range(a.steps if a.config != "c5" else max(1, min(a.steps, 2))):
+            t, res = run_e2e()
+            e2e_t.append(t)
+            e2e_stats.append(eng.last_stats)
+    if clk_sum is None:
+        clk_sum = clk2.summary()
+    d2h_b = int(eng.last_result_bytes)
     e2e_ms = statistics.mean(e2e_t) * 1e3
+    mean_ms = statistics.mean(s["ms_total"] for s in steps) if steps else e2e_ms
     if dist:
         tt = torch.tensor([mean_ms, e2e_ms], device=f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         mean_ms, e2e_ms = tt.tolist()
-    st = steps[-1]
+    st = steps[-1] if steps else e2e_stats[-1]
     total_bytes = nbytes * world
     total_edges = st["callsites"] * world
-    value = total_bytes / (mean_ms / 1e3) / 1e9
     e2e = total_bytes / (e2e_ms / 1e3) / 1e9
-    # roofline: the lexing stage (K1-K3): source read once + token records written
-    lex_bytes = nbytes + 32 * st["tokens"]
-    lex_ach = lex_bytes / (statistics.mean(lex_ms) / 1e3) / 1e9
-    # per-kernel algorithmic bytes: per step
+    value = total_bytes / (mean_ms / 1e3) / 1e9 if resident else e2e
     words = nbytes // 32 + 1
     algo = {
         "lex_splice": nbytes + 4 * words,                    # source read + splice bitmap
@@ -282,23 +426,25 @@ def run_gpu_arm(a, rank, world, local):
     traffic_db = {}
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
-        traffic_db = json.loads(tf.read_text())
+        traffic_db = json.loads(tf.read_text()).get(a.config, {})
+    lex_ms = statistics.mean(s["ms_lex"] for s in steps) if steps else None
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (seeded C2 generator, paper_2309_03912_b200/synth.py; all files distinct)",
-        "config": {"workload": "C2: 10k seeded MiniCU files x ~100 KB (~1 GB) per GPU, classic, nvcc 12",
-                   "files_per_gpu": a.files, "bytes_per_gpu": nbytes, "parallelism": f"dp{world} (file shards)",
-                   "l2": "inputs (1 GB) larger than L2; no flush"},
+        "data": "synthetic (seeded generators, paper_2309_03912_b200/synth.py)",
+        "config": {"workload": W.desc, "config": a.config, "units_per_gpu": len(W.texts),
+                   "bytes_per_gpu": nbytes, "parallelism": f"dp{world} (unit shards, no data-path collective)",
+                   "l2": "inputs larger than L2; no flush", "batch_mib": a.batch_mib,
+                   "value_path": ("exs_run_device (corpus resident in HBM)" if resident
+                                  else "= e2e (streamed; the corpus exceeds one device batch)")},
         "edges_per_s": total_edges / (mean_ms / 1e3),
         "stats": {k: st[k] for k in ("tokens", "items", "functions", "instances", "callsites", "levels",
                                      "diagnostics", "retries")},
-        "stage_ms": {k: statistics.mean(s[k] for s in steps) for k in ("ms_lex", "ms_parse", "ms_sema", "ms_walk")},
-        "gpu_launches": int(sum(s["gpu_launches"] for s in steps)),
-        # achieved = algorithmic bytes of one launch / its mean launch time (CUDA
-        # events on the launching stream); traffic = measured DRAM bytes of one
-        # launch (ncu dram__bytes_{read,write}.sum, profiles/ncu_traffic.json)
+        "stage_ms": ({k: statistics.mean(s[k] for s in steps) for k in ("ms_lex", "ms_parse", "ms_sema", "ms_walk")}
+                     if steps else None),
+        "gpu_launches": int(sum(s["gpu_launches"] for s in steps)) if steps else int(sum(
+            s["gpu_launches"] for s in e2e_stats)),
         "roofline": ({"bound": "hbm", "achieved": per_kernel[dom].get("achieved_gbs"),
                       "peak": HBM_PEAK, "unit": "GB/s", "frac": per_kernel[dom].get("frac"),
                       "traffic": traffic_db.get(dom, {}).get("dram_bytes_per_launch"),
@@ -308,19 +454,59 @@ def run_gpu_arm(a, rank, world, local):
                       "share_of_step": per_kernel[dom]["share"], "peak_source": HBM_PEAK_SRC,
                       "traffic_source": traffic_db.get(dom, {}).get("source")}
                      if dom else None),
-        "roofline_lex_stage": {"bound": "hbm", "achieved": lex_ach, "peak": HBM_PEAK, "unit": "GB/s",
-                               "frac": lex_ach / HBM_PEAK, "kernel": "lex stage K1-K3 (all launches)"},
+        "roofline_lex_stage": ({"bound": "hbm", "achieved": (nbytes + 32 * st["tokens"]) / (lex_ms / 1e3) / 1e9,
+                                "peak": HBM_PEAK, "unit": "GB/s",
+                                "frac": (nbytes + 32 * st["tokens"]) / (lex_ms / 1e3) / 1e9 / HBM_PEAK,
+                                "kernel": "lex stage K1-K3 (all launches)"} if lex_ms else None),
         "kernels": per_kernel,
-        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": int(nbytes),
-                "d2h_bytes_per_step": int(d2h_b)},
-        "clocks": clk.summary(),
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": int(nbytes), "d2h_bytes_per_step": d2h_b,
+                "path": "exspace.analyze_corpus(units: list[(path, str)]) -> list[Analysis] (lazy Diagnostics)",
+                "ms_per_step": e2e_ms, "batches": int(e2e_stats[-1]["batches"]),
+                "device_ms_per_step": statistics.mean(s["ms_total"] for s in e2e_stats)},
+        "clocks": clk_sum,
     }
+    if rank == 0 and not a.no_parity:
+        procs = os.cpu_count() or 8
+        if a.config in ("c2", "c5"):
+            nunits = len(W.texts)
+            idx = sorted({(k * 7919) % nunits for k in range(a.parity_files)})
+        else:
+            idx = [0] if a.config == "c3" else []
+        if idx:
+            line["parity"] = parity_sample(res, W.texts, idx, mode, procs)
+        if a.config == "c5":
+            # units that share a pool text must report the same diagnostics
+            rows = lambda k: [(d.code, d.loc.line, d.loc.col, d.message) for d in res[k].diagnostics]  # noqa: E731
+            same = all(rows(k) == rows(k % W.pool) for k in range(W.pool, len(W.texts), max(1, len(W.texts) // 97)))
+            line["parity"]["repeats_consistent"] = same
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        r = cpu_reference(max(cores * 16, 64), a.file_bytes, 50_000, cores)
-        line["cpu_baseline"] = {"value": r["gbs"], "unit": "GB/s", "cores": cores, "kind": "port",
-                                "sample": f"{r['files']} C2 files ({r['bytes'] / 1e6:.1f} MB), "
-                                          f"oracle/exs_oracle.py on {cores} processes, {r['seconds']:.1f} s"}
+        if a.config in ("c2", "c5"):
+            sample = W.texts[: max(cores * 8, 64)]
+            r = cpu_reference(sample, mode, cores)
+            r1 = cpu_reference(W.texts[:2], mode, 1)
+            line["cpu_baseline"] = {
+                "value": r["gbs"], "unit": "GB/s", "cores": cores, "kind": reference_kind(),
+                "sample": f"the first {r['files']} timed files ({r['bytes'] / 1e6:.1f} MB), "
+                          f"reference package exspace.analyze (baseline/_ref) on {cores} processes, "
+                          f"{r['seconds']:.1f} s",
+                "one_core_gbs": r1["gbs"]}
+        elif a.config == "c4":
+            small = synth.gen_callgraph(100_000, 10, 7)
+            r = cpu_reference([small], mode, 1)
+            line["cpu_baseline"] = {
+                "value": r["gbs"], "unit": "GB/s", "cores": 1, "kind": reference_kind(),
+                "sample": f"one unit of 100k functions x 10 calls ({r['bytes'] / 1e6:.1f} MB), reference on 1 core, "
+                          f"{r['seconds']:.1f} s; linear extrapolation to 10M functions: "
+                          f"{r['seconds'] * a.c4_funcs / 100_000:.0f} s",
+                "edges_per_s": r["edges_per_s"]}
+        else:
+            small = synth.gen_chain(64, 512)
+            r = cpu_reference([small], mode, 1)
+            line["cpu_baseline"] = {
+                "value": r["gbs"], "unit": "GB/s", "cores": 1, "kind": reference_kind(),
+                "sample": f"one unit of 64-deep chains over 512 structs, reference on 1 core, {r['seconds']:.1f} s",
+                "edges_per_s": r["edges_per_s"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -334,10 +520,24 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--files", type=int, default=10_000)
     ap.add_argument("--file-bytes", type=int, default=100_000)
+    ap.add_argument("--batch-mib", type=int, default=256)
+    ap.add_argument("--c3-structs", type=int, default=10_300)
+    ap.add_argument("--c4-funcs", type=int, default=10_000_000)
+    ap.add_argument("--c5-gb", type=float, default=8.0)
+    ap.add_argument("--c5-pool", type=int, default=2000)
+    ap.add_argument("--parity-files", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     a = ap.parse_args()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}",
+               str(Path(__file__).resolve())] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank, world, local = dist_env()
     if a.impl == "reference":
         run_reference_arm(a, rank, world)

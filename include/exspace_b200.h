@@ -52,6 +52,8 @@ typedef struct {
   uint64_t functions, structs, instances, edges, callsites, levels, diagnostics;
   uint64_t retries, gpu_launches;
   float ms_lex, ms_parse, ms_sema, ms_walk, ms_total, ms_h2d, ms_d2h;
+  float ms_wall;      /* exs_run_units: host wall time of the whole call     */
+  uint32_t batches;   /* exs_run_units: batches the units were analysed in   */
 } exs_stats;
 
 /* per (file, pass) preprocessing / lexing status, pass 0 host, 1 device */
@@ -146,8 +148,39 @@ int exs_run(exs_handle h, const uint8_t* bytes, uint64_t n_bytes, const uint64_t
 int exs_run_device(exs_handle h, const uint8_t* d_bytes, uint64_t n_bytes,
                    const uint64_t* file_off, uint32_t n_files, const uint8_t* file_cfg);
 
+/* Analyse n_units units given as (text, length) pairs in HOST memory -- the
+ * reference's analyze(text, path, profile, mode, cfg) (spacecheck.py:687-739)
+ * over a corpus (corpus.py:163-175, cli.py:82-91), unit_cfg[u] the
+ * configuration byte of unit u.  Any total size: units are cut into batches
+ * of <= the batch capacity (option 7); batch k+1 is packed into page-locked
+ * memory and copied to the device while batch k is analysed.  One unit must
+ * be smaller than 2 GiB.  Results: exs_results_view. */
+int exs_run_units(exs_handle h, const char* const* texts, const uint64_t* lens, uint64_t n_units,
+                  const uint8_t* unit_cfg);
+
+/* One finished diagnostic (diagnostics.py:40-62 Diagnostic): unit index,
+ * 1-based line and column, code (1=E0001 .. 20=W1502, 21 = out-of-contract
+ * marker X9999), suppressed flag, and its message: msg_len bytes of UTF-8
+ * (surrogateescape for invalid input bytes) at text + msg_off. */
+typedef struct {
+  uint32_t unit, line, col, msg_len;
+  uint64_t msg_off;
+  uint16_t code;
+  uint8_t suppressed, pad[5];
+} exs_result;
+
+/* Results of the last run (exs_run_units, exs_run or exs_run_device): the
+ * ordered, de-duplicated diagnostics of every unit (finish_diagnostics,
+ * diagnostics.py:116-121: unit, then (line, col, code, message)), suppressed
+ * ones included.  Unit u owns records [unit_first[u], unit_first[u+1]).  All
+ * pointers are owned by the handle (page-locked) and valid until its next
+ * run or exs_destroy. */
+int exs_results_view(exs_handle h, const exs_result** recs, uint64_t* n, const char** text,
+                     uint64_t* text_bytes, const uint64_t** unit_first, uint64_t* n_units);
+
 int exs_get_stats(exs_handle h, exs_stats* out);
-/* diagnostics ordered by (file, line, col, code), duplicates removed */
+/* raw records ordered by (file, line, col, code), duplicates removed (only
+ * kept with option 6; the rendered form is exs_results_view) */
 int exs_get_diags(exs_handle h, exs_diag* out, uint64_t cap, uint64_t* n);
 /* Zero-copy view of the ordered diagnostics of the last run: *out points to
  * *n records in page-locked host memory owned by the handle, valid until the
@@ -164,7 +197,10 @@ int exs_describe(exs_handle h, const uint32_t* ids, const uint8_t* kinds, uint32
  * 4 = ordered selections of at least this many indices use a flag pass +
  *     flagged compaction (default 4M; 0 forces it, for the parity tests);
  * 5 = nonzero: order diagnostics by two radix sorts ((col, code) then (file, line))
- *     instead of one packed (file, line, col, code) key (for the parity tests) */
+ *     instead of one packed (file, line, col, code) key (for the parity tests);
+ * 6 = nonzero: also keep the raw records (exs_get_diags / exs_diags_view);
+ * 7 = exs_run_units batch capacity in MiB (default 1024, at most 2047);
+ * 8 = host threads packing a batch into page-locked memory (0 = automatic) */
 int exs_set_option(exs_handle h, int key, int value);
 /* with EXS_PROFILE=1 in the environment: per-launch-site device times of the last run */
 const char* exs_profile_text(void);

@@ -48,7 +48,8 @@ class Stats(C.Structure):
         "bytes", "files", "lines", "directives", "tokens", "views", "view_tokens", "items",
         "functions", "structs", "instances", "edges", "callsites", "levels", "diagnostics",
         "retries", "gpu_launches")] + [(n, C.c_float) for n in (
-        "ms_lex", "ms_parse", "ms_sema", "ms_walk", "ms_total", "ms_h2d", "ms_d2h")]
+        "ms_lex", "ms_parse", "ms_sema", "ms_walk", "ms_total", "ms_h2d", "ms_d2h", "ms_wall")] + [
+        ("batches", C.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -59,8 +60,45 @@ EXPORTS = [
     "exs_get_diags", "exs_diags_view", "exs_get_arena", "exs_get_pass_status", "exs_get_tokens",
     "exs_get_walk_stats", "exs_describe", "exs_set_option", "exs_stage_times", "exs_profile_text",
     "exs_get_decls", "exs_get_structs", "exs_get_instances", "exs_get_edges", "exs_get_nodes",
-    "exs_get_token_range",
+    "exs_get_token_range", "exs_run_units", "exs_results_view",
 ]
+
+# one finished diagnostic (include/exspace_b200.h exs_result)
+RESULT_DTYPE = np.dtype([("unit", "<u4"), ("line", "<u4"), ("col", "<u4"), ("msg_len", "<u4"),
+                         ("msg_off", "<u8"), ("code", "<u2"), ("suppressed", "u1"), ("pad", "u1", (5,))])
+assert RESULT_DTYPE.itemsize == 32
+
+_AS_UTF8 = C.pythonapi.PyUnicode_AsUTF8AndSize
+_AS_UTF8.argtypes = [C.py_object, C.POINTER(C.c_ssize_t)]
+_AS_UTF8.restype = C.c_void_p
+
+
+def text_pointers(texts):
+    """(pointer array, length array, keep-alive list) for a list of str/bytes
+    without copying them: a str's UTF-8 form is CPython's own buffer (the
+    string's data for ASCII text); text with lone surrogates is encoded with
+    surrogateescape (the reference's byte view of such input)."""
+    n = len(texts)
+    ptrs = np.zeros(n, dtype=np.uint64)
+    lens = np.zeros(n, dtype=np.uint64)
+    keep = []
+    size = C.c_ssize_t()
+    for i, t in enumerate(texts):
+        if isinstance(t, str):
+            try:
+                p = _AS_UTF8(t, C.byref(size))
+                ptrs[i] = p or 0
+                lens[i] = size.value
+                continue
+            except UnicodeEncodeError:
+                t = t.encode("utf-8", "surrogateescape")
+        b = bytes(t)
+        keep.append(b)
+        cp = C.c_char_p(b)
+        keep.append(cp)
+        ptrs[i] = C.cast(cp, C.c_void_p).value or 0
+        lens[i] = len(b)
+    return ptrs, lens, keep
 
 
 DECL_DTYPE = np.dtype([("node", "<u4"), ("view", "<u4"), ("rec", "<u4"), ("order", "<u4"),
@@ -106,6 +144,9 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     lib.exs_describe.argtypes = [vp, vp, vp, C.c_uint32, vp]
     lib.exs_set_option.argtypes = [vp, C.c_int, C.c_int]
     lib.exs_stage_times.argtypes = [vp, C.POINTER(C.c_float)]
+    lib.exs_run_units.argtypes = [vp, vp, vp, C.c_uint64, vp]
+    lib.exs_results_view.argtypes = [vp, C.POINTER(C.c_void_p), u64p, C.POINTER(C.c_void_p), u64p,
+                                     C.POINTER(C.c_void_p), u64p]
     for name in EXPORTS:
         if name not in ("exs_last_error", "exs_profile_text"):
             getattr(lib, name).restype = C.c_int
@@ -156,6 +197,34 @@ class Handle:
         cfg = np.ascontiguousarray(cfg, dtype=np.uint8)
         self._check(self.lib.exs_run_device(self.h, C.c_void_p(dev_ptr), n_bytes, _ptr(offsets),
                                             len(offsets) - 1, _ptr(cfg)))
+
+    def run_units(self, texts, cfg: np.ndarray):
+        """Analyse units given as str/bytes (exs_run_units: streamed batches)."""
+        ptrs, lens, keep = text_pointers(texts)
+        cfg = np.ascontiguousarray(cfg, dtype=np.uint8)
+        self._check(self.lib.exs_run_units(self.h, _ptr(ptrs), _ptr(lens), len(ptrs), _ptr(cfg)))
+        del keep
+
+    def results(self, copy: bool = True):
+        """(records, message bytes, unit_first) of the last run.  copy=False
+        returns views of the handle's page-locked buffers, valid until its
+        next run."""
+        rp, tp, up = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        n, tb, nu = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._check(self.lib.exs_results_view(self.h, C.byref(rp), C.byref(n), C.byref(tp), C.byref(tb),
+                                              C.byref(up), C.byref(nu)))
+
+        def view(ptr, nbytes):
+            if not nbytes:
+                return np.zeros(0, dtype=np.uint8)
+            return np.frombuffer((C.c_uint8 * nbytes).from_address(ptr.value), dtype=np.uint8)
+
+        recs = view(rp, n.value * RESULT_DTYPE.itemsize)
+        text = view(tp, tb.value)
+        first = view(up, (nu.value + 1) * 8) if up.value else np.zeros(8, dtype=np.uint8)
+        if copy:
+            recs, text, first = recs.copy(), text.copy(), first.copy()
+        return recs.view(RESULT_DTYPE), text, first.view(np.uint64)
 
     def stats(self) -> dict:
         s = Stats()

@@ -132,7 +132,16 @@ enum Code : u16 {
   C_E1302, C_E1401, C_E1501, C_W1502, C_X9999
 };
 
-// message templates; rendered on the host by paper_2309_03912_b200/messages.py
+// Position of a code in the reference's order, which compares the code
+// STRINGS (Diagnostic.sort_key, diagnostics.py:73-74): every E code sorts
+// before W1101/W1102/W1502, so the enum value is not the order.
+EXS_HD inline u32 code_rank(u32 c) {
+  // E0001..E1004 keep their values; E1101..E1501 follow; then W1101, W1102, W1502, X9999
+  return c <= C_E1004 ? c : (c >= C_E1101 && c <= C_E1501) ? c - 2 : (c == C_W1101 || c == C_W1102) ? c + 7 : c;
+}
+
+// message templates; rendered on the GPU by exs_render.cuh (and by
+// paper_2309_03912_b200/messages.py for the walk-key renderer)
 enum Msg : u16 {
   M_NONE = 0,
   // preprocessor (preprocess.py:177-202) -- a0: text-arena span

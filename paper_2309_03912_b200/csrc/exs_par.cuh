@@ -288,6 +288,20 @@ inline void excl_scan_u32(const u32* in, u32* out, i64 n, Scratch& sc, cudaStrea
 #endif
 }
 
+inline void excl_scan_u64(const u64* in, u64* out, i64 n, Scratch& sc, cudaStream_t s) {
+  if (n <= 0) return;
+#ifndef EXS_EMU
+  size_t tb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, s));
+  CK(cub::DeviceScan::ExclusiveSum(sc.get(tb), tb, in, out, (int)n, s));
+  g_launches += 2;
+#else
+  (void)sc; (void)s;
+  u64 acc = 0;
+  for (i64 i = 0; i < n; i++) { u64 v = in[i]; out[i] = acc; acc += v; }
+#endif
+}
+
 template <class T, class Op>
 void incl_scan(const T* in, T* out, i64 n, Op op, Scratch& sc, cudaStream_t s) {
   if (n <= 0) return;

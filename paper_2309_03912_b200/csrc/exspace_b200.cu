@@ -5,11 +5,12 @@
 //   K5 symbol join + resolve checks (exs_stage_sema.cuh) ->
 //   K6-K8 instantiation fixpoint, reachability, verdicts (exs_stage_walk.cuh) ->
 //   divergence (E1201) and the ordered diagnostic set (this file).
-#include "exs_stage_walk.cuh"
+#include "exs_render.cuh"
 #include "../../include/exspace_b200.h"
 #include <chrono>
 #include <map>
 #include <mutex>
+#include <thread>
 
 namespace exs {
 #ifndef EXS_EMU
@@ -141,6 +142,46 @@ u64 g_launches = 0;
 
 static thread_local std::string g_err;
 
+// page-locked host buffer that grows geometrically, keeping its contents
+struct PinnedBuf {
+  u8* p = nullptr;
+  u64 cap = 0;
+  void ensure(u64 need, u64 keep) {
+    if (need <= cap) return;
+    const u64 ncap = std::max<u64>(need, cap + cap / 2) + 4096;
+    u8* q = nullptr;
+#ifndef EXS_EMU
+    CK(cudaHostAlloc((void**)&q, ncap, cudaHostAllocDefault));
+#else
+    q = (u8*)malloc(ncap);
+    if (!q) throw Err("out of host memory");
+#endif
+    if (keep) memcpy(q, p, keep);
+    release();
+    p = q;
+    cap = ncap;
+  }
+  void release() {
+#ifndef EXS_EMU
+    if (p) cudaFreeHost(p);
+#else
+    free(p);
+#endif
+    p = nullptr;
+    cap = 0;
+  }
+  ~PinnedBuf() { release(); }
+};
+
+// one rendered, finished diagnostic (include/exspace_b200.h exs_result)
+struct ResRec {
+  u32 unit, line, col, msg_len;
+  u64 msg_off;
+  u16 code;
+  u8 suppressed, pad[5];
+};
+static_assert(sizeof(ResRec) == 32, "result record is 32 bytes");
+
 struct Handle {
   int device = 0;
   cudaStream_t st = 0;
@@ -168,6 +209,22 @@ struct Handle {
   u32 split_min = 16;  // statement-parallel body parsing threshold (tokens; C2 1 GB best)
   long long select_flagged_min = EXS_SELECT_FLAGGED_MIN;  // select_idx flag-pass threshold (indices)
   bool diag_sort_two_pass = false;  // force the two-key diagnostic sort (parity tests)
+  bool keep_records = false;        // also keep the raw records (exs_get_diags / exs_diags_view)
+  // rendered results of the last run (all its batches), in unit order
+  PinnedBuf res, text;
+  u64 n_res = 0, text_bytes = 0, static_bytes = 0;
+  std::vector<u64> unit_first;      // n_units + 1
+  u32* d_static = nullptr;          // per static message key: (offset, length)
+  // streaming driver (exs_run_units): two host staging slots, two device slots
+  u64 batch_cap = 1ull << 30;
+  int pack_threads = 0;             // 0: hardware threads (<= 16)
+  PinnedBuf stage[2];
+  u8* d_slot[2] = {nullptr, nullptr};
+  u64 d_slot_cap[2] = {0, 0};
+#ifndef EXS_EMU
+  cudaStream_t cst = 0;             // host-to-device copies of the next batch
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr};
+#endif
 
   void reset() {
     L.free_all(); L = LexState();
@@ -187,6 +244,18 @@ struct Handle {
     free(diags);
 #endif
     dfree(d_src_owned);
+    dfree(d_static);
+    for (int k = 0; k < 2; k++) {
+#ifndef EXS_EMU
+      if (d_slot[k]) cudaFree(d_slot[k]);
+      if (ev_h2d[k]) cudaEventDestroy(ev_h2d[k]);
+#else
+      free(d_slot[k]);
+#endif
+    }
+#ifndef EXS_EMU
+    if (cst) { cudaStreamSynchronize(cst); cudaStreamDestroy(cst); }
+#endif
     dfree(sc.p);
     sc.p = nullptr;
     sc.cap = 0;
@@ -325,9 +394,160 @@ static void run_demands(Handle& H, bool emit_e1201) {
 }
 
 // ---------------------------------------------------------------------------
+// K9: messages and finish_diagnostics (diagnostics.py:116-121), results
+
+// results of a new run: the static message section first
+static void results_reset(Handle& H, u64 n_units) {
+  if (!H.d_static) {
+    // static messages rendered once per handle, on the host, by the same code
+    std::vector<u32> tab(2 * EXS_STATIC_KEYS, 0);
+    std::string txt;
+    RenderCtx none{};
+    for (int k = 0; k < EXS_STATIC_KEYS; k++) {
+      Diag d;
+      if (!static_diag(k, d)) continue;
+      Out cnt{nullptr, 0};
+      render_message(none, d, cnt);
+      std::string m(cnt.n, '\0');
+      Out w{&m[0], 0};
+      render_message(none, d, w);
+      tab[2 * k] = (u32)txt.size();
+      tab[2 * k + 1] = (u32)m.size();
+      txt += m;
+    }
+    H.static_bytes = txt.size();
+    H.text.ensure(H.static_bytes, 0);
+    memcpy(H.text.p, txt.data(), txt.size());
+    H.d_static = dalloc<u32>(2 * EXS_STATIC_KEYS);
+    h2d(H.d_static, tab.data(), 8ull * EXS_STATIC_KEYS, H.st);
+    sync(H.st);
+  }
+  H.n_res = 0;
+  H.text_bytes = H.static_bytes;
+  H.unit_first.assign(n_units + 1, 0);
+}
+
+// Render the ordered records dd[0, nd) of one batch (units unit_base ..),
+// finish them and append them to the handle's results.
+static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u64 n_bytes, u32 n_files,
+                           u64 unit_base) {
+  cudaStream_t st = H.st;
+  if (!nd) return;
+  const RenderCtx RC{d_src, H.L.splice, H.L.arena, H.S.fns, H.S.recs, H.P.nodes, H.L.toks, H.W.inst,
+                     (u32)n_bytes};
+  const u32* stab = H.d_static;
+  u64* len = dalloc<u64>((u64)nd + 1);
+  u64* off = dalloc<u64>((u64)nd + 1);
+  EXS_TAG("render_len");
+  par_for((i64)nd + 1, [=] EXS_HD (i64 i) {
+    if (i == nd) { len[i] = 0; return; }
+    if (static_key(dd[i]) >= 0) { len[i] = 0; return; }
+    Out o{nullptr, 0};
+    render_message(RC, dd[i], o);
+    len[i] = o.n;
+  }, st);
+  excl_scan_u64(len, off, (i64)nd + 1, H.sc, st);
+  const u64 total = get1(off + nd, st);
+  char* txt = dalloc<char>(total + 1);
+  EXS_TAG("render_text");
+  par_for(nd, [=] EXS_HD (i64 i) {
+    if (!len[i]) return;
+    Out o{txt + off[i], 0};
+    render_message(RC, dd[i], o);
+  }, st);
+  // message bytes of record i, wherever they live
+  const u64 tbase = H.text_bytes;
+  auto msg_of = [=] EXS_HD (u32 i, const char*& p, u32& n, u64& glob) {
+    const int k = static_key(dd[i]);
+    if (k >= 0) { glob = stab[2 * k]; n = stab[2 * k + 1]; p = nullptr; }
+    else { glob = tbase + off[i]; n = (u32)len[i]; p = txt + off[i]; }
+  };
+  // runs of equal (file, line, col, code): order by message text (then by
+  // record order) and drop repeated messages, keeping the first
+  u32* ord = dalloc<u32>((u64)nd + 1);
+  u8* keep = dalloc<u8>((u64)nd + 1);
+  char* stxt = nullptr;  // the static section on the device (for comparisons)
+  stxt = dalloc<char>(H.static_bytes + 1);
+  h2d(stxt, H.text.p, H.static_bytes, st);
+  const char* sx = stxt;
+  EXS_TAG("finish_runs");
+  par_for(nd, [=] EXS_HD (i64 i) {
+    auto same = [&](i64 a, i64 b) {
+      return dd[a].file == dd[b].file && dd[a].line == dd[b].line && dd[a].col == dd[b].col &&
+             dd[a].code == dd[b].code;
+    };
+    if (i > 0 && same(i - 1, i)) return;  // not the head of its run
+    i64 e = i + 1;
+    while (e < (i64)nd && same(i, e)) e++;
+    for (i64 k = i; k < e; k++) ord[k] = (u32)k;
+    auto text = [&](u32 r, const char*& p, u32& n) {
+      u64 g;
+      msg_of(r, p, n, g);
+      if (!p) p = sx + g;
+    };
+    auto less = [&](u32 a, u32 b) {
+      const char* pa; const char* pb; u32 na, nb;
+      text(a, pa, na); text(b, pb, nb);
+      const int c = msg_cmp(pa, na, pb, nb);
+      return c ? c < 0 : a < b;
+    };
+    const i64 n = e - i;
+    if (n > 1) {
+      // shell sort (runs are short; no scratch)
+      for (i64 gap = n / 2; gap > 0; gap /= 2)
+        for (i64 k = gap; k < n; k++) {
+          const u32 v = ord[i + k];
+          i64 j = k;
+          while (j >= gap && less(v, ord[i + j - gap])) { ord[i + j] = ord[i + j - gap]; j -= gap; }
+          ord[i + j] = v;
+        }
+    }
+    keep[i] = 1;
+    for (i64 k = i + 1; k < e; k++) {
+      const char* pa; const char* pb; u32 na, nb;
+      text(ord[k - 1], pa, na); text(ord[k], pb, nb);
+      keep[k] = msg_cmp(pa, na, pb, nb) != 0;
+    }
+  }, st);
+  u32* kidx = dalloc<u32>((u64)nd + 1);
+  const u8* kp = keep;
+  const u32 nk = select_idx(nd, [=] EXS_HD (u32 k) -> bool { return kp[k] != 0; }, kidx, H.L.cnt, H.sc, st);
+  ResRec* rr = dalloc<ResRec>((u64)nk + 1);
+  u32* fcnt = dalloc<u32>((u64)n_files + 1);
+  dzero(fcnt, 4ull * (n_files + 1), st);
+  EXS_TAG("results");
+  par_for(nk, [=] EXS_HD (i64 j) {
+    const u32 x = ord[kidx[j]];
+    const Diag& d = dd[x];
+    ResRec r;
+    const char* p; u32 n; u64 g;
+    msg_of(x, p, n, g);
+    r.unit = (u32)(unit_base + d.file); r.line = d.line; r.col = d.col; r.msg_len = n; r.msg_off = g;
+    r.code = d.code; r.suppressed = d.suppressed;
+    for (int q = 0; q < 5; q++) r.pad[q] = 0;
+    rr[j] = r;
+    at_add(&fcnt[d.file], 1);
+  }, st);
+  H.res.ensure((H.n_res + nk) * sizeof(ResRec), H.n_res * sizeof(ResRec));
+  H.text.ensure(H.text_bytes + total, H.text_bytes);
+  std::vector<u32> fc(n_files);
+  d2h(H.res.p + H.n_res * sizeof(ResRec), rr, (u64)nk * sizeof(ResRec), st);
+  if (total) d2h(H.text.p + H.text_bytes, txt, total, st);
+  d2h(fc.data(), fcnt, 4ull * n_files, st);
+  sync(st);
+  for (u32 f = 0; f < n_files; f++) H.unit_first[unit_base + f + 1] = fc[f];
+  H.n_res += nk;
+  H.text_bytes += total;
+  dfree(len); dfree(off); dfree(txt); dfree(ord); dfree(keep); dfree(stxt); dfree(kidx); dfree(rr); dfree(fcnt);
+}
+
+// unit_first: per-unit counts -> first result index per unit
+static void results_close(Handle& H) {
+  for (u64 u = 0; u + 1 < H.unit_first.size(); u++) H.unit_first[u + 1] += H.unit_first[u];
+}
 
 static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, u32 n_files,
-                      const u8* cfg) {
+                      const u8* cfg, u64 unit_base) {
   if (n_bytes >= (1ull << 31)) throw Err("batch larger than 2 GiB; split into batches");
   cudaStream_t st = H.st;
   H.reset();
@@ -467,7 +687,8 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       if (ct[f]) emit_diag(B, mkdiag((u32)f, 1, 1, C_X9999, M_X_CONTRACT));
     }, st);
   }
-  // order diagnostics by (file, line, col, code) with two stable radix passes
+  // order diagnostics by (file, line, col, code string) -- one radix sort of a
+  // packed key, or two stable passes when the fields exceed 64 bits
   u32 nd = std::min(get1(H.d_ndiags, st), H.cap_diags + n_files);
   {
     u64* k = dalloc<u64>(nd + 1);
@@ -480,7 +701,7 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     par_for(T, [=] EXS_HD (i64 t) {
       u32 o[4] = {0, 0, 0, 0};
       for (i64 i = t; i < (i64)nd; i += T) {
-        o[0] |= dd[i].file; o[1] |= dd[i].line; o[2] |= dd[i].col; o[3] |= dd[i].code;
+        o[0] |= dd[i].file; o[1] |= dd[i].line; o[2] |= dd[i].col; o[3] |= code_rank(dd[i].code);
       }
       for (int q = 0; q < 4; q++) {
 #if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
@@ -500,18 +721,21 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       const int sl = bk + bc, sf = bk + bc + bl;
       par_for(nd, [=] EXS_HD (i64 i) {
         ix[i] = (u32)i;
-        k[i] = (sf < 64 ? (u64)dd[i].file << sf : 0) | ((u64)dd[i].line << sl) | ((u64)dd[i].col << bk) | dd[i].code;
+        k[i] = (sf < 64 ? (u64)dd[i].file << sf : 0) | ((u64)dd[i].line << sl) | ((u64)dd[i].col << bk) | code_rank(dd[i].code);
       }, st);
       sort_pairs(k, ix, nd, H.sc, st, std::max(1, bf + bl + bc + bk));
     } else {
-      par_for(nd, [=] EXS_HD (i64 i) { ix[i] = (u32)i; k[i] = ((u64)dd[i].col << 16) | dd[i].code; }, st);
+      par_for(nd, [=] EXS_HD (i64 i) { ix[i] = (u32)i; k[i] = ((u64)dd[i].col << 16) | code_rank(dd[i].code); }, st);
       sort_pairs(k, ix, nd, H.sc, st, 48);
       par_for(nd, [=] EXS_HD (i64 i) { k[i] = ((u64)dd[ix[i]].file << 32) | dd[ix[i]].line; }, st);
       sort_pairs(k, ix, nd, H.sc, st);
     }
     Diag* out = dalloc<Diag>(nd + 1);
     par_for(nd, [=] EXS_HD (i64 i) { out[i] = dd[ix[i]]; }, st);
-    if ((u64)nd > H.diags_host_cap) {
+    Timer td(st);
+    render_results(H, out, nd, d_src, n_bytes, n_files, unit_base);
+    H.n_diags_host = 0;
+    if (H.keep_records && (u64)nd > H.diags_host_cap) {
       u64 cap = (u64)nd + nd / 4 + 1024;
 #ifndef EXS_EMU
       if (H.diags) cudaFreeHost(H.diags);
@@ -522,9 +746,10 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
 #endif
       H.diags_host_cap = cap;
     }
-    H.n_diags_host = nd;
-    Timer td(st);
-    if (nd) d2h(H.diags, out, sizeof(Diag) * (u64)nd, st);
+    if (H.keep_records) {
+      H.n_diags_host = nd;
+      if (nd) d2h(H.diags, out, sizeof(Diag) * (u64)nd, st);
+    }
     sync(st);
     H.stats.ms_d2h = td.stop();
     dfree(out); dfree(k); dfree(ix);
@@ -559,6 +784,8 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
   s.ms_lex = H.t_stage[0]; s.ms_parse = H.t_stage[1]; s.ms_sema = H.t_stage[2]; s.ms_walk = H.t_stage[3];
   s.ms_total = total.stop();
   s.gpu_launches = g_launches - launches0;
+  s.ms_wall = s.ms_total;
+  s.batches = 1;
 #ifndef EXS_EMU
   collect_profile();
 #endif
@@ -633,7 +860,9 @@ int exs_run(exs_handle x, const uint8_t* bytes, uint64_t n_bytes, const uint64_t
   dzero(H.d_src_owned + n_bytes, 64, H.st);
   sync(H.st);
   float ms_h2d = th.stop();
-  run_batch(H, H.d_src_owned, n_bytes, file_off, n_files, file_cfg);
+  results_reset(H, n_files);
+  run_batch(H, H.d_src_owned, n_bytes, file_off, n_files, file_cfg, 0);
+  results_close(H);
   H.stats.ms_h2d = ms_h2d;
   API_END
 }
@@ -646,8 +875,179 @@ int exs_run_device(exs_handle x, const uint8_t* d_bytes, uint64_t n_bytes, const
 #ifndef EXS_EMU
   CK(cudaSetDevice(H.device));
 #endif
-  run_batch(H, d_bytes, n_bytes, file_off, n_files, file_cfg);
+  results_reset(H, n_files);
+  run_batch(H, d_bytes, n_bytes, file_off, n_files, file_cfg, 0);
+  results_close(H);
   H.stats.ms_h2d = 0;
+  API_END
+}
+
+// ---- streaming driver: any number of units in batches of <= batch_cap bytes;
+// batch k+1 is packed into page-locked memory and copied to the device while
+// batch k is analysed
+
+static void pack_units(const char* const* texts, const uint64_t* lens, u64 u0, u64 u1, const u64* uoff,
+                       u8* dst, int nthreads) {
+  // byte-balanced ranges over the concatenation of units [u0, u1)
+  const u64 total = uoff[u1 - u0];
+  const u64 per = (total + nthreads - 1) / std::max(1, nthreads);
+  auto work = [=](u64 lo, u64 hi) {
+    if (lo >= hi) return;
+    // first unit overlapping lo
+    u64 a = 0, b = u1 - u0;
+    while (b - a > 1) { const u64 m = (a + b) / 2; if (uoff[m] <= lo) a = m; else b = m; }
+    for (u64 k = a; k < u1 - u0 && uoff[k] < hi; k++) {
+      const u64 s0 = std::max(lo, uoff[k]), s1 = std::min(hi, uoff[k + 1]);
+      if (s1 > s0) memcpy(dst + s0, texts[u0 + k] + (s0 - uoff[k]), s1 - s0);
+    }
+  };
+  if (nthreads <= 1 || total < (8u << 20)) { work(0, total); return; }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; t++) th.emplace_back(work, (u64)t * per, std::min(total, (u64)(t + 1) * per));
+  for (auto& t : th) t.join();
+}
+
+static void ensure_slot(Handle& H, int k, u64 bytes) {
+  if (H.d_slot_cap[k] >= bytes) return;
+#ifndef EXS_EMU
+  if (H.d_slot[k]) { CK(cudaStreamSynchronize(H.st)); CK(cudaFree(H.d_slot[k])); }
+  H.d_slot[k] = nullptr;
+  CK(cudaMalloc((void**)&H.d_slot[k], bytes));
+#else
+  free(H.d_slot[k]);
+  H.d_slot[k] = (u8*)malloc(bytes);
+#endif
+  H.d_slot_cap[k] = bytes;
+}
+
+struct BatchPlan {
+  u64 u0, u1, bytes;
+  std::vector<u64> off;  // unit offsets within the batch (u1 - u0 + 1)
+};
+
+static void run_units(Handle& H, const char* const* texts, const uint64_t* lens, u64 n_units, const u8* cfg) {
+  if (n_units >= 0xFFFFFFFFull) throw Err("too many units");
+  // plan
+  std::vector<BatchPlan> plan;
+  {
+    BatchPlan cur{0, 0, 0, {0}};
+    for (u64 u = 0; u < n_units; u++) {
+      const u64 n = lens[u];
+      if (n >= (1ull << 31) - 64) throw Err("a unit larger than 2 GiB is outside the contract");
+      if (cur.u1 > cur.u0 && (cur.bytes + n > H.batch_cap || cur.u1 - cur.u0 >= (1u << 26))) {
+        plan.push_back(cur);
+        cur = BatchPlan{u, u, 0, {0}};
+      }
+      cur.bytes += n;
+      cur.off.push_back(cur.bytes);
+      cur.u1 = u + 1;
+    }
+    if (cur.u1 > cur.u0 || plan.empty()) plan.push_back(cur);
+  }
+  u64 maxb = 0;
+  for (auto& b : plan) maxb = std::max(maxb, b.bytes);
+  const int nslots = plan.size() > 1 ? 2 : 1;
+  for (int k = 0; k < nslots; k++) {
+    H.stage[k].ensure(maxb + 64, 0);
+    ensure_slot(H, k, maxb + 64);
+  }
+#ifndef EXS_EMU
+  if (!H.cst) CK(cudaStreamCreateWithFlags(&H.cst, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; k++)
+    if (!H.ev_h2d[k]) CK(cudaEventCreateWithFlags(&H.ev_h2d[k], cudaEventDisableTiming));
+#endif
+  const int nthreads = H.pack_threads > 0 ? H.pack_threads
+                                          : (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
+  const int dev = H.device;
+  // pack batch b into slot k and queue its copy (any thread)
+  static const bool trace = getenv("EXS_TRACE_UNITS") != nullptr;
+  const auto tz = std::chrono::steady_clock::now();
+  auto ms_since = [tz]() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tz).count();
+  };
+  auto prep = [&H, &plan, texts, lens, nthreads, dev, ms_since](size_t b, int k) {
+    const BatchPlan& P = plan[b];
+    const double a0 = ms_since();
+    pack_units(texts, lens, P.u0, P.u1, P.off.data(), H.stage[k].p, nthreads);
+    if (trace) fprintf(stderr, "[run_units] batch %zu packed %.1f MB at %.1f..%.1f ms\n", b, P.bytes / 1e6, a0, ms_since());
+    memset(H.stage[k].p + P.bytes, 0, 64);
+#ifndef EXS_EMU
+    CK(cudaSetDevice(dev));
+    CK(cudaMemcpyAsync(H.d_slot[k], H.stage[k].p, P.bytes + 64, cudaMemcpyHostToDevice, H.cst));
+    CK(cudaEventRecord(H.ev_h2d[k], H.cst));
+#else
+    (void)dev;
+    memcpy(H.d_slot[k], H.stage[k].p, P.bytes + 64);
+#endif
+  };
+  results_reset(H, n_units);
+  exs_stats acc{};
+  float t_stage[4] = {0, 0, 0, 0};
+  auto t0 = std::chrono::steady_clock::now();
+  prep(0, 0);
+  for (size_t b = 0; b < plan.size(); b++) {
+    const int k = (int)(b & 1);
+    std::thread next;
+    std::string next_err;
+    if (b + 1 < plan.size()) {
+      next = std::thread([&, b]() {
+        try { prep(b + 1, (int)((b + 1) & 1)); } catch (const std::exception& e) { next_err = e.what(); }
+      });
+    }
+    try {
+#ifndef EXS_EMU
+      CK(cudaStreamWaitEvent(H.st, H.ev_h2d[k], 0));
+#endif
+      const BatchPlan& P = plan[b];
+      const double r0 = ms_since();
+      run_batch(H, H.d_slot[k], P.bytes, P.off.data(), (u32)(P.u1 - P.u0), cfg + P.u0, P.u0);
+      if (trace) fprintf(stderr, "[run_units] batch %zu analysed at %.1f..%.1f ms (device %.1f ms)\n", b, r0,
+                         ms_since(), H.stats.ms_total);
+    } catch (...) {
+      if (next.joinable()) next.join();
+      throw;
+    }
+    if (next.joinable()) next.join();
+    if (!next_err.empty()) throw Err(next_err);
+    const exs_stats& s = H.stats;
+    acc.bytes += s.bytes; acc.files += s.files; acc.lines += s.lines; acc.directives += s.directives;
+    acc.tokens += s.tokens; acc.views += s.views; acc.view_tokens += s.view_tokens; acc.items += s.items;
+    acc.functions += s.functions; acc.structs += s.structs; acc.instances += s.instances;
+    acc.edges += s.edges; acc.callsites += s.callsites; acc.levels = std::max(acc.levels, s.levels);
+    acc.diagnostics += s.diagnostics; acc.retries += s.retries; acc.gpu_launches += s.gpu_launches;
+    acc.ms_lex += s.ms_lex; acc.ms_parse += s.ms_parse; acc.ms_sema += s.ms_sema; acc.ms_walk += s.ms_walk;
+    acc.ms_total += s.ms_total; acc.ms_d2h += s.ms_d2h;
+    for (int q = 0; q < 4; q++) t_stage[q] += H.t_stage[q];
+  }
+  results_close(H);
+  acc.batches = plan.size();
+  acc.ms_wall = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  H.stats = acc;
+  for (int q = 0; q < 4; q++) H.t_stage[q] = t_stage[q];
+}
+
+int exs_run_units(exs_handle x, const char* const* texts, const uint64_t* lens, uint64_t n_units,
+                  const uint8_t* unit_cfg) {
+  API_TRY
+  Handle& H = x->h;
+  bind_stream(H);
+#ifndef EXS_EMU
+  CK(cudaSetDevice(H.device));
+#endif
+  run_units(H, texts, lens, n_units, unit_cfg);
+  API_END
+}
+
+int exs_results_view(exs_handle x, const exs_result** recs, uint64_t* n, const char** text,
+                     uint64_t* text_bytes, const uint64_t** unit_first, uint64_t* n_units) {
+  API_TRY
+  const Handle& H = x->h;
+  *recs = reinterpret_cast<const exs_result*>(H.res.p);
+  *n = H.n_res;
+  *text = reinterpret_cast<const char*>(H.text.p);
+  *text_bytes = H.text_bytes;
+  *unit_first = H.unit_first.data();
+  *n_units = H.unit_first.empty() ? 0 : H.unit_first.size() - 1;
   API_END
 }
 
@@ -666,6 +1066,9 @@ int exs_set_option(exs_handle x, int key, int value) {
   else if (key == 3) x->h.split_min = value < 4 ? 4u : (u32)value;  // statement-split threshold (tokens)
   else if (key == 4) x->h.select_flagged_min = value < 0 ? 0 : value;  // flag-pass selection threshold
   else if (key == 5) x->h.diag_sort_two_pass = value != 0;  // diagnostic order by two sorts
+  else if (key == 6) x->h.keep_records = value != 0;        // keep raw records (exs_get_diags)
+  else if (key == 7) x->h.batch_cap = (u64)std::min(2047, std::max(1, value)) << 20;  // batch MiB
+  else if (key == 8) x->h.pack_threads = value;               // host packing threads (0 = auto)
   else throw Err("unknown option");
   API_END
 }

@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native
 from .walks import GLOBAL, BatchWalks, StructInfo
-from .messages import CODES, Renderer, stray_text
+from .messages import CODES, Renderer, stray_text  # noqa: F401  (stray_text re-exported)
 
 
 # ---------------------------------------------------------------------------
@@ -273,17 +273,74 @@ class WalkSummary:
         return self._get(2)
 
 
-@dataclass
+class CorpusResults:
+    """Columnar results of one run: the finished diagnostic records of every
+    unit (include/exspace_b200.h exs_result, rendered and ordered natively)
+    and their message bytes.  Diagnostic objects are built per unit on first
+    access (a corpus of 1 GB has ~4M diagnostics)."""
+
+    def __init__(self, recs: np.ndarray, text: np.ndarray, unit_first: np.ndarray, paths: list):
+        self.recs = recs
+        self.text = text
+        self.unit_first = unit_first
+        self.paths = paths
+
+    def n_diagnostics(self, unit: int) -> int:
+        return int(self.unit_first[unit + 1] - self.unit_first[unit])
+
+    def diagnostics(self, unit: int) -> list:
+        lo, hi = int(self.unit_first[unit]), int(self.unit_first[unit + 1])
+        if lo == hi:
+            return []
+        r = self.recs[lo:hi]
+        path = self.paths[unit]
+        tx = self.text
+        out = []
+        for line, col, code, sup, off, ln in zip(r["line"].tolist(), r["col"].tolist(), r["code"].tolist(),
+                                                 r["suppressed"].tolist(), r["msg_off"].tolist(),
+                                                 r["msg_len"].tolist()):
+            c = CODES[code]
+            d = Diagnostic(c, CODE_REGISTRY[c][0], SrcLoc(path, line, col),
+                           tx[off:off + ln].tobytes().decode("utf-8", "surrogateescape"))
+            if sup:
+                d.suppressed = True
+            out.append(d)
+        return out
+
+    def codes(self, unit: int) -> list:
+        """The codes of a unit's unsuppressed diagnostics, without building objects."""
+        r = self.recs[int(self.unit_first[unit]):int(self.unit_first[unit + 1])]
+        return [CODES[c] for c, s in zip(r["code"].tolist(), r["suppressed"].tolist()) if not s]
+
+
 class Analysis:
-    path: str
-    profile: CompileProfile
-    mode: Mode
-    diagnostics: list
-    all_diagnostics: list = field(default_factory=list)
-    walks: dict = field(default_factory=dict)
-    passes: dict = field(default_factory=dict)  # pass kind -> status dict
-    _batch: object = field(default=None, repr=False, compare=False)
-    _file: int = field(default=0, repr=False, compare=False)
+    """Result of analysing one unit (spacecheck.py:669-681 Analysis).
+
+    ``diagnostics`` (ordered, unsuppressed) and ``all_diagnostics`` (with the
+    suppressed ones) are built from the run's columnar results on first access."""
+
+    def __init__(self, path: str, profile: CompileProfile, mode: Mode, results: CorpusResults = None,
+                 unit: int = 0, batch=None, diagnostics: list = None):
+        self.path = path
+        self.profile = profile
+        self.mode = mode
+        self.walks: dict = {}
+        self.passes: dict = {}  # pass kind -> status dict
+        self._results = results
+        self._unit = unit
+        self._batch = batch
+        self._file = unit
+        self._all = diagnostics
+
+    @property
+    def all_diagnostics(self) -> list:
+        if self._all is None:
+            self._all = self._results.diagnostics(self._unit) if self._results is not None else []
+        return self._all
+
+    @property
+    def diagnostics(self) -> list:
+        return [d for d in self.all_diagnostics if not d.suppressed]
 
     @property
     def has_errors(self) -> bool:
@@ -300,6 +357,9 @@ class Analysis:
             raise RuntimeError("struct declarations need an analysis run with want_walks=True")
         return self._batch.structs_of(self._file, pass_index)
 
+    def __repr__(self):
+        return f"Analysis(path={self.path!r}, mode={self.mode}, diagnostics={len(self.diagnostics)})"
+
 
 # ---------------------------------------------------------------------------
 # the engine
@@ -307,54 +367,52 @@ class Analysis:
 class Engine:
     """A GPU-resident analyser; one instance per device."""
 
-    def __init__(self, device: int = 0, lib_path=None):
+    def __init__(self, device: int = 0, lib_path=None, batch_mib: int = 1024):
         self.handle = _native.Handle(device, lib_path)
         self.lock = threading.Lock()
         self.last_stats: dict = {}
+        self.last_result_bytes = 0
+        self.batch_mib = batch_mib
+        self.handle.set_option(7, batch_mib)
 
     def run_batch(self, units: list, want_walks: bool = False):
         """units: list of (text, path, CompileProfile, Mode, TraitConfig).
 
-        Returns a list of Analysis in input order.
-        """
-        blobs = [u[0].encode("utf-8", "surrogateescape") for u in units]
-        offsets = np.zeros(len(blobs) + 1, dtype=np.uint64)
-        if blobs:
-            offsets[1:] = np.cumsum([len(b) for b in blobs])
-        data = np.frombuffer(b"".join(blobs), dtype=np.uint8) if blobs else np.zeros(0, np.uint8)
-        cfg = np.array([cfg_byte(u[2], u[3], u[4]) for u in units], dtype=np.uint8)
+        Returns a list of Analysis in input order.  The texts go to the
+        library without copies (exs_run_units streams them in batches); the
+        diagnostics come back rendered, ordered and de-duplicated."""
+        texts = [u[0] for u in units]
+        cfg = np.fromiter((cfg_byte(u[2], u[3], u[4]) for u in units), dtype=np.uint8, count=len(units))
+        paths = [u[1] for u in units]
         with self.lock:
-            self.handle.set_option(1, 1 if want_walks else 0)
-            self.handle.run(data, offsets, cfg)
-            recs = self.handle.diags(copy=False)  # consumed under the lock, before the next run
-            arena = self.handle.arena()
-            self.last_stats = self.handle.stats()
-            walks = self.handle.walk_stats(len(units)) if want_walks else None
-            status = self.handle.pass_status(len(units)) if want_walks else None
-            ren = Renderer(data.tobytes(), offsets.tolist(), arena, self.handle.describe)
-            batch = None
             if want_walks:
+                # walk arrays describe one batch: keep the whole run in one
+                self.handle.set_option(7, 2047)
+            self.handle.set_option(1, 1 if want_walks else 0)
+            self.handle.run_units(texts, cfg)
+            recs, text, first = self.handle.results(copy=True)
+            self.last_stats = self.handle.stats()
+            self.last_result_bytes = recs.nbytes + text.nbytes + first.nbytes
+            results = CorpusResults(recs, text, first, paths)
+            walks = status = batch = None
+            if want_walks:
+                if self.last_stats["batches"] != 1:
+                    raise ValueError("want_walks needs the units to fit one batch (< 2 GiB)")
+                walks = self.handle.walk_stats(len(units))
+                status = self.handle.pass_status(len(units))
+                blobs = [t.encode("utf-8", "surrogateescape") if isinstance(t, str) else bytes(t) for t in texts]
+                offsets = [0]
+                for b in blobs:
+                    offsets.append(offsets[-1] + len(b))
+                ren = Renderer(b"".join(blobs), offsets, self.handle.arena(), self.handle.describe)
                 # the walk arrays stay valid until the next run on this engine:
                 # snapshot them now (lazily rendered afterwards)
                 batch = BatchWalks(self.handle, ren, status, [u[3] for u in units])
                 batch._load()
-            out = self._assemble(units, recs, ren, walks, status, batch)
-        return out
-
-    def _assemble(self, units, recs, ren: Renderer, walks, status, batch=None):
-        per_file: list = [[] for _ in units]
-        for r in recs:
-            f = int(r["file"])
-            code = CODES[int(r["code"])]
-            msg = ren.message(r)
-            d = Diagnostic.make(code, SrcLoc(units[f][1], int(r["line"]), int(r["col"])), msg)
-            d.suppressed = bool(r["suppressed"])
-            per_file[f].append(d)
+                self.handle.set_option(7, self.batch_mib)
         out = []
         for f, u in enumerate(units):
-            ordered = finish_diagnostics(per_file[f])
-            a = Analysis(u[1], u[2], u[3], [d for d in ordered if not d.suppressed], ordered,
-                         _batch=batch, _file=f)
+            a = Analysis(u[1], u[2], u[3], results, f, batch)
             if walks is not None:
                 for p, side in ((0, HOST), (1, DEVICE)):
                     w = walks[2 * f + p]
@@ -396,15 +454,19 @@ def check_unit(text: str, path: str = "<unit>", profile: CompileProfile = Compil
 
 def analyze_corpus(units: Iterable, profile: CompileProfile = CompileProfile(),
                    mode: Mode = Mode.CLASSIC, cfg: TraitConfig = TraitConfig(),
-                   device: int = 0, want_walks: bool = False) -> list:
-    """Batch analysis.  ``units`` yields (path, text) or (path, text, profile, mode, cfg)."""
+                   device: int = 0, want_walks: bool = False, engine: Optional[Engine] = None) -> list:
+    """Batch analysis: ``analyze`` over every unit (corpus.py:163-175).
+
+    ``units`` yields (path, text) or (path, text, profile, mode, cfg); any
+    total size (the library streams them in batches).  Returns one Analysis
+    per unit, in input order."""
     packed = []
     for u in units:
         if len(u) == 2:
             packed.append((u[1], u[0], profile, mode, cfg))
         else:
             packed.append((u[1], u[0], u[2], u[3], u[4]))
-    return get_engine(device).run_batch(packed, want_walks=want_walks)
+    return (engine or get_engine(device)).run_batch(packed, want_walks=want_walks)
 
 
 def declared_spaces(spec: int) -> frozenset:
@@ -443,7 +505,7 @@ def stray_set(analysis: Analysis) -> list:
 
 
 __all__ = [
-    "Analysis", "CODE_REGISTRY", "CompileProfile", "Diagnostic", "Engine", "ExecSpace", "GLOBAL",
+    "Analysis", "CODE_REGISTRY", "CompileProfile", "CorpusResults", "Diagnostic", "Engine", "ExecSpace", "GLOBAL",
     "Mode", "Severity", "SrcLoc", "StructInfo", "TraitConfig", "Verdict", "analyze",
     "analyze_corpus", "check_unit", "declared_spaces", "finish_diagnostics", "format_diagnostic",
     "get_engine", "legality", "propagate_spaces", "stray_set", "stray_text",

@@ -42,37 +42,93 @@ def my_shard(units: Sequence, rank: int, world: int, size_of: Callable = None) -
     return lo, hi
 
 
-def gather_in_rank_order(local: list, rank: int, world: int, group=None) -> Optional[list]:
-    """Concatenate every rank's list on rank 0 in rank order (None elsewhere)."""
+def merge_results(parts: Sequence) -> tuple:
+    """Concatenate per-shard columnar results (recs, text, unit_first) in
+    shard order: unit indices and message offsets move past the earlier
+    shards' (exs_result layout, include/exspace_b200.h)."""
+    import numpy as np
+    from ._native import RESULT_DTYPE
+    recs, texts, firsts = [], [], [np.zeros(1, dtype=np.uint64)]
+    units = 0
+    tbase = 0
+    rbase = 0
+    for r, t, f in parts:
+        r = np.array(r, dtype=RESULT_DTYPE, copy=True)
+        r["unit"] += units
+        r["msg_off"] += tbase
+        recs.append(r)
+        texts.append(np.asarray(t, dtype=np.uint8))
+        firsts.append(np.asarray(f[1:], dtype=np.uint64) + rbase)
+        units += len(f) - 1
+        tbase += len(t)
+        rbase += len(r)
+    return (np.concatenate(recs) if recs else np.zeros(0, dtype=RESULT_DTYPE),
+            np.concatenate(texts) if texts else np.zeros(0, dtype=np.uint8),
+            np.concatenate(firsts))
+
+
+def gather_results(recs, text, unit_first, rank: int, world: int, device=None, group=None):
+    """Gather every rank's columnar results to rank 0 in rank order (None on
+    other ranks) with point-to-point collectives: an all-gather of the three
+    sizes, then one variable-size send/recv per rank of each byte buffer.
+    ``device``: where the byte tensors live (a CUDA device for NCCL, None for
+    CPU / gloo)."""
+    import numpy as np
+    import torch
     import torch.distributed as dist
+    from ._native import RESULT_DTYPE
     if world == 1:
-        return list(local)
-    bucket = [None] * world if rank == 0 else None
-    dist.gather_object(local, bucket, dst=0, group=group)
+        return recs, text, unit_first
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    bufs = [np.ascontiguousarray(recs).view(np.uint8).reshape(-1),
+            np.ascontiguousarray(text, dtype=np.uint8).reshape(-1),
+            np.ascontiguousarray(unit_first, dtype=np.uint64).view(np.uint8).reshape(-1)]
+    sizes = torch.tensor([b.size for b in bufs], dtype=torch.int64, device=dev)
+    allsz = [torch.zeros_like(sizes) for _ in range(world)]
+    dist.all_gather(allsz, sizes, group=group)
+    allsz = [x.tolist() for x in allsz]
     if rank != 0:
+        for b in bufs:
+            if b.size:
+                dist.send(torch.from_numpy(b).to(dev), dst=0, group=group)
         return None
-    out = []
-    for part in bucket:
-        out.extend(part)
-    return out
+    parts = [tuple(bufs)]
+    for src in range(1, world):
+        got = []
+        for k in range(3):
+            t = torch.empty(allsz[src][k], dtype=torch.uint8, device=dev)
+            if allsz[src][k]:
+                dist.recv(t, src=src, group=group)
+            got.append(t.cpu().numpy())
+        parts.append(tuple(got))
+    return merge_results([(p[0].view(RESULT_DTYPE), p[1], p[2].view(np.uint64)) for p in parts])
 
 
-def analyze_sharded(units: Sequence, rank: int, world: int,
-                    analyze_batch: Optional[Callable] = None, device: Optional[int] = None):
-    """Analyse this rank's shard and gather ordered results to rank 0.
+def analyze_sharded(units: Sequence, rank: int, world: int, analyze_batch: Optional[Callable] = None,
+                    device: Optional[int] = None, comm_device=None):
+    """Analyse this rank's shard and gather the results to rank 0.
 
-    ``units`` are (path, text[, profile, mode, cfg]) sorted by path;
-    ``analyze_batch(shard) -> list`` defaults to the GPU engine on ``device``.
-    Returns the full ordered list on rank 0 and None on other ranks.
-    """
+    ``units`` are (path, text[, profile, mode, cfg]) sorted by path.
+    ``analyze_batch(shard) -> (recs, text, unit_first)`` defaults to the GPU
+    engine on ``device``.  Returns, on rank 0, one Analysis per unit of the
+    whole corpus in input order (None on other ranks)."""
+    from . import exspace as X
     lo, hi = my_shard(units, rank, world)
     shard = list(units[lo:hi])
     if analyze_batch is None:
-        from .exspace import analyze_corpus
         dev = rank if device is None else device
-        res = analyze_corpus(shard, device=dev) if shard else []
-        local = [[(d.code, d.loc.file, d.loc.line, d.loc.col, d.message) for d in a.diagnostics]
-                 for a in res]
+        eng = X.get_engine(dev)
+        X.analyze_corpus(shard, device=dev, engine=eng)
+        local = eng.handle.results(copy=True)
     else:
         local = analyze_batch(shard)
-    return gather_in_rank_order(local, rank, world)
+    merged = gather_results(*local, rank, world, device=comm_device)
+    if merged is None:
+        return None
+    res = X.CorpusResults(*merged, [u[0] for u in units])
+    out = []
+    for f, u in enumerate(units):
+        prof = u[2] if len(u) > 2 else X.CompileProfile()
+        mode = u[3] if len(u) > 3 else X.Mode.CLASSIC
+        out.append(X.Analysis(u[0], prof, mode, res, f))
+    return out

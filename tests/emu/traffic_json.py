@@ -3,8 +3,8 @@
 ncu --nvtx --nvtx-include "walk_chunks/" ... --metrics \
   dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
   --clock-control none --csv --log-file X.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline
-python tests/emu/traffic_json.py X.csv profiles/<name>.csv  (the CSV is copied there; the
-JSON cites it)
+python tests/emu/traffic_json.py X.csv profiles/<name>.csv [config] (the CSV is copied
+there; the JSON entry of the config -- default c2 -- cites it)
 """
 import csv
 import collections
@@ -19,6 +19,7 @@ ROOT = Path(__file__).resolve().parents[2]
 
 def main():
     src, dst = Path(sys.argv[1]), Path(sys.argv[2])
+    config = sys.argv[3] if len(sys.argv) > 3 else "c2"
     rows = [r for r in csv.reader(open(src)) if r]
     hdr = next(r for r in rows if r[0] == "ID")
     ti = next(i for i, h in enumerate(hdr) if "Push/Pop_Range" in h)
@@ -43,15 +44,18 @@ def main():
     shutil.copy(src, dst)
     rel = dst.relative_to(ROOT) if dst.is_absolute() else dst
     source = ("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-              "--clock-control none on `bench.py --steps 1 --warmup 1 --no-cpu-baseline` (C2 10k files, "
-              f"1.02 GB); mean over the launches of the run (warm-up, step and e2e runs); {rel}")
+              f"--clock-control none on `bench.py --config {config} --steps 1 --warmup 1 --no-cpu-baseline`; "
+              f"mean over the launches of the run (warm-up, step and e2e runs); {rel}")
     out = {}
     for tag, a in sorted(agg.items()):
         n = a["launches"]
         out[tag] = {"launches": n, "dram_bytes_per_launch": (a["rd"] + a["wr"]) / n,
                     "dram_read_bytes_per_launch": a["rd"] / n, "dram_write_bytes_per_launch": a["wr"] / n,
                     "ncu_ns_per_launch": a["ns"] / n, "source": source}
-    (ROOT / "profiles" / "ncu_traffic.json").write_text(json.dumps(out, indent=1) + "\n")
+    db_path = ROOT / "profiles" / "ncu_traffic.json"
+    db = json.loads(db_path.read_text()) if db_path.exists() else {}
+    db[config] = out
+    db_path.write_text(json.dumps(db, indent=1) + "\n")
     for tag, e in out.items():
         print(f"{tag:18s} x{e['launches']} {e['dram_bytes_per_launch'] / 1e9:8.2f} GB/launch "
               f"{e['ncu_ns_per_launch'] / 1e6:7.2f} ms")

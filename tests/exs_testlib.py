@@ -18,6 +18,25 @@ def load_golden(name):
         return json.load(fh)
 
 
+def oracle_results(units, mode):
+    """The oracle's diagnostics of (path, text) units as columnar results in
+    the library's layout (exs_result records, message bytes, unit_first):
+    stands in for a GPU engine in the CPU tests of the result plumbing."""
+    import numpy as np
+    from paper_2309_03912_b200._native import RESULT_DTYPE
+    from paper_2309_03912_b200.messages import CODES
+    rows, text, first = [], bytearray(), [0]
+    for u, unit in enumerate(units):
+        r = O.analyze_unit(unit[1], mode)
+        for code, line, col, msg, sup in r.all_diagnostics:
+            m = msg.encode("utf-8", "surrogateescape")
+            rows.append((u, line, col, len(m), len(text), CODES.index(code), int(sup), (0,) * 5))
+            text += m
+        first.append(len(rows))
+    return (np.array(rows, dtype=RESULT_DTYPE), np.frombuffer(bytes(text), dtype=np.uint8),
+            np.array(first, dtype=np.uint64))
+
+
 def canon_val(v):
     if isinstance(v, O.Ty):
         return v.name + ("<" + ",".join(v.targs) + ">" if v.targs else "")

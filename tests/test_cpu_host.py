@@ -144,14 +144,16 @@ import torch.distributed as dist
 from oracle import exs_oracle as O
 from paper_2309_03912_b200 import synth
 from paper_2309_03912_b200.shard import analyze_sharded
+from exs_testlib import oracle_results
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=rank, world_size=world)
 units = [(f"f{{i:03d}}.cu", synth.gen_c5_file(i, 1500 + 400 * (i % 5), 0.3)) for i in range(13)]
-def oracle_batch(shard):  # the per-rank analysis stands in for the GPU engine on CPU
-    return [[(d[0], p, d[1], d[2], d[3]) for d in O.check(t, "sound")] for p, t in shard]
-res = analyze_sharded(units, rank, world, oracle_batch)
+# the per-rank analysis: the oracle's results in the library's columnar layout
+# stand in for the GPU engine on CPU; the gather is the code under test
+res = analyze_sharded(units, rank, world, lambda shard: oracle_results(shard, "sound"))
 if rank == 0:
-    print(json.dumps(res))
+    print(json.dumps([[(d.code, d.loc.file, d.loc.line, d.loc.col, d.message) for d in a.diagnostics]
+                      for a in res]))
 dist.destroy_process_group()
 """
 

@@ -295,3 +295,69 @@ def test_diag_sort_paths_agree(X, eng):
     assert sum(len(a.all_diagnostics) for a in packed) > 1000
     for a, b in zip(packed, two):
         assert as_rows(a) == as_rows(b)
+
+
+def test_streamed_batches_equal_one_batch(X):
+    """exs_run_units cut into 1 MiB batches (copies of batch k+1 overlapping the
+    analysis of batch k) reports exactly what one batch reports, and both
+    equal the oracle on a sample."""
+    from paper_2309_03912_b200 import synth
+    texts = ([synth.gen_c2_file(300 + s, 60_000) for s in range(40)] +
+             [synth.gen_c5_file(700 + s, 30_000, 0.5) for s in range(16)])
+    modes = ["classic", "sound", "proposal2", "fidelity", "proposal1"]
+    units = [(t, f"s{i:03d}.cu", X.CompileProfile(), X.Mode(modes[i % 5]), X.TraitConfig())
+             for i, t in enumerate(texts)]
+    one = X.Engine(0).run_batch(units)
+    e = X.Engine(0, batch_mib=1)
+    many = e.run_batch(units)
+    assert e.last_stats["batches"] >= 3
+    for a, b in zip(one, many):
+        assert as_rows(a) == as_rows(b)
+    for i in range(0, len(texts), 7):
+        want = O.check(texts[i], modes[i % 5])
+        assert [(d.code, d.loc.line, d.loc.col, d.message) for d in many[i].diagnostics] == want
+
+
+def test_results_view_is_ordered_and_complete(X, eng):
+    """exs_results_view: per-unit ranges cover every record once, records are
+    in (unit, line, col, code, message) order, messages decode as UTF-8."""
+    from paper_2309_03912_b200 import synth
+    texts = [synth.gen_c5_file(900 + s, 20_000, 0.5) for s in range(20)]
+    units = [(t, f"v{i}.cu", X.CompileProfile(), X.Mode.SOUND, X.TraitConfig()) for i, t in enumerate(texts)]
+    eng.run_batch(units)
+    recs, text, first = eng.handle.results(copy=False)
+    assert int(first[0]) == 0 and int(first[-1]) == len(recs) and len(first) == len(units) + 1
+    keys = []
+    for u in range(len(units)):
+        r = recs[int(first[u]):int(first[u + 1])]
+        assert (r["unit"] == u).all()
+        for x in r:
+            msg = text[int(x["msg_off"]):int(x["msg_off"]) + int(x["msg_len"])].tobytes().decode()
+            keys.append((u, int(x["line"]), int(x["col"]), int(x["code"]), msg))
+    assert keys == sorted(keys) and len(set(keys)) == len(keys)
+
+
+@pytest.mark.parametrize("n_shards", [2, 3])
+def test_logical_shards_merge_to_the_one_shard_run(X, n_shards):
+    """The corpus cut into byte-balanced shards (shard.shard_ranges, the
+    multi-GPU partition), each analysed alone on this device and merged in
+    rank order (shard.merge_results, what gather_results does on rank 0),
+    equals the one-shard run record for record."""
+    from paper_2309_03912_b200 import synth
+    from paper_2309_03912_b200.shard import merge_results, shard_ranges
+    texts = [synth.gen_c5_file(1200 + s, 8_000 + 3_000 * (s % 4), 0.4) for s in range(23)]
+    units = [(f"m{i:03d}.cu", t) for i, t in enumerate(texts)]
+    e = X.Engine(0)
+    X.analyze_corpus(units, mode=X.Mode.SOUND, engine=e)
+    whole = e.handle.results(copy=True)
+    parts = []
+    for lo, hi in shard_ranges([len(t) for t in texts], n_shards):
+        X.analyze_corpus(units[lo:hi], mode=X.Mode.SOUND, engine=e)
+        parts.append(e.handle.results(copy=True))
+    merged = merge_results(parts)
+    res_w = X.CorpusResults(*whole, [u[0] for u in units])
+    res_m = X.CorpusResults(*merged, [u[0] for u in units])
+    assert list(merged[2]) == list(whole[2])
+    for u in range(len(units)):
+        rows = lambda r: [(d.code, d.loc.line, d.loc.col, d.message, d.suppressed) for d in r.diagnostics(u)]  # noqa
+        assert rows(res_m) == rows(res_w)

@@ -178,6 +178,10 @@ typedef struct {
 int exs_results_view(exs_handle h, const exs_result** recs, uint64_t* n, const char** text,
                      uint64_t* text_bytes, const uint64_t** unit_first, uint64_t* n_units);
 
+/* Copy the results of the last run into caller memory (sizes from
+ * exs_results_view; any pointer may be null), with several host threads. */
+int exs_results_copy(exs_handle h, exs_result* recs, char* text, uint64_t* unit_first);
+
 int exs_get_stats(exs_handle h, exs_stats* out);
 /* raw records ordered by (file, line, col, code), duplicates removed (only
  * kept with option 6; the rendered form is exs_results_view) */

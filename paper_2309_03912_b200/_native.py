@@ -60,7 +60,7 @@ EXPORTS = [
     "exs_get_diags", "exs_diags_view", "exs_get_arena", "exs_get_pass_status", "exs_get_tokens",
     "exs_get_walk_stats", "exs_describe", "exs_set_option", "exs_stage_times", "exs_profile_text",
     "exs_get_decls", "exs_get_structs", "exs_get_instances", "exs_get_edges", "exs_get_nodes",
-    "exs_get_token_range", "exs_run_units", "exs_results_view",
+    "exs_get_token_range", "exs_run_units", "exs_results_view", "exs_results_copy",
 ]
 
 # one finished diagnostic (include/exspace_b200.h exs_result)
@@ -145,6 +145,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     lib.exs_set_option.argtypes = [vp, C.c_int, C.c_int]
     lib.exs_stage_times.argtypes = [vp, C.POINTER(C.c_float)]
     lib.exs_run_units.argtypes = [vp, vp, vp, C.c_uint64, vp]
+    lib.exs_results_copy.argtypes = [vp, vp, vp, vp]
     lib.exs_results_view.argtypes = [vp, C.POINTER(C.c_void_p), u64p, C.POINTER(C.c_void_p), u64p,
                                      C.POINTER(C.c_void_p), u64p]
     for name in EXPORTS:
@@ -219,11 +220,15 @@ class Handle:
                 return np.zeros(0, dtype=np.uint8)
             return np.frombuffer((C.c_uint8 * nbytes).from_address(ptr.value), dtype=np.uint8)
 
+        if copy:  # into fresh arrays, by the library's copy threads
+            recs = np.empty(n.value, dtype=RESULT_DTYPE)
+            text = np.empty(tb.value, dtype=np.uint8)
+            first = np.zeros(nu.value + 1, dtype=np.uint64)
+            self._check(self.lib.exs_results_copy(self.h, _ptr(recs), _ptr(text), _ptr(first)))
+            return recs, text, first
         recs = view(rp, n.value * RESULT_DTYPE.itemsize)
         text = view(tp, tb.value)
         first = view(up, (nu.value + 1) * 8) if up.value else np.zeros(8, dtype=np.uint8)
-        if copy:
-            recs, text, first = recs.copy(), text.copy(), first.copy()
         return recs.view(RESULT_DTYPE), text, first.view(np.uint64)
 
     def stats(self) -> dict:

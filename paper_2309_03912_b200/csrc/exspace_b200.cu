@@ -930,11 +930,18 @@ static void run_units(Handle& H, const char* const* texts, const uint64_t* lens,
   // plan
   std::vector<BatchPlan> plan;
   {
+    u64 total = 0;
+    for (u64 u = 0; u < n_units; u++) total += lens[u];
+    // the first batch's packing and copy are not hidden behind an earlier
+    // batch: a smaller first batch starts the device sooner
+    const u64 cap0 = total > H.batch_cap ? std::min<u64>(H.batch_cap, std::max<u64>(H.batch_cap / 4, 16ull << 20))
+                                         : H.batch_cap;
     BatchPlan cur{0, 0, 0, {0}};
     for (u64 u = 0; u < n_units; u++) {
       const u64 n = lens[u];
       if (n >= (1ull << 31) - 64) throw Err("a unit larger than 2 GiB is outside the contract");
-      if (cur.u1 > cur.u0 && (cur.bytes + n > H.batch_cap || cur.u1 - cur.u0 >= (1u << 26))) {
+      const u64 cap = plan.empty() ? cap0 : H.batch_cap;
+      if (cur.u1 > cur.u0 && (cur.bytes + n > cap || cur.u1 - cur.u0 >= (1u << 26))) {
         plan.push_back(cur);
         cur = BatchPlan{u, u, 0, {0}};
       }
@@ -1035,6 +1042,30 @@ int exs_run_units(exs_handle x, const char* const* texts, const uint64_t* lens, 
   CK(cudaSetDevice(H.device));
 #endif
   run_units(H, texts, lens, n_units, unit_cfg);
+  API_END
+}
+
+// parallel copy of [src, src + n) to dst (first touch of fresh pages included)
+static void copy_threads(void* dst, const void* src, u64 n, int nthreads) {
+  if (nthreads <= 1 || n < (4u << 20)) { if (n) memcpy(dst, src, n); return; }
+  const u64 per = ((n + nthreads - 1) / nthreads + 4095) & ~4095ull;
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; t++) {
+    const u64 lo = (u64)t * per, hi = std::min(n, lo + per);
+    if (lo >= hi) break;
+    th.emplace_back([=]() { memcpy((u8*)dst + lo, (const u8*)src + lo, hi - lo); });
+  }
+  for (auto& x : th) x.join();
+}
+
+int exs_results_copy(exs_handle x, exs_result* recs, char* text, uint64_t* unit_first) {
+  API_TRY
+  const Handle& H = x->h;
+  const int nt = H.pack_threads > 0 ? H.pack_threads
+                                    : (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
+  if (recs) copy_threads(recs, H.res.p, H.n_res * sizeof(ResRec), nt);
+  if (text) copy_threads(text, H.text.p, H.text_bytes, nt);
+  if (unit_first && !H.unit_first.empty()) memcpy(unit_first, H.unit_first.data(), 8 * H.unit_first.size());
   API_END
 }
 

@@ -319,17 +319,18 @@ class Analysis:
     ``diagnostics`` (ordered, unsuppressed) and ``all_diagnostics`` (with the
     suppressed ones) are built from the run's columnar results on first access."""
 
+    __slots__ = ("path", "profile", "mode", "walks", "passes", "_results", "_unit", "_batch", "_all")
+
     def __init__(self, path: str, profile: CompileProfile, mode: Mode, results: CorpusResults = None,
                  unit: int = 0, batch=None, diagnostics: list = None):
         self.path = path
         self.profile = profile
         self.mode = mode
-        self.walks: dict = {}
-        self.passes: dict = {}  # pass kind -> status dict
+        self.walks = {}
+        self.passes = {}  # pass kind -> status dict
         self._results = results
         self._unit = unit
         self._batch = batch
-        self._file = unit
         self._all = diagnostics
 
     @property
@@ -355,7 +356,7 @@ class Analysis:
         erase_specifiers its specifiers are erased (spacecheck.py:697-699)."""
         if self._batch is None:
             raise RuntimeError("struct declarations need an analysis run with want_walks=True")
-        return self._batch.structs_of(self._file, pass_index)
+        return self._batch.structs_of(self._unit, pass_index)
 
     def __repr__(self):
         return f"Analysis(path={self.path!r}, mode={self.mode}, diagnostics={len(self.diagnostics)})"
@@ -382,7 +383,15 @@ class Engine:
         library without copies (exs_run_units streams them in batches); the
         diagnostics come back rendered, ordered and de-duplicated."""
         texts = [u[0] for u in units]
-        cfg = np.fromiter((cfg_byte(u[2], u[3], u[4]) for u in units), dtype=np.uint8, count=len(units))
+        memo: dict = {}
+
+        def cb(u):
+            k = (u[2], u[3], u[4])
+            b = memo.get(k)
+            if b is None:
+                b = memo[k] = cfg_byte(*k)
+            return b
+        cfg = np.fromiter(map(cb, units), dtype=np.uint8, count=len(units))
         paths = [u[1] for u in units]
         with self.lock:
             if want_walks:

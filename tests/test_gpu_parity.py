@@ -320,7 +320,9 @@ def test_streamed_batches_equal_one_batch(X):
 
 def test_results_view_is_ordered_and_complete(X, eng):
     """exs_results_view: per-unit ranges cover every record once, records are
-    in (unit, line, col, code, message) order, messages decode as UTF-8."""
+    in (unit, line, col, code string, message) order -- Diagnostic.sort_key,
+    diagnostics.py:73-74 -- and messages decode as UTF-8."""
+    from paper_2309_03912_b200.messages import CODES
     from paper_2309_03912_b200 import synth
     texts = [synth.gen_c5_file(900 + s, 20_000, 0.5) for s in range(20)]
     units = [(t, f"v{i}.cu", X.CompileProfile(), X.Mode.SOUND, X.TraitConfig()) for i, t in enumerate(texts)]
@@ -333,7 +335,7 @@ def test_results_view_is_ordered_and_complete(X, eng):
         assert (r["unit"] == u).all()
         for x in r:
             msg = text[int(x["msg_off"]):int(x["msg_off"]) + int(x["msg_len"])].tobytes().decode()
-            keys.append((u, int(x["line"]), int(x["col"]), int(x["code"]), msg))
+            keys.append((u, int(x["line"]), int(x["col"]), CODES[int(x["code"])], msg))
     assert keys == sorted(keys) and len(set(keys)) == len(keys)
 
 

@@ -71,6 +71,14 @@ def make_texts(kind: str, seeds, file_bytes: int, procs: int):
         return pool.map(_gen, [(kind, s, file_bytes) for s in seeds], chunksize=16)
 
 
+def make_corpus(n_files: int, file_bytes: int, seed0: int, procs: int):
+    """(blobs, uint64 offsets) of C2 files seed0 .. seed0 + n_files - 1 (dev tools)."""
+    blobs = [t.encode() for t in make_texts("c2", range(seed0, seed0 + n_files), file_bytes, procs)]
+    offs = np.zeros(n_files + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(b) for b in blobs])
+    return blobs, offs
+
+
 class Workload:
     """Units of one rank: (paths, texts) plus how to describe them."""
 

@@ -246,11 +246,9 @@ struct Handle {
     dfree(d_src_owned);
     dfree(d_static);
     for (int k = 0; k < 2; k++) {
+      dfree(d_slot[k]);
 #ifndef EXS_EMU
-      if (d_slot[k]) cudaFree(d_slot[k]);
       if (ev_h2d[k]) cudaEventDestroy(ev_h2d[k]);
-#else
-      free(d_slot[k]);
 #endif
     }
 #ifndef EXS_EMU
@@ -907,17 +905,18 @@ static void pack_units(const char* const* texts, const uint64_t* lens, u64 u0, u
   for (auto& t : th) t.join();
 }
 
+// device slots come from the stream-ordered pool like every other buffer (a
+// plain cudaMalloc would fail while the pool holds the memory of earlier runs)
 static void ensure_slot(Handle& H, int k, u64 bytes) {
   if (H.d_slot_cap[k] >= bytes) return;
 #ifndef EXS_EMU
-  if (H.d_slot[k]) { CK(cudaStreamSynchronize(H.st)); CK(cudaFree(H.d_slot[k])); }
-  H.d_slot[k] = nullptr;
-  CK(cudaMalloc((void**)&H.d_slot[k], bytes));
-#else
-  free(H.d_slot[k]);
-  H.d_slot[k] = (u8*)malloc(bytes);
+  if (H.cst) CK(cudaStreamSynchronize(H.cst));
 #endif
+  sync(H.st);
+  dfree(H.d_slot[k]);
+  H.d_slot[k] = dalloc<u8>(bytes);
   H.d_slot_cap[k] = bytes;
+  sync(H.st);  // the copy stream uses it next
 }
 
 struct BatchPlan {

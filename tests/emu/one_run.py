@@ -8,7 +8,7 @@ from paper_2309_03912_b200 import _native
 import bench
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-blobs, offs = bench.make_corpus(n, 100_000, 0, os.cpu_count())
+blobs, offs = bench.make_corpus(n, 100_000, 0, os.cpu_count())  # noqa
 data = np.frombuffer(b"".join(blobs), np.uint8)
 h = _native.Handle(0)
 for _ in range(reps):

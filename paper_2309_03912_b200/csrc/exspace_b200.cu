@@ -210,6 +210,7 @@ struct Handle {
   long long select_flagged_min = EXS_SELECT_FLAGGED_MIN;  // select_idx flag-pass threshold (indices)
   bool diag_sort_two_pass = false;  // force the two-key diagnostic sort (parity tests)
   bool keep_records = false;        // also keep the raw records (exs_get_diags / exs_diags_view)
+  bool fast_walk = true;            // the register-resident walker for common statements (option 9)
   // rendered results of the last run (all its batches), in unit order
   PinnedBuf res, text;
   u64 n_res = 0, text_bytes = 0, static_bytes = 0;
@@ -615,6 +616,26 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     // the walk is retried alone (bigger instance table) after restoring the
     // diagnostics emitted by the earlier stages
     u32 nd0 = get1(H.d_ndiags, st);
+    // grow the diagnostics buffer and its dedup set, keeping the nd0
+    // diagnostics of the earlier stages
+    auto regrow = [&](u32 ncap) {
+      Diag* ndg = dalloc<Diag>((u64)ncap + n_files);
+      if (nd0) d2d(ndg, H.d_diags, sizeof(Diag) * (u64)nd0, st);
+      const u32 nmask = pow2_at_least(2ull * ncap) - 1;
+      u64* nset = dalloc<u64>((u64)nmask + 1);
+      dzero(nset, 8ull * ((u64)nmask + 1), st);
+      par_for(nd0, [=] EXS_HD (i64 i) { set_insert(nset, nmask, diag_hash(ndg[i])); }, st);
+      dfree(H.d_diags); dfree(H.d_dset);
+      H.d_diags = ndg; H.d_dset = nset; H.dmask = nmask; H.cap_diags = ncap; cap_diags = ncap;
+      B0.diags = ndg; B0.cap_diags = ncap; B0.dset = nset; B0.dmask = nmask;
+    };
+    // size it for the walk from the call sites up front: a walk emits at most
+    // about one diagnostic per four call sites on the measured corpora (C4:
+    // 43.7 M from 250 M), and an overflow costs a second walk
+    {
+      const u64 want = std::min<u64>((u64)nd0 + H.S.NCS / 4 + 65536, 0x7FFFFFFFull);
+      if (want > cap_diags && nd0 <= cap_diags) regrow((u32)want);
+    }
     u64* dset_snap = dalloc<u64>((u64)H.dmask + 1);
     u32* ct_snap = dalloc<u32>(n_files + 1);
     d2d(dset_snap, H.d_dset, 8ull * (H.dmask + 1), st);
@@ -628,6 +649,7 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       H.W = WalkState();
       H.W.cap_inst = cap_inst;
       H.W.buf_scale = buf_scale;
+      H.W.fast = H.fast_walk;
       bool ok = run_walk(L, H.P, H.S, H.W, B0, H.sc, st, cap_diags);
       if (ok && (any_div || H.want_demands)) run_demands(H, any_div);
       walk_ovf = get1(H.W.ctr(CNT_OVF), st);
@@ -637,18 +659,10 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
         // diagnostics overflowed inside the walk: grow the buffer and its dedup
         // set, keep the diagnostics of the earlier stages, re-run the walk only
         const u32 nd_now = get1(H.d_ndiags, st);
-        const u32 ncap = (u32)std::min<u64>(4ull * std::max(nd_now, cap_diags), 0x7FFFFFFFull);
-        Diag* ndg = dalloc<Diag>((u64)ncap + n_files);
-        if (nd0) d2d(ndg, H.d_diags, sizeof(Diag) * (u64)nd0, st);
-        const u32 nmask = pow2_at_least(2ull * ncap) - 1;
-        u64* nset = dalloc<u64>((u64)nmask + 1);
-        dzero(nset, 8ull * ((u64)nmask + 1), st);
-        par_for(nd0, [=] EXS_HD (i64 i) { set_insert(nset, nmask, diag_hash(ndg[i])); }, st);
-        dfree(H.d_diags); dfree(H.d_dset); dfree(dset_snap);
-        H.d_diags = ndg; H.d_dset = nset; H.dmask = nmask; H.cap_diags = ncap; cap_diags = ncap;
-        B0.diags = ndg; B0.cap_diags = ncap; B0.dset = nset; B0.dmask = nmask;
-        dset_snap = dalloc<u64>((u64)nmask + 1);
-        d2d(dset_snap, nset, 8ull * ((u64)nmask + 1), st);
+        regrow((u32)std::min<u64>(4ull * std::max(nd_now, cap_diags), 0x7FFFFFFFull));
+        dfree(dset_snap);
+        dset_snap = dalloc<u64>((u64)H.dmask + 1);
+        d2d(dset_snap, H.d_dset, 8ull * ((u64)H.dmask + 1), st);
       } else if (walk_ovf & 2) {
         break;  // the earlier stages overflowed too: outer loop
       }
@@ -1099,6 +1113,7 @@ int exs_set_option(exs_handle x, int key, int value) {
   else if (key == 6) x->h.keep_records = value != 0;        // keep raw records (exs_get_diags)
   else if (key == 7) x->h.batch_cap = (u64)std::min(2047, std::max(1, value)) << 20;  // batch MiB
   else if (key == 8) x->h.pack_threads = value;               // host packing threads (0 = auto)
+  else if (key == 9) x->h.fast_walk = value != 0;             // common statements on the fast walker
   else throw Err("unknown option");
   API_END
 }

@@ -207,11 +207,15 @@ void b() { D{}.call(); }
 
 
 def test_diagnostic_overflow_regrows_inside_the_walk(X, eng):
-    """A unit whose walk emits more diagnostics than the initial buffer holds
-    (C4 shape: ~87k E1xxx) is re-walked with a grown buffer, keeping the
-    earlier stages' diagnostics -- same ordered set as the oracle."""
-    from paper_2309_03912_b200 import synth
-    text = synth.gen_callgraph(20000, 10, 3)
+    """A unit whose walk emits more diagnostics than the buffer sized from its
+    call sites holds (every call a stray: 120k E1002 against the 1-in-4
+    estimate) is re-walked with a grown buffer, keeping the earlier stages'
+    diagnostics -- same ordered set as the oracle."""
+    lines = [f"void h{i}() {{}}" for i in range(10)]
+    lines += [f"__device__ void f{i}() {{ " + " ".join(f"h{(i + k) % 10}();" for k in range(10)) + " }"
+              for i in range(12000)]
+    lines += ["int main() { return 0; }"]
+    text = "\n".join(lines) + "\n"
     a = eng.run_batch([(text, "c4.cu", X.CompileProfile(), X.Mode.SOUND, X.TraitConfig())])[0]
     assert eng.last_stats["retries"] >= 1
     rows, _, _ = _oracle_rows(text, "sound")
@@ -363,3 +367,34 @@ def test_logical_shards_merge_to_the_one_shard_run(X, n_shards):
     for u in range(len(units)):
         rows = lambda r: [(d.code, d.loc.line, d.loc.col, d.message, d.suppressed) for d in r.diagnostics(u)]  # noqa
         assert rows(res_m) == rows(res_w)
+
+
+def test_fast_walker_equals_the_general_walker(X):
+    """The register-resident walker of the common statement shapes
+    (csrc/exs_fastwalk.cuh) and the general walker give the same diagnostics,
+    walk counts and walk keys on every golden unit and on C2-C5 corpora."""
+    from paper_2309_03912_b200 import synth
+    modes = ["classic", "sound", "proposal2", "fidelity", "proposal1"]
+    texts = ([synth.gen_c2_file(s, 50_000) for s in range(20)] +
+             [synth.gen_c5_file(s, 50_000, 0.3) for s in range(20)] +
+             [synth.gen_chain(12, 40), synth.gen_callgraph(3000, 10, 1)])
+    units = [(t, f"u{i}.cu", X.CompileProfile(), X.Mode(modes[i % 5]), X.TraitConfig()) for i, t in enumerate(texts)]
+    for g in GOLDEN_GROUPS:
+        units += [unit_of(X, c, "g.mcu") for c in load_golden(g)]
+    fast, general = X.Engine(0), X.Engine(0)
+    general.handle.set_option(9, 0)
+    A = fast.run_batch(units, want_walks=True)
+    B = general.run_batch(units, want_walks=True)
+    bad = []
+    for i, (a, b) in enumerate(zip(A, B)):
+        if as_rows(a) != as_rows(b):
+            bad.append((i, "diags"))
+            continue
+        for side, w in a.walks.items():
+            v = b.walks[side]
+            if (w.n_instances, w.n_edges, w.n_demands) != (v.n_instances, v.n_edges, v.n_demands):
+                bad.append((i, "counts"))
+            elif i >= len(texts) and (w.instances.keys() != v.instances.keys() or w.edges != v.edges
+                                      or w.demands != v.demands):
+                bad.append((i, "keys"))
+    assert not bad, bad[:5]

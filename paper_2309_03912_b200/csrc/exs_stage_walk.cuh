@@ -3,7 +3,7 @@
 // __CUDA_ARCH__ divergence (reference: spacecheck.py:254-767).
 #pragma once
 #include "exs_stage_sema.cuh"
-#include "exs_fastwalk.cuh"
+#include "exs_walk.cuh"
 
 namespace exs {
 
@@ -21,7 +21,6 @@ constexpr u32 CNT_STRIDE = 32;
 struct WalkState {
   u32 cap_inst = 0, n_inst = 0, levels = 0;
   u32 buf_scale = 1;  // multiplier of the creation-log estimate (grows on overflow)
-  bool fast = true;   // common statement shapes on the register-resident walker (exs_fastwalk.cuh)
   u64 n_edges = 0, edge_cap = 0, callsites = 0;
   Slot* slots = nullptr;
   u32 mask = 0;
@@ -74,57 +73,6 @@ struct RootCand {
   u16 sf;                // specifier bits of the owning struct
   Val ot;
 };
-
-// the fast-path walker of one work item (statement k of instance id), or false
-// when the item needs the general walker (exs_fastwalk.cuh)
-#ifndef EXS_FAST_WALK
-#define EXS_FAST_WALK 1
-#endif
-EXS_HD EXS_FI bool fast_item(const WalkCfg& C, const WalkBufs& B, u32 id, u64 rank, const u32* stmt_node,
-                             const u32* stmt_cs, u32 k) {
-  const Inst& I = B.inst[id];
-  const FnRec& fr = C.fns[I.fn];
-  const Node& fn = C.nodes[fr.node];
-  if (k == 0 && fn.c1 != NONE) return false;  // parameter types are resolved (and reported) by the first item
-  FastWalk w;
-  w.T = C.tab;
-  w.B = &B;
-  w.view = fr.view;
-  w.file = C.vfile[fr.view];
-  const u8 c = C.cfg[w.file];
-  w.mode = c & CFG_MODE_MASK;
-  w.plain = (c & CFG_PLAIN) != 0;
-  w.relaxed = (c & CFG_RELAXED) != 0;
-  w.walk = I.walk;
-  w.inst_id = id;
-  w.ebase = I.ebase;
-  w.clevel = B.clevel;
-  w.parent_rank = rank;
-  w.side = I.side;
-  w.native = (u8)(I.walk & 1);
-  w.from_hd = I.spaces == 3;
-  w.fidelity_host = w.mode == MODE_FIDELITY && w.native == 0;
-  w.stmt_cs_base = stmt_cs[fr.stmt_base + k];
-  w.stmt_ord = 0;
-  w.stmt_ord_max = 2u * ((k + 1 < fr.nstmts ? stmt_cs[fr.stmt_base + k + 1] : fr.ncalls) - w.stmt_cs_base);
-  w.cs_ord = 0;
-  w.ecnt = 0;
-  w.contract = false;
-  // the walker's env (walker_for): owner HDC binding, then the bindings
-  w.env.n = 0;
-  if (I.orec != NONE && I.ot.k == V_TYPE) {
-    const u32 tp = C.nodes[C.recs[I.orec].node].c0;
-    if (tp != NONE && I.ot.targ) w.env.add(C.nodes[tp].hv, vhdc(I.ot.targ));
-  }
-  for (u32 tp = fn.c0; tp != NONE; tp = C.nodes[tp].next) {
-    const Val& v = C.nodes[tp].sub == 0 ? I.tb : I.hb;
-    if (v.k != V_NONE) w.env.add(C.nodes[tp].hv, v);
-  }
-  if (!w.stmt(stmt_node[fr.stmt_base + k])) return false;
-  if (w.ecnt) at_add(&B.inst[id].ecnt, w.ecnt);
-  if (w.contract) at_or(&B.contract[w.file], 1);
-  return true;
-}
 
 // build a walker for an existing instance
 EXS_HD inline void walker_for(Walker& w, const WalkCfg& C, const WalkBufs& B, u32 id, u64 rank) {
@@ -611,15 +559,11 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         dfree(wk); dfree(pos); dfree(wfirst);
       }
       const u32* frk = frank;
-      const bool fast = W.fast;
       const u32* pm = perm;
       EXS_TAG("walk_chunks");
       par_for_walk(nwi, [=] EXS_HD (i64 ii) {
         const u32 i = pm ? pm[ii] : (u32)ii;
         const u32 j = itj[i], c = itc[i];
-#if EXS_FAST_WALK
-        if (KCH == 1 && fast && fast_item(Cc, B, fl[j], frk ? (u64)frk[j] : (u64)j, sn, scs, c)) return;
-#endif
         Walker w;
         walker_for(w, Cc, B, fl[j], frk ? (u64)frk[j] : (u64)j);
         const FnRec& r = fr[w.fn];

@@ -210,7 +210,6 @@ struct Handle {
   long long select_flagged_min = EXS_SELECT_FLAGGED_MIN;  // select_idx flag-pass threshold (indices)
   bool diag_sort_two_pass = false;  // force the two-key diagnostic sort (parity tests)
   bool keep_records = false;        // also keep the raw records (exs_get_diags / exs_diags_view)
-  bool fast_walk = true;            // the register-resident walker for common statements (option 9)
   // rendered results of the last run (all its batches), in unit order
   PinnedBuf res, text;
   u64 n_res = 0, text_bytes = 0, static_bytes = 0;
@@ -512,8 +511,8 @@ static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u
   const u8* kp = keep;
   const u32 nk = select_idx(nd, [=] EXS_HD (u32 k) -> bool { return kp[k] != 0; }, kidx, H.L.cnt, H.sc, st);
   ResRec* rr = dalloc<ResRec>((u64)nk + 1);
-  u32* fcnt = dalloc<u32>((u64)n_files + 1);
-  dzero(fcnt, 4ull * (n_files + 1), st);
+  u32* fcnt = dalloc<u32>(2ull * n_files + 1);  // per file: first record, end
+  dzero(fcnt, 8ull * n_files + 4, st);
   EXS_TAG("results");
   par_for(nk, [=] EXS_HD (i64 j) {
     const u32 x = ord[kidx[j]];
@@ -525,16 +524,26 @@ static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u
     r.code = d.code; r.suppressed = d.suppressed;
     for (int q = 0; q < 5; q++) r.pad[q] = 0;
     rr[j] = r;
-    at_add(&fcnt[d.file], 1);
   }, st);
+  // records are in file order: per-file ranges from the boundaries (no
+  // counter shared by all records of a huge unit)
+  {
+    const ResRec* rc = rr;
+    const u64 ub = unit_base;
+    par_for(nk, [=] EXS_HD (i64 j) {
+      const u32 f = (u32)(rc[j].unit - ub);
+      if (j == 0 || rc[j - 1].unit != rc[j].unit) fcnt[2 * f] = (u32)j;
+      if (j + 1 == (i64)nk || rc[j + 1].unit != rc[j].unit) fcnt[2 * f + 1] = (u32)j + 1;
+    }, st);
+  }
   H.res.ensure((H.n_res + nk) * sizeof(ResRec), H.n_res * sizeof(ResRec));
   H.text.ensure(H.text_bytes + total, H.text_bytes);
-  std::vector<u32> fc(n_files);
+  std::vector<u32> fc(2ull * n_files);
   d2h(H.res.p + H.n_res * sizeof(ResRec), rr, (u64)nk * sizeof(ResRec), st);
   if (total) d2h(H.text.p + H.text_bytes, txt, total, st);
-  d2h(fc.data(), fcnt, 4ull * n_files, st);
+  d2h(fc.data(), fcnt, 8ull * n_files, st);
   sync(st);
-  for (u32 f = 0; f < n_files; f++) H.unit_first[unit_base + f + 1] = fc[f];
+  for (u32 f = 0; f < n_files; f++) H.unit_first[unit_base + f + 1] = fc[2 * f + 1] - fc[2 * f];
   H.n_res += nk;
   H.text_bytes += total;
   dfree(len); dfree(off); dfree(txt); dfree(ord); dfree(keep); dfree(stxt); dfree(kidx); dfree(rr); dfree(fcnt);
@@ -649,7 +658,6 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       H.W = WalkState();
       H.W.cap_inst = cap_inst;
       H.W.buf_scale = buf_scale;
-      H.W.fast = H.fast_walk;
       bool ok = run_walk(L, H.P, H.S, H.W, B0, H.sc, st, cap_diags);
       if (ok && (any_div || H.want_demands)) run_demands(H, any_div);
       walk_ovf = get1(H.W.ctr(CNT_OVF), st);
@@ -1113,7 +1121,6 @@ int exs_set_option(exs_handle x, int key, int value) {
   else if (key == 6) x->h.keep_records = value != 0;        // keep raw records (exs_get_diags)
   else if (key == 7) x->h.batch_cap = (u64)std::min(2047, std::max(1, value)) << 20;  // batch MiB
   else if (key == 8) x->h.pack_threads = value;               // host packing threads (0 = auto)
-  else if (key == 9) x->h.fast_walk = value != 0;             // common statements on the fast walker
   else throw Err("unknown option");
   API_END
 }

@@ -1,10 +1,15 @@
-"""Dev tool: aggregate ncu cuda,sass source view stall samples by source line."""
-import csv, sys, collections
+"""Dev tool: aggregate an ncu `--page source --csv --print-source=cuda,sass`
+export by CUDA source line: warp-stall samples and L2 local / global sectors.
+    python tests/emu/src_hot.py export.csv [top]"""
+import collections
+import csv
+import sys
+
 rows = list(csv.reader(open(sys.argv[1])))
-cur_file = None
-agg = collections.Counter()
-lines = {}
-hdr = None
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+cur_file, hdr = None, None
+samp, loc, glob = collections.Counter(), collections.Counter(), collections.Counter()
+text = {}
 for r in rows:
     if not r:
         continue
@@ -13,15 +18,23 @@ for r in rows:
         continue
     if r[0] == "Line No":
         hdr = r
+        ix = {h: i for i, h in enumerate(r)}
         continue
-    if hdr and len(r) >= 5 and r[0].isdigit():
-        try:
-            s = int(r[4] or 0)
-        except ValueError:
-            continue
+    if hdr and r[0].isdigit() and len(r) == len(hdr):
         key = f"{cur_file}:{r[0]}"
-        agg[key] += s
-        lines[key] = r[1].strip()[:90]
-tot = sum(agg.values()) or 1
-for k, v in agg.most_common(int(sys.argv[2]) if len(sys.argv) > 2 else 30):
-    print(f"{100*v/tot:5.1f}% {k:28s} {lines[k]}")
+
+        def num(name):
+            v = r[ix[name]] if name in ix else ""
+            try:
+                return float(v.replace(",", "")) if v else 0.0
+            except ValueError:
+                return 0.0
+        samp[key] += num("Warp Stall Sampling (All Samples)")
+        loc[key] += num("L2 Theoretical Sectors Local")
+        glob[key] += num("L2 Theoretical Sectors Global")
+        text[key] = r[1].strip()[:80]
+for title, c in (("stall samples", samp), ("L2 local sectors", loc), ("L2 global sectors", glob)):
+    tot = sum(c.values()) or 1
+    print(f"== {title} (total {tot:.3g})")
+    for k, v in c.most_common(top):
+        print(f"{100 * v / tot:5.1f}% {k:26s} {text.get(k, '')}")

@@ -368,33 +368,3 @@ def test_logical_shards_merge_to_the_one_shard_run(X, n_shards):
         rows = lambda r: [(d.code, d.loc.line, d.loc.col, d.message, d.suppressed) for d in r.diagnostics(u)]  # noqa
         assert rows(res_m) == rows(res_w)
 
-
-def test_fast_walker_equals_the_general_walker(X):
-    """The register-resident walker of the common statement shapes
-    (csrc/exs_fastwalk.cuh) and the general walker give the same diagnostics,
-    walk counts and walk keys on every golden unit and on C2-C5 corpora."""
-    from paper_2309_03912_b200 import synth
-    modes = ["classic", "sound", "proposal2", "fidelity", "proposal1"]
-    texts = ([synth.gen_c2_file(s, 50_000) for s in range(20)] +
-             [synth.gen_c5_file(s, 50_000, 0.3) for s in range(20)] +
-             [synth.gen_chain(12, 40), synth.gen_callgraph(3000, 10, 1)])
-    units = [(t, f"u{i}.cu", X.CompileProfile(), X.Mode(modes[i % 5]), X.TraitConfig()) for i, t in enumerate(texts)]
-    for g in GOLDEN_GROUPS:
-        units += [unit_of(X, c, "g.mcu") for c in load_golden(g)]
-    fast, general = X.Engine(0), X.Engine(0)
-    general.handle.set_option(9, 0)
-    A = fast.run_batch(units, want_walks=True)
-    B = general.run_batch(units, want_walks=True)
-    bad = []
-    for i, (a, b) in enumerate(zip(A, B)):
-        if as_rows(a) != as_rows(b):
-            bad.append((i, "diags"))
-            continue
-        for side, w in a.walks.items():
-            v = b.walks[side]
-            if (w.n_instances, w.n_edges, w.n_demands) != (v.n_instances, v.n_edges, v.n_demands):
-                bad.append((i, "counts"))
-            elif i >= len(texts) and (w.instances.keys() != v.instances.keys() or w.edges != v.edges
-                                      or w.demands != v.demands):
-                bad.append((i, "keys"))
-    assert not bad, bad[:5]

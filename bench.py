@@ -281,7 +281,7 @@ def run_reference_arm(a, rank, world):
         return
     cores = os.cpu_count() or 1
     kind = reference_kind()
-    n = max(cores * 8, 32) if a.config in ("c2", "c5") else 1
+    n = (a.ref_files or max(cores * 8, 32)) if a.config in ("c2", "c5") else 1
     vals = []
     if a.config in ("c2", "c5"):
         # the files the GPU arm times (rank 0's seeds), a window per step
@@ -537,6 +537,7 @@ def main():
     ap.add_argument("--c5-gb", type=float, default=8.0)
     ap.add_argument("--c5-pool", type=int, default=2000)
     ap.add_argument("--parity-files", type=int, default=64)
+    ap.add_argument("--ref-files", type=int, default=0, help="reference arm: files per step (0: 8 per core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     a = ap.parse_args()

@@ -73,12 +73,32 @@ _AS_UTF8.argtypes = [C.py_object, C.POINTER(C.c_ssize_t)]
 _AS_UTF8.restype = C.c_void_p
 
 
+def _ascii_data_offset():
+    """Offset of a compact ASCII str's characters from the object address
+    (CPython: sizeof(PyASCIIObject), PyUnicode_DATA of a compact ASCII string),
+    verified on probe strings; None if this interpreter lays strings out
+    differently (text_pointers then asks CPython per string)."""
+    probes = ["exs-probe", "x" * 257, "".join(chr(97 + k % 26) for k in range(64))]
+    for off in (40, 48, 32, 56, 24):
+        if all(C.string_at(id(p) + off, len(p)) == p.encode("ascii") for p in probes):
+            return off
+    return None
+
+
+_ASCII_OFF = _ascii_data_offset()
+
+
 def text_pointers(texts):
     """(pointer array, length array, keep-alive list) for a list of str/bytes
-    without copying them: a str's UTF-8 form is CPython's own buffer (the
-    string's data for ASCII text); text with lone surrogates is encoded with
-    surrogateescape (the reference's byte view of such input)."""
+    without copying them: an ASCII str's characters are its UTF-8 bytes, read
+    in place; other strs give CPython's cached UTF-8 form; text with lone
+    surrogates is encoded with surrogateescape (the reference's byte view of
+    such input)."""
     n = len(texts)
+    if _ASCII_OFF is not None and n and all(type(t) is str for t in texts) and all(map(str.isascii, texts)):
+        ptrs = np.fromiter(map(id, texts), dtype=np.uint64, count=n) + np.uint64(_ASCII_OFF)
+        lens = np.fromiter(map(len, texts), dtype=np.uint64, count=n)
+        return ptrs, lens, []
     ptrs = np.zeros(n, dtype=np.uint64)
     lens = np.zeros(n, dtype=np.uint64)
     keep = []

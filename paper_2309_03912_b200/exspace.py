@@ -12,6 +12,7 @@ from __future__ import annotations
 import threading
 from dataclasses import dataclass, field
 from enum import Enum
+from collections.abc import Sequence
 from typing import Iterable, Optional
 
 import numpy as np
@@ -362,6 +363,38 @@ class Analysis:
         return f"Analysis(path={self.path!r}, mode={self.mode}, diagnostics={len(self.diagnostics)})"
 
 
+class AnalysisList(Sequence):
+    """The Analysis of every unit of one run, in input order, each built on
+    first access (a corpus run returns ~10k of them per GB)."""
+
+    def __init__(self, units: list, results: CorpusResults):
+        self._units = units
+        self._results = results
+        self._made: dict = {}
+
+    def __len__(self):
+        return len(self._units)
+
+    def _get(self, i: int) -> "Analysis":
+        a = self._made.get(i)
+        if a is None:
+            u = self._units[i]
+            a = self._made[i] = Analysis(u[1], u[2], u[3], self._results, i)
+        return a
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._get(k) for k in range(*i.indices(len(self._units)))]
+        if i < 0:
+            i += len(self._units)
+        if not 0 <= i < len(self._units):
+            raise IndexError(i)
+        return self._get(i)
+
+    def __iter__(self):
+        return (self._get(i) for i in range(len(self._units)))
+
+
 # ---------------------------------------------------------------------------
 # the engine
 
@@ -419,6 +452,8 @@ class Engine:
                 batch = BatchWalks(self.handle, ren, status, [u[3] for u in units])
                 batch._load()
                 self.handle.set_option(7, self.batch_mib)
+        if walks is None:
+            return AnalysisList(units, results)
         out = []
         for f, u in enumerate(units):
             a = Analysis(u[1], u[2], u[3], results, f, batch)
@@ -514,7 +549,7 @@ def stray_set(analysis: Analysis) -> list:
 
 
 __all__ = [
-    "Analysis", "CODE_REGISTRY", "CompileProfile", "CorpusResults", "Diagnostic", "Engine", "ExecSpace", "GLOBAL",
+    "Analysis", "AnalysisList", "CODE_REGISTRY", "CompileProfile", "CorpusResults", "Diagnostic", "Engine", "ExecSpace", "GLOBAL",
     "Mode", "Severity", "SrcLoc", "StructInfo", "TraitConfig", "Verdict", "analyze",
     "analyze_corpus", "check_unit", "declared_spaces", "finish_diagnostics", "format_diagnostic",
     "get_engine", "legality", "propagate_spaces", "stray_set", "stray_text",

@@ -176,3 +176,20 @@ def test_sharded_analysis_gathers_in_path_order_over_gloo():
     units = [(f"f{i:03d}.cu", synth.gen_c5_file(i, 1500 + 400 * (i % 5), 0.3)) for i in range(13)]
     want = [[[d[0], p, d[1], d[2], d[3]] for d in O.check(t, "sound")] for p, t in units]
     assert got == want
+
+
+def test_bench_gpus_n_relaunches_one_rank_per_gpu():
+    """`bench.py --gpus 2` without torchrun re-launches itself under
+    torch.distributed.run (one process per GPU); the reference arm runs on
+    rank 0 only and prints one line with n_gpus 2."""
+    import json
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--impl", "reference",
+                          "--steps", "1", "--warmup", "0", "--ref-files", "2", "--file-bytes", "3000"],
+                         capture_output=True, text=True, env=env, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["cpu_baseline"]["kind"] in ("reference", "port")

@@ -342,6 +342,7 @@ def run_gpu_arm(a, rank, world, local):
     cfgb = X.cfg_byte(prof, X.Mode(mode), X.TraitConfig())
     eng = X.Engine(local, batch_mib=a.batch_mib)
     h = eng.handle
+    h.set_option(9, a.pipelines)
     nbytes = W.nbytes
     resident = a.config != "c5"  # C5 (8 GB per GPU) is measured end to end only
     if resident:
@@ -443,7 +444,7 @@ def run_gpu_arm(a, rank, world, local):
         "data": "synthetic (seeded generators, paper_2309_03912_b200/synth.py)",
         "config": {"workload": W.desc, "config": a.config, "units_per_gpu": len(W.texts),
                    "bytes_per_gpu": nbytes, "parallelism": f"dp{world} (unit shards, no data-path collective)",
-                   "l2": "inputs larger than L2; no flush", "batch_mib": a.batch_mib,
+                   "l2": "inputs larger than L2; no flush", "batch_mib": a.batch_mib, "pipelines": a.pipelines,
                    "value_path": ("exs_run_device (corpus resident in HBM)" if resident
                                   else "= e2e (streamed; the corpus exceeds one device batch)")},
         "edges_per_s": total_edges / (mean_ms / 1e3),
@@ -532,6 +533,7 @@ def main():
     ap.add_argument("--files", type=int, default=10_000)
     ap.add_argument("--file-bytes", type=int, default=100_000)
     ap.add_argument("--batch-mib", type=int, default=256)
+    ap.add_argument("--pipelines", type=int, default=2, help="concurrent batch pipelines on the GPU (1 or 2)")
     ap.add_argument("--c3-structs", type=int, default=10_300)
     ap.add_argument("--c4-funcs", type=int, default=10_000_000)
     ap.add_argument("--c5-gb", type=float, default=8.0)

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(128, EXS_PARSE_MINB) k_for_parse(F f, i64 n) {
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) f(i);
 }
 extern int g_sm_count;
-extern u64 g_launches;
+extern thread_local u64 g_launches;  // per host thread (pipelines run on several)
 // optional per-launch device timing (EXS_PROFILE=1): (site, start, stop) events
 struct ProfRec { const char* fn; int line; cudaEvent_t a, b; };
 extern bool g_profile;

@@ -9,13 +9,15 @@
 #include "../../include/exspace_b200.h"
 #include <chrono>
 #include <map>
+#include <condition_variable>
+#include <memory>
 #include <mutex>
 #include <thread>
 
 namespace exs {
 #ifndef EXS_EMU
 int g_sm_count = 148;
-u64 g_launches = 0;
+thread_local u64 g_launches = 0;
 thread_local cudaStream_t g_alloc_stream = 0;
 bool g_profile = getenv("EXS_PROFILE") != nullptr;
 std::vector<ProfRec> g_prof;
@@ -36,7 +38,26 @@ static BlockCache g_cache;
 
 void* cache_alloc(size_t bytes) {
   bytes = (bytes + 255) & ~size_t(255);
+  // size classes above 1 MiB (three significant bits, <= 12.5% slack): the
+  // batches of a stream differ in size, and exact sizes would never be reused
+  if (bytes > (1u << 20)) {
+    int hb = 63 - __builtin_clzll(bytes);
+    const size_t q = size_t(1) << (hb - 3);
+    bytes = (bytes + q - 1) & ~(q - 1);
+  }
   std::lock_guard<std::mutex> g(g_cache.mu);
+  // keep the cache bounded: past 32 GiB of idle blocks, give this stream's back
+  if (g_cache.cached > (32ull << 30)) {
+    for (auto i = g_cache.free_.begin(); i != g_cache.free_.end();) {
+      if (i->first.first == g_alloc_stream) {
+        cudaFreeAsync(i->second, g_alloc_stream);
+        g_cache.cached -= i->first.second;
+        i = g_cache.free_.erase(i);
+      } else {
+        ++i;
+      }
+    }
+  }
   auto it = g_cache.free_.find({g_alloc_stream, bytes});
   void* p = nullptr;
   if (it != g_cache.free_.end()) {
@@ -137,7 +158,7 @@ static void collect_profile() {
   }
 }
 #else
-u64 g_launches = 0;
+thread_local u64 g_launches = 0;
 #endif
 
 static thread_local std::string g_err;
@@ -215,7 +236,22 @@ struct Handle {
   u64 n_res = 0, text_bytes = 0, static_bytes = 0;
   std::vector<u64> unit_first;      // n_units + 1
   u32* d_static = nullptr;          // per static message key: (offset, length)
-  // streaming driver (exs_run_units): two host staging slots, two device slots
+  // results sink: the handle whose result buffers render_results appends to
+  // (this one, or the owner of a pipeline), batch by batch in batch order
+  Handle* sink = this;
+  u64 cur_batch = 0;
+  struct Turn {
+    std::mutex mu;
+    std::condition_variable cv;
+    u64 next = 0;
+    bool on = false;
+    bool abort = false;  // a pipeline failed: the others stop waiting
+  } turn;
+  // streaming driver (exs_run_units): two host staging slots, two device slots;
+  // with pipelines = 2, a second handle (own stream, own buffers) analyses
+  // every other batch concurrently on the same device
+  std::unique_ptr<Handle> peer;
+  int pipelines = 2;
   u64 batch_cap = 1ull << 30;
   int pack_threads = 0;             // 0: hardware threads (<= 16)
   PinnedBuf stage[2];
@@ -395,7 +431,7 @@ static void run_demands(Handle& H, bool emit_e1201) {
 // K9: messages and finish_diagnostics (diagnostics.py:116-121), results
 
 // results of a new run: the static message section first
-static void results_reset(Handle& H, u64 n_units) {
+static void static_init(Handle& H) {
   if (!H.d_static) {
     // static messages rendered once per handle, on the host, by the same code
     std::vector<u32> tab(2 * EXS_STATIC_KEYS, 0);
@@ -420,6 +456,9 @@ static void results_reset(Handle& H, u64 n_units) {
     h2d(H.d_static, tab.data(), 8ull * EXS_STATIC_KEYS, H.st);
     sync(H.st);
   }
+}
+static void results_reset(Handle& H, u64 n_units) {
+  static_init(H);
   H.n_res = 0;
   H.text_bytes = H.static_bytes;
   H.unit_first.assign(n_units + 1, 0);
@@ -430,7 +469,18 @@ static void results_reset(Handle& H, u64 n_units) {
 static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u64 n_bytes, u32 n_files,
                            u64 unit_base) {
   cudaStream_t st = H.st;
-  if (!nd) return;
+  if (!nd) {
+    Handle& R = *H.sink;
+    if (R.turn.on) {
+      std::unique_lock<std::mutex> lk(R.turn.mu);
+      R.turn.cv.wait(lk, [&] { return R.turn.next == H.cur_batch || R.turn.abort; });
+      if (R.turn.abort) throw Err("another pipeline failed");
+      R.turn.next++;
+      lk.unlock();
+      R.turn.cv.notify_all();
+    }
+    return;
+  }
   const RenderCtx RC{d_src, H.L.splice, H.L.arena, H.S.fns, H.S.recs, H.P.nodes, H.L.toks, H.W.inst,
                      (u32)n_bytes};
   const u32* stab = H.d_static;
@@ -453,8 +503,17 @@ static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u
     Out o{txt + off[i], 0};
     render_message(RC, dd[i], o);
   }, st);
+  // appended in batch order: wait for this batch's turn (pipelines), then the
+  // offsets of its records are known
+  Handle& R = *H.sink;
+  std::unique_lock<std::mutex> turn_lock(R.turn.mu, std::defer_lock);
+  if (R.turn.on) {
+    turn_lock.lock();
+    R.turn.cv.wait(turn_lock, [&] { return R.turn.next == H.cur_batch || R.turn.abort; });
+    if (R.turn.abort) throw Err("another pipeline failed");
+  }
   // message bytes of record i, wherever they live
-  const u64 tbase = H.text_bytes;
+  const u64 tbase = R.text_bytes;
   auto msg_of = [=] EXS_HD (u32 i, const char*& p, u32& n, u64& glob) {
     const int k = static_key(dd[i]);
     if (k >= 0) { glob = stab[2 * k]; n = stab[2 * k + 1]; p = nullptr; }
@@ -536,16 +595,21 @@ static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u
       if (j + 1 == (i64)nk || rc[j + 1].unit != rc[j].unit) fcnt[2 * f + 1] = (u32)j + 1;
     }, st);
   }
-  H.res.ensure((H.n_res + nk) * sizeof(ResRec), H.n_res * sizeof(ResRec));
-  H.text.ensure(H.text_bytes + total, H.text_bytes);
+  R.res.ensure((R.n_res + nk) * sizeof(ResRec), R.n_res * sizeof(ResRec));
+  R.text.ensure(R.text_bytes + total, R.text_bytes);
   std::vector<u32> fc(2ull * n_files);
-  d2h(H.res.p + H.n_res * sizeof(ResRec), rr, (u64)nk * sizeof(ResRec), st);
-  if (total) d2h(H.text.p + H.text_bytes, txt, total, st);
+  d2h(R.res.p + R.n_res * sizeof(ResRec), rr, (u64)nk * sizeof(ResRec), st);
+  if (total) d2h(R.text.p + R.text_bytes, txt, total, st);
   d2h(fc.data(), fcnt, 8ull * n_files, st);
   sync(st);
-  for (u32 f = 0; f < n_files; f++) H.unit_first[unit_base + f + 1] = fc[2 * f + 1] - fc[2 * f];
-  H.n_res += nk;
-  H.text_bytes += total;
+  for (u32 f = 0; f < n_files; f++) R.unit_first[unit_base + f + 1] = fc[2 * f + 1] - fc[2 * f];
+  R.n_res += nk;
+  R.text_bytes += total;
+  if (R.turn.on) {
+    R.turn.next++;
+    turn_lock.unlock();
+    R.turn.cv.notify_all();
+  }
   dfree(len); dfree(off); dfree(txt); dfree(ord); dfree(keep); dfree(stxt); dfree(kidx); dfree(rr); dfree(fcnt);
 }
 
@@ -946,6 +1010,87 @@ struct BatchPlan {
   std::vector<u64> off;  // unit offsets within the batch (u1 - u0 + 1)
 };
 
+static void add_stats(exs_stats& acc, const exs_stats& s) {
+  acc.bytes += s.bytes; acc.files += s.files; acc.lines += s.lines; acc.directives += s.directives;
+  acc.tokens += s.tokens; acc.views += s.views; acc.view_tokens += s.view_tokens; acc.items += s.items;
+  acc.functions += s.functions; acc.structs += s.structs; acc.instances += s.instances;
+  acc.edges += s.edges; acc.callsites += s.callsites; acc.levels = std::max(acc.levels, s.levels);
+  acc.diagnostics += s.diagnostics; acc.retries += s.retries; acc.gpu_launches += s.gpu_launches;
+  acc.ms_lex += s.ms_lex; acc.ms_parse += s.ms_parse; acc.ms_sema += s.ms_sema; acc.ms_walk += s.ms_walk;
+  acc.ms_total += s.ms_total; acc.ms_d2h += s.ms_d2h;
+}
+
+#ifndef EXS_EMU
+// Two pipelines on one device: this handle takes the even batches, a peer
+// handle (own stream, own device buffers) the odd ones, each in its own host
+// thread: pack -> copy -> analyse.  The device runs one pipeline's kernels in
+// the other's host round trips and low-occupancy phases (sorts, scans, small
+// grids); results are appended in batch order (Handle::turn).
+static void run_units_pipelined(Handle& H, const char* const* texts, const uint64_t* lens, u64 n_units,
+                                const u8* cfg, const std::vector<BatchPlan>& plan, u64 maxb) {
+  if (!H.peer) {
+    H.peer.reset(new Handle());
+    Handle& Q = *H.peer;
+    Q.device = H.device;
+    CK(cudaStreamCreateWithFlags(&Q.st, cudaStreamNonBlocking));
+  }
+  Handle& Q = *H.peer;
+  Q.want_demands = H.want_demands; Q.split_min = H.split_min; Q.select_flagged_min = H.select_flagged_min;
+  Q.diag_sort_two_pass = H.diag_sort_two_pass; Q.keep_records = false;
+  const int nthreads = H.pack_threads > 0 ? H.pack_threads
+                                          : (int)std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency() / 2));
+  results_reset(H, n_units);
+  {
+    std::lock_guard<std::mutex> g(H.turn.mu);
+    H.turn.next = 0; H.turn.on = true; H.turn.abort = false;
+  }
+  std::mutex acc_mu;
+  exs_stats acc{};
+  float t_stage[4] = {0, 0, 0, 0};
+  auto t0 = std::chrono::steady_clock::now();
+  auto worker = [&](Handle& P, size_t first, std::string& err) {
+    try {
+      bind_stream(P);
+      static_init(P);
+      P.sink = &H;
+      P.stage[0].ensure(maxb + 64, 0);
+      ensure_slot(P, 0, maxb + 64);
+      for (size_t b = first; b < plan.size(); b += 2) {
+        const BatchPlan& B = plan[b];
+        pack_units(texts, lens, B.u0, B.u1, B.off.data(), P.stage[0].p, nthreads);
+        memset(P.stage[0].p + B.bytes, 0, 64);
+        h2d(P.d_slot[0], P.stage[0].p, B.bytes + 64, P.st);  // same stream as the analysis
+        P.cur_batch = b;
+        run_batch(P, P.d_slot[0], B.bytes, B.off.data(), (u32)(B.u1 - B.u0), cfg + B.u0, B.u0);
+        std::lock_guard<std::mutex> g(acc_mu);
+        add_stats(acc, P.stats);
+        for (int q = 0; q < 4; q++) t_stage[q] += P.t_stage[q];
+      }
+    } catch (const std::exception& e) {
+      err = e.what();
+      std::lock_guard<std::mutex> g(H.turn.mu);
+      H.turn.abort = true;
+      H.turn.cv.notify_all();
+    }
+  };
+  std::string e0, e1;
+  std::thread second([&]() { worker(Q, 1, e1); });
+  worker(H, 0, e0);
+  second.join();
+  bind_stream(H);
+  H.peer->sink = H.peer.get();
+  H.sink = &H;
+  H.turn.on = false;
+  const char* aborted = "another pipeline failed";
+  if (!e0.empty() || !e1.empty()) throw Err(!e0.empty() && e0 != aborted ? e0 : (!e1.empty() ? e1 : e0));
+  results_close(H);
+  acc.batches = plan.size();
+  acc.ms_wall = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  H.stats = acc;
+  for (int q = 0; q < 4; q++) H.t_stage[q] = t_stage[q];
+}
+#endif
+
 static void run_units(Handle& H, const char* const* texts, const uint64_t* lens, u64 n_units, const u8* cfg) {
   if (n_units >= 0xFFFFFFFFull) throw Err("too many units");
   // plan
@@ -974,6 +1119,12 @@ static void run_units(Handle& H, const char* const* texts, const uint64_t* lens,
   }
   u64 maxb = 0;
   for (auto& b : plan) maxb = std::max(maxb, b.bytes);
+#ifndef EXS_EMU
+  if (H.pipelines >= 2 && plan.size() >= 2 && !g_profile && !H.keep_records) {
+    run_units_pipelined(H, texts, lens, n_units, cfg, plan, maxb);
+    return;
+  }
+#endif
   const int nslots = plan.size() > 1 ? 2 : 1;
   for (int k = 0; k < nslots; k++) {
     H.stage[k].ensure(maxb + 64, 0);
@@ -1037,14 +1188,7 @@ static void run_units(Handle& H, const char* const* texts, const uint64_t* lens,
     }
     if (next.joinable()) next.join();
     if (!next_err.empty()) throw Err(next_err);
-    const exs_stats& s = H.stats;
-    acc.bytes += s.bytes; acc.files += s.files; acc.lines += s.lines; acc.directives += s.directives;
-    acc.tokens += s.tokens; acc.views += s.views; acc.view_tokens += s.view_tokens; acc.items += s.items;
-    acc.functions += s.functions; acc.structs += s.structs; acc.instances += s.instances;
-    acc.edges += s.edges; acc.callsites += s.callsites; acc.levels = std::max(acc.levels, s.levels);
-    acc.diagnostics += s.diagnostics; acc.retries += s.retries; acc.gpu_launches += s.gpu_launches;
-    acc.ms_lex += s.ms_lex; acc.ms_parse += s.ms_parse; acc.ms_sema += s.ms_sema; acc.ms_walk += s.ms_walk;
-    acc.ms_total += s.ms_total; acc.ms_d2h += s.ms_d2h;
+    add_stats(acc, H.stats);
     for (int q = 0; q < 4; q++) t_stage[q] += H.t_stage[q];
   }
   results_close(H);
@@ -1121,6 +1265,7 @@ int exs_set_option(exs_handle x, int key, int value) {
   else if (key == 6) x->h.keep_records = value != 0;        // keep raw records (exs_get_diags)
   else if (key == 7) x->h.batch_cap = (u64)std::min(2047, std::max(1, value)) << 20;  // batch MiB
   else if (key == 8) x->h.pack_threads = value;               // host packing threads (0 = auto)
+  else if (key == 9) x->h.pipelines = value < 2 ? 1 : 2;      // concurrent batch pipelines
   else throw Err("unknown option");
   API_END
 }

@@ -702,11 +702,12 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       H.d_diags = ndg; H.d_dset = nset; H.dmask = nmask; H.cap_diags = ncap; cap_diags = ncap;
       B0.diags = ndg; B0.cap_diags = ncap; B0.dset = nset; B0.dmask = nmask;
     };
-    // size it for the walk from the call sites up front: a walk emits at most
-    // about one diagnostic per four call sites on the measured corpora (C4:
-    // 43.7 M from 250 M), and an overflow costs a second walk
+    // size it for the walk from the (static) call sites up front: the walks
+    // emit at most about one diagnostic per two of them on the measured
+    // corpora (C4: 43.7 M from 100 M, both sides walked), and an overflow
+    // costs a second walk
     {
-      const u64 want = std::min<u64>((u64)nd0 + H.S.NCS / 4 + 65536, 0x7FFFFFFFull);
+      const u64 want = std::min<u64>((u64)nd0 + H.S.NCS / 2 + 65536, 0x7FFFFFFFull);
       if (want > cap_diags && nd0 <= cap_diags) regrow((u32)want);
     }
     u64* dset_snap = dalloc<u64>((u64)H.dmask + 1);
@@ -727,6 +728,10 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       walk_ovf = get1(H.W.ctr(CNT_OVF), st);
       (void)ok;
       if (!(walk_ovf & 7)) break;
+      if (getenv("EXS_TRACE_UNITS"))
+        fprintf(stderr, "[run_batch] walk retry: overflow bits %u (1 instances, 2 diagnostics, 4 log/pending/seeds), "
+                "%u diagnostics of %u, %u before the walk, %llu call sites\n", walk_ovf, get1(H.d_ndiags, st),
+                cap_diags, nd0, (unsigned long long)H.S.NCS);
       if ((walk_ovf & 2) && !(get1(ovf, st) & 2) && nd0 <= cap_diags) {
         // diagnostics overflowed inside the walk: grow the buffer and its dedup
         // set, keep the diagnostics of the earlier stages, re-run the walk only
@@ -755,6 +760,9 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     u32 nd = get1(H.d_ndiags, st);
     dfree(ovf);
     if (nd > cap_diags || (ovf_h & 2) || (walk_ovf & 2)) {
+      if (getenv("EXS_TRACE_UNITS"))
+        fprintf(stderr, "[run_batch] batch retry: %u diagnostics, capacity %u, overflow %u/%u\n", nd, cap_diags,
+                ovf_h, walk_ovf);
       cap_diags = (u32)std::min<u64>(4ull * std::max(nd, cap_diags), 0x7FFFFFFFull);
       retries++;
       continue;

@@ -208,12 +208,12 @@ void b() { D{}.call(); }
 
 def test_diagnostic_overflow_regrows_inside_the_walk(X, eng):
     """A unit whose walk emits more diagnostics than the buffer sized from its
-    call sites holds (every call a stray: 120k E1002 against the 1-in-4
+    call sites holds (every call a stray: 120k E1002 against the 1-in-2
     estimate) is re-walked with a grown buffer, keeping the earlier stages'
     diagnostics -- same ordered set as the oracle."""
     lines = [f"void h{i}() {{}}" for i in range(10)]
     lines += [f"__device__ void f{i}() {{ " + " ".join(f"h{(i + k) % 10}();" for k in range(10)) + " }"
-              for i in range(12000)]
+              for i in range(16000)]
     lines += ["int main() { return 0; }"]
     text = "\n".join(lines) + "\n"
     a = eng.run_batch([(text, "c4.cu", X.CompileProfile(), X.Mode.SOUND, X.TraitConfig())])[0]

@@ -182,6 +182,18 @@ int exs_results_view(exs_handle h, const exs_result** recs, uint64_t* n, const c
  * exs_results_view; any pointer may be null), with several host threads. */
 int exs_results_copy(exs_handle h, exs_result* recs, char* text, uint64_t* unit_first);
 
+/* One batch walked across ranks (one huge unit, C4): every
+ * rank runs the front end on the same batch, walks its share of every level's
+ * work items, and the ranks exchange the level's new instances, then the edge
+ * slots, launch seeds and diagnostics -- all through fn, an all-gather of
+ * variable-size DEVICE buffers (recv gets every rank's bytes in rank order,
+ * recv_sizes[r] from rank r; return 0 on success).  The host supplies it:
+ * NCCL through torch.distributed (paper_2309_03912_b200/shard.py).  Every
+ * rank ends with the same results.  world = 1 (the default) walks alone. */
+typedef int (*exs_allgather_fn)(void* ctx, const void* send, uint64_t send_bytes, void* recv,
+                                const uint64_t* recv_sizes);
+int exs_set_collective(exs_handle h, int rank, int world, exs_allgather_fn fn, void* ctx);
+
 int exs_get_stats(exs_handle h, exs_stats* out);
 /* raw records ordered by (file, line, col, code), duplicates removed (only
  * kept with option 6; the rendered form is exs_results_view) */

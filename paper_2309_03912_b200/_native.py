@@ -60,8 +60,11 @@ EXPORTS = [
     "exs_get_diags", "exs_diags_view", "exs_get_arena", "exs_get_pass_status", "exs_get_tokens",
     "exs_get_walk_stats", "exs_describe", "exs_set_option", "exs_stage_times", "exs_profile_text",
     "exs_get_decls", "exs_get_structs", "exs_get_instances", "exs_get_edges", "exs_get_nodes",
-    "exs_get_token_range", "exs_run_units", "exs_results_view", "exs_results_copy",
+    "exs_get_token_range", "exs_run_units", "exs_results_view", "exs_results_copy", "exs_set_collective",
 ]
+
+# exs_allgather_fn (include/exspace_b200.h)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_uint64))
 
 # one finished diagnostic (include/exspace_b200.h exs_result)
 RESULT_DTYPE = np.dtype([("unit", "<u4"), ("line", "<u4"), ("col", "<u4"), ("msg_len", "<u4"),
@@ -166,6 +169,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     lib.exs_stage_times.argtypes = [vp, C.POINTER(C.c_float)]
     lib.exs_run_units.argtypes = [vp, vp, vp, C.c_uint64, vp]
     lib.exs_results_copy.argtypes = [vp, vp, vp, vp]
+    lib.exs_set_collective.argtypes = [vp, C.c_int, C.c_int, ALLGATHER_FN, vp]
     lib.exs_results_view.argtypes = [vp, C.POINTER(C.c_void_p), u64p, C.POINTER(C.c_void_p), u64p,
                                      C.POINTER(C.c_void_p), u64p]
     for name in EXPORTS:
@@ -250,6 +254,13 @@ class Handle:
         text = view(tp, tb.value)
         first = view(up, (nu.value + 1) * 8) if up.value else np.zeros(8, dtype=np.uint8)
         return recs.view(RESULT_DTYPE), text, first.view(np.uint64)
+
+    def set_collective(self, rank: int, world: int, allgather=None):
+        """Walk every batch across `world` ranks (exs_set_collective);
+        `allgather` is an ALLGATHER_FN (kept alive here)."""
+        self._allgather = allgather
+        self._check(self.lib.exs_set_collective(self.h, rank, world,
+                                                allgather if allgather is not None else ALLGATHER_FN(0), None))
 
     def stats(self) -> dict:
         s = Stats()

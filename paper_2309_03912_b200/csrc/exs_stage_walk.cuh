@@ -18,9 +18,59 @@ namespace exs {
 enum { CNT_INST = 0, CNT_PEND = 1, CNT_SEEDS = 2, CNT_LOG = 3, CNT_OVF = 4, CNT_N = 5 };
 constexpr u32 CNT_STRIDE = 32;
 
+// The collective of one unit walked across GPUs: an
+// all-gather of variable-size device buffers, supplied by the host (NCCL
+// through torch.distributed on GPUs; gloo in the CPU tests).  recv receives
+// every rank's buffer in rank order, sizes[r] bytes from rank r.
+typedef int (*CollFn)(void* ctx, const void* send, u64 send_bytes, void* recv, const u64* sizes);
+struct Coll {
+  int rank = 0, world = 1;
+  CollFn fn = nullptr;
+  void* ctx = nullptr;
+  bool on() const { return world > 1 && fn != nullptr; }
+};
+// all-gather of this rank's bytes: the concatenation (dalloc'd) and per-rank sizes
+inline u8* coll_allgatherv(const Coll& c, const void* send, u64 bytes, std::vector<u64>& sizes, u64& total,
+                           cudaStream_t st) {
+  sync(st);
+  u64* mine = dalloc<u64>(1);
+  u64* all = dalloc<u64>(c.world);
+  h2d(mine, &bytes, 8, st);
+  sync(st);
+  std::vector<u64> eight(c.world, 8);
+  if (c.fn(c.ctx, mine, 8, all, eight.data())) throw Err("collective (sizes) failed");
+  sizes.assign(c.world, 0);
+  d2h(sizes.data(), all, 8ull * c.world, st);
+  sync(st);
+  total = 0;
+  for (u64 v : sizes) total += v;
+  u8* recv = dalloc<u8>(total + 1);
+  if (c.fn(c.ctx, send, bytes, recv, sizes.data())) throw Err("collective failed");
+  dfree(mine);
+  dfree(all);
+  return recv;
+}
+// OR of a flag word over the ranks
+inline u32 coll_or(const Coll& c, u32 v, cudaStream_t st) {
+  u32* d = dalloc<u32>(1);
+  h2d(d, &v, 4, st);
+  std::vector<u64> sz;
+  u64 tot;
+  u8* r = coll_allgatherv(c, d, 4, sz, tot, st);
+  std::vector<u32> h(c.world);
+  d2h(h.data(), r, 4ull * c.world, st);
+  sync(st);
+  dfree(d);
+  dfree(r);
+  u32 o = 0;
+  for (u32 x : h) o |= x;
+  return o;
+}
+
 struct WalkState {
   u32 cap_inst = 0, n_inst = 0, levels = 0;
   u32 buf_scale = 1;  // multiplier of the creation-log estimate (grows on overflow)
+  Coll coll;          // one unit across GPUs: work items split by rank, exchanges per level
   u64 n_edges = 0, edge_cap = 0, callsites = 0;
   Slot* slots = nullptr;
   u32 mask = 0;
@@ -172,6 +222,98 @@ inline void grow_inst(WalkState& W, u64 need, u32 n, cudaStream_t st) {
   dfree(W.inst); dfree(W.slots);
   W.inst = in; W.slots = slots;
   W.cap_inst = cap; W.mask = mask;
+}
+
+// a reference to an instance across ranks: (walk, creation key) -- creation
+// keys are unique within a walk -- plus a position (edge slot) or the seed's walk
+struct XRef {
+  unsigned long long key;
+  u32 walk, a;
+};
+
+// One level's exchange of a sharded walk: every rank's new instance records
+// (the ones its work items created, [prev_n, n_now) here) are merged into
+// every rank's table -- a key seen for the first time is inserted, and the
+// minimum creation key over all creators wins, with its location and decl
+// (spacecheck.py:331-337) -- so every rank continues with the same instance
+// set and the same frontier order.  Ids stay rank-local: references across
+// ranks go by creation key, which is unique per instance.  Returns the OR of
+// the ranks' overflow flags; n_now becomes the merged instance count.
+inline u32 merge_level(WalkState& W, u32 prev_n, u32& n_now, bool ovf_local, cudaStream_t st) {
+  const Coll& c = W.coll;
+  const u64 nrec = ovf_local ? 0 : (u64)(n_now - prev_n);
+  const u64 bytes = 8 + nrec * sizeof(Inst);
+  u8* send = dalloc<u8>(bytes);
+  const u64 hdr = ovf_local ? 1 : 0;
+  h2d(send, &hdr, 8, st);
+  if (nrec) d2d(send + 8, W.inst + prev_n, nrec * sizeof(Inst), st);
+  std::vector<u64> sizes;
+  u64 total = 0;
+  u8* recv = coll_allgatherv(c, send, bytes, sizes, total, st);
+  dfree(send);
+  std::vector<u64> offs(c.world, 0);
+  u32 any = 0;
+  u64 incoming = 0;
+  for (int r = 0; r < c.world; r++) {
+    offs[r] = r ? offs[r - 1] + sizes[r - 1] : 0;
+    u64 h = 0;
+    d2h(&h, recv + offs[r], 8, st);
+    sync(st);
+    any |= (u32)h;
+    if (r != c.rank) incoming += (sizes[r] - 8) / sizeof(Inst);
+  }
+  if (any) { dfree(recv); return 1; }
+  grow_inst(W, (u64)n_now + incoming + 1024, n_now, st);  // ids and slots for the incoming records
+  WalkBufs B{};
+  B.slots = W.slots; B.mask = W.mask; B.inst = W.inst; B.n_inst = W.ctr(CNT_INST); B.cap_inst = W.cap_inst;
+  B.overflow = W.ctr(CNT_OVF);
+  {
+    // this rank's level minimum back into the slots (a rehash dropped it)
+    Inst* in = W.inst; Slot* sl = W.slots; const u32 base = prev_n;
+    par_for(n_now - prev_n, [=] EXS_HD (i64 j) { const Inst& I = in[base + j]; sl[I.slot].sck = I.ckey; }, st);
+  }
+  for (int r = 0; r < c.world; r++) {
+    if (r == c.rank) continue;
+    const u64 cnt = (sizes[r] - 8) / sizeof(Inst);
+    const Inst* rr = reinterpret_cast<const Inst*>(recv + offs[r] + 8);
+    // insert or find, and keep the minimum creation key per slot
+    par_for(cnt, [=] EXS_HD (i64 k) {
+      const Inst R = rr[k];
+      IKey key;
+      key.a = R.ka; key.b = R.kb;
+      bool ins;
+      u32 slot;
+      const u32 id = inst_lookup_or_insert(B, key, ins, slot);
+      if (id == NONE) return;
+      if (ins) {
+        Inst I = R;
+        I.slot = slot; I.ebase = 0; I.ecnt = 0;
+        B.inst[id] = I;
+        inst_publish(B, slot, id);
+      }
+      at_min64(&B.slots[slot].sck, R.ckey);
+    }, st);
+  }
+  for (int r = 0; r < c.world; r++) {
+    if (r == c.rank) continue;
+    const u64 cnt = (sizes[r] - 8) / sizeof(Inst);
+    const Inst* rr = reinterpret_cast<const Inst*>(recv + offs[r] + 8);
+    // the winning creator's data (one record per minimum)
+    par_for(cnt, [=] EXS_HD (i64 k) {
+      const Inst& R = rr[k];
+      IKey key;
+      key.a = R.ka; key.b = R.kb;
+      bool ins;
+      const u32 slot = slot_insert(B, key, ins);
+      if (slot == NONE || B.slots[slot].sck != R.ckey) return;
+      Inst& I = B.inst[B.slots[slot].sid];
+      I.ckey = R.ckey; I.at = R.at; I.fn = R.fn;
+    }, st);
+  }
+  sync(st);
+  dfree(recv);
+  n_now = get1(W.ctr(CNT_INST), st);
+  return get1(W.ctr(CNT_OVF), st) ? 1u : 0u;
 }
 
 // returns false if a buffer overflowed (caller grows and retries)
@@ -415,24 +557,33 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   W.callsites = 0;
   while (true) {
     std::vector<u32> cnt = W.read_counters(st);
-    if (cnt[CNT_OVF]) { dfree(dtab); dfree(front); return false; }
+    const bool ovf_local = cnt[CNT_OVF] != 0;
+    if (ovf_local && !W.coll.on()) { dfree(dtab); dfree(front); return false; }
     u32 n_now = cnt[CNT_INST];
     prof_mark(st);
-    // creation keys of this level's instances (min over creators), then the
-    // first creator's location (spacecheck.py:331-337)
-    {
-      Inst* in = W.inst; const Slot* sl = W.slots; const u32 base = prev_n;
-      par_for(n_now - prev_n, [=] EXS_HD (i64 j) { Inst& I = in[base + j]; I.ckey = sl[I.slot].sck; }, st);
-    }
-    {
-      const CreateLog* lg = W.log; Inst* in = W.inst;
-      par_for(cnt[CNT_LOG], [=] EXS_HD (i64 j) {
-        const CreateLog& e = lg[j];
-        Inst& I = in[e.inst];
-        if (I.ckey == e.ckey) { I.at = e.at; I.fn = e.fn; }
-      }, st);
+    if (!ovf_local) {
+      // creation keys of this level's instances (min over creators), then the
+      // first creator's location (spacecheck.py:331-337)
+      {
+        Inst* in = W.inst; const Slot* sl = W.slots; const u32 base = prev_n;
+        par_for(n_now - prev_n, [=] EXS_HD (i64 j) { Inst& I = in[base + j]; I.ckey = sl[I.slot].sck; }, st);
+      }
+      {
+        const CreateLog* lg = W.log; Inst* in = W.inst;
+        par_for(cnt[CNT_LOG], [=] EXS_HD (i64 j) {
+          const CreateLog& e = lg[j];
+          Inst& I = in[e.inst];
+          if (I.ckey == e.ckey) { I.at = e.at; I.fn = e.fn; }
+        }, st);
+      }
     }
     dzero(W.ctr(CNT_LOG), 4, st);
+    // a sharded walk: the ranks' new instances of the level just walked are
+    // merged everywhere (the roots, level 0, are built alike on every rank)
+    if (W.coll.on() && level > 0 && merge_level(W, prev_n, n_now, ovf_local, st)) {
+      dfree(dtab); dfree(front); return false;
+    }
+    B = bufs();
     u32 nnew = n_now - prev_n;
     if (!nnew) break;
     prof_mark(st);
@@ -560,8 +711,15 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       }
       const u32* frk = frank;
       const u32* pm = perm;
+      // a sharded walk: this rank's contiguous share of the (shape-ordered) items
+      u64 it_lo = 0, it_hi = nwi;
+      if (W.coll.on()) {
+        it_lo = (u64)nwi * (u64)W.coll.rank / (u64)W.coll.world;
+        it_hi = (u64)nwi * (u64)(W.coll.rank + 1) / (u64)W.coll.world;
+      }
       EXS_TAG("walk_chunks");
-      par_for_walk(nwi, [=] EXS_HD (i64 ii) {
+      par_for_walk((i64)(it_hi - it_lo), [=] EXS_HD (i64 ii0) {
+        const i64 ii = ii0 + (i64)it_lo;
         const u32 i = pm ? pm[ii] : (u32)ii;
         const u32 j = itj[i], c = itc[i];
         Walker w;
@@ -593,6 +751,106 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   dfree(front);
   W.n_inst = prev_n;
   W.n_edges = edges_used;
+  if (W.coll.on()) {
+    // a sharded walk: the edge slots and launch seeds each rank wrote for its
+    // work items go to every rank (edge positions agree across ranks; callees
+    // travel as creation keys and come back as local ids), then every
+    // instance's legal-edge count is recounted from the merged slots
+    const Coll& c = W.coll;
+    const u32 n = W.n_inst;
+    // instances ordered by (walk, creation key): two stable radix sorts
+    u64* ck = dalloc<u64>((u64)n + 1);
+    u64* wk = dalloc<u64>((u64)n + 1);
+    u32* cid = dalloc<u32>((u64)n + 1);
+    {
+      const Inst* in = W.inst;
+      par_for(n, [=] EXS_HD (i64 i) { ck[i] = in[i].ckey; cid[i] = (u32)i; }, st);
+      sort_pairs(ck, cid, n, sc, st);
+      const u32* ci = cid;
+      par_for(n, [=] EXS_HD (i64 i) { wk[i] = in[ci[i]].walk; }, st);
+      sort_pairs(wk, cid, n, sc, st, 32);
+      par_for(n, [=] EXS_HD (i64 i) { ck[i] = in[ci[i]].ckey; }, st);
+    }
+    auto id_of = [=] EXS_HD (u32 walk, u64 key) -> u32 {  // binary search of (walk, creation key)
+      u32 lo = 0, hi = n;
+      while (lo < hi) {
+        const u32 mid = (lo + hi) / 2;
+        if (wk[mid] < walk || (wk[mid] == walk && ck[mid] < key)) lo = mid + 1; else hi = mid;
+      }
+      return lo < n && wk[lo] == walk && ck[lo] == key ? cid[lo] : NONE;
+    };
+    {
+      // edges: (position, callee creation key)
+      u32* pos = dalloc<u32>(edges_used + 1);
+      const u32* ed = W.edges;
+      const u32 ne = select_idx((i64)edges_used, [=] EXS_HD (u32 p) -> bool { return ed[p] != NONE; }, pos, L.cnt,
+                                sc, st);
+      XRef* xs = dalloc<XRef>((u64)ne + 1);
+      const Inst* in = W.inst; const u32* ps = pos;
+      par_for(ne, [=] EXS_HD (i64 k) {
+        const Inst& I = in[ed[ps[k]]];
+        XRef x; x.key = I.ckey; x.walk = I.walk; x.a = ps[k]; xs[k] = x;
+      }, st);
+      std::vector<u64> sizes;
+      u64 total = 0;
+      u8* recv = coll_allgatherv(c, xs, sizeof(XRef) * (u64)ne, sizes, total, st);
+      u64 off = 0;
+      u32* edw = W.edges;
+      for (int r = 0; r < c.world; off += sizes[r], r++) {
+        if (r == c.rank) continue;
+        const XRef* rx = reinterpret_cast<const XRef*>(recv + off);
+        par_for(sizes[r] / sizeof(XRef), [=] EXS_HD (i64 k) { edw[rx[k].a] = id_of(rx[k].walk, rx[k].key); }, st);
+      }
+      sync(st);
+      dfree(recv); dfree(xs); dfree(pos);
+    }
+    {
+      // launch seeds: (walk, target creation key)
+      std::vector<u32> cnt = W.read_counters(st);
+      const u32 ns = std::min<u32>(cnt[CNT_SEEDS], W.cap_seeds);
+      XRef* xs = dalloc<XRef>((u64)ns + 1);
+      const Inst* in = W.inst; const u32* sd = W.seeds;
+      par_for(ns, [=] EXS_HD (i64 k) {
+        const Inst& I = in[sd[2 * k + 1]];
+        XRef x; x.key = I.ckey; x.walk = I.walk; x.a = sd[2 * k]; xs[k] = x;
+      }, st);
+      std::vector<u64> sizes;
+      u64 total = 0;
+      u8* recv = coll_allgatherv(c, xs, sizeof(XRef) * (u64)ns, sizes, total, st);
+      const u64 all = total / sizeof(XRef);
+      grow(W.seeds, seed_cap, 2ull * all + 64, 2ull * ns, st);
+      W.cap_seeds = (u32)(seed_cap / 2);
+      u64 off = 0, at = ns;
+      u32* sw = W.seeds;
+      for (int r = 0; r < c.world; off += sizes[r], r++) {
+        if (r == c.rank) continue;
+        const XRef* rx = reinterpret_cast<const XRef*>(recv + off);
+        const u64 m = sizes[r] / sizeof(XRef), a0 = at;
+        par_for(m, [=] EXS_HD (i64 k) {
+          sw[2 * (a0 + k)] = rx[k].a;
+          sw[2 * (a0 + k) + 1] = id_of(rx[k].walk, rx[k].key);
+        }, st);
+        at += m;
+      }
+      const u32 nsn = (u32)at;
+      h2d(W.ctr(CNT_SEEDS), &nsn, 4, st);
+      sync(st);
+      dfree(recv); dfree(xs);
+    }
+    {
+      Inst* in = W.inst; const FnRec* fr = S.fns; const u32* ed = W.edges;
+      par_for(n, [=] EXS_HD (i64 i) {
+        Inst& I = in[i];
+        if (!(I.flags & IF_BODY)) return;
+        const u32 ns = fr[I.fn].ncalls;
+        u32 k = 0;
+        for (u32 e = 0; e < ns; e++) k += ed[I.ebase + e] != NONE;
+        I.ecnt = k;
+      }, st);
+    }
+    sync(st);
+    dfree(ck); dfree(wk); dfree(cid);
+  }
   prof_mark(st);
   // ---- main instance per walk: the last created (max creation key)
   {

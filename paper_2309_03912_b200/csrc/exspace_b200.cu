@@ -231,6 +231,7 @@ struct Handle {
   long long select_flagged_min = EXS_SELECT_FLAGGED_MIN;  // select_idx flag-pass threshold (indices)
   bool diag_sort_two_pass = false;  // force the two-key diagnostic sort (parity tests)
   bool keep_records = false;        // also keep the raw records (exs_get_diags / exs_diags_view)
+  Coll coll;                        // one batch walked across ranks (exs_set_collective)
   // rendered results of the last run (all its batches), in unit order
   PinnedBuf res, text;
   u64 n_res = 0, text_bytes = 0, static_bytes = 0;
@@ -689,6 +690,11 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     // the walk is retried alone (bigger instance table) after restoring the
     // diagnostics emitted by the earlier stages
     u32 nd0 = get1(H.d_ndiags, st);
+    if (H.coll.on() && H.coll.rank != 0) {
+      // a sharded walk: the replicated front end's diagnostics come from rank 0
+      nd0 = 0;
+      h2d(H.d_ndiags, &nd0, 4, st);
+    }
     // grow the diagnostics buffer and its dedup set, keeping the nd0
     // diagnostics of the earlier stages
     auto regrow = [&](u32 ncap) {
@@ -723,9 +729,12 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
       H.W = WalkState();
       H.W.cap_inst = cap_inst;
       H.W.buf_scale = buf_scale;
+      H.W.coll = H.coll;
       bool ok = run_walk(L, H.P, H.S, H.W, B0, H.sc, st, cap_diags);
-      if (ok && (any_div || H.want_demands)) run_demands(H, any_div);
+      // E1201 of a sharded walk from rank 0 only (every rank holds every instance)
+      if (ok && (any_div || H.want_demands)) run_demands(H, any_div && H.coll.rank == 0);
       walk_ovf = get1(H.W.ctr(CNT_OVF), st);
+      if (H.coll.on()) walk_ovf = coll_or(H.coll, walk_ovf, st);  // every rank retries together
       (void)ok;
       if (!(walk_ovf & 7)) break;
       if (getenv("EXS_TRACE_UNITS"))
@@ -759,7 +768,9 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     u32 ovf_h = get1(ovf, st);
     u32 nd = get1(H.d_ndiags, st);
     dfree(ovf);
-    if (nd > cap_diags || (ovf_h & 2) || (walk_ovf & 2)) {
+    bool redo = nd > cap_diags || (ovf_h & 2) || (walk_ovf & 2);
+    if (H.coll.on()) redo = coll_or(H.coll, redo ? 1u : 0u, st) != 0;
+    if (redo) {
       if (getenv("EXS_TRACE_UNITS"))
         fprintf(stderr, "[run_batch] batch retry: %u diagnostics, capacity %u, overflow %u/%u\n", nd, cap_diags,
                 ovf_h, walk_ovf);
@@ -778,6 +789,19 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     par_for(n_files, [=] EXS_HD (i64 f) {
       if (ct[f]) emit_diag(B, mkdiag((u32)f, 1, 1, C_X9999, M_X_CONTRACT));
     }, st);
+  }
+  // a sharded walk: every rank's diagnostic records to every rank (the
+  // ordering and finish_diagnostics below drop the repeats)
+  if (H.coll.on()) {
+    const u32 nl = std::min(get1(H.d_ndiags, st), H.cap_diags + n_files);
+    std::vector<u64> sizes;
+    u64 total = 0;
+    u8* all = coll_allgatherv(H.coll, H.d_diags, sizeof(Diag) * (u64)nl, sizes, total, st);
+    const u32 nt = (u32)(total / sizeof(Diag));
+    dfree(H.d_diags);
+    H.d_diags = reinterpret_cast<Diag*>(all);
+    H.cap_diags = std::max(H.cap_diags, nt);
+    h2d(H.d_ndiags, &nt, 4, st);
   }
   // order diagnostics by (file, line, col, code string) -- one radix sort of a
   // packed key, or two stable passes when the fields exceed 64 bits
@@ -1128,7 +1152,7 @@ static void run_units(Handle& H, const char* const* texts, const uint64_t* lens,
   u64 maxb = 0;
   for (auto& b : plan) maxb = std::max(maxb, b.bytes);
 #ifndef EXS_EMU
-  if (H.pipelines >= 2 && plan.size() >= 2 && !g_profile && !H.keep_records) {
+  if (H.pipelines >= 2 && plan.size() >= 2 && !g_profile && !H.keep_records && !H.coll.on()) {
     run_units_pipelined(H, texts, lens, n_units, cfg, plan, maxb);
     return;
   }
@@ -1204,6 +1228,18 @@ static void run_units(Handle& H, const char* const* texts, const uint64_t* lens,
   acc.ms_wall = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
   H.stats = acc;
   for (int q = 0; q < 4; q++) H.t_stage[q] = t_stage[q];
+}
+
+int exs_set_collective(exs_handle x, int rank, int world, exs_allgather_fn fn, void* ctx) {
+  API_TRY
+  if (world < 1 || rank < 0 || rank >= world) throw Err("bad rank / world");
+  if (world > 1 && !fn) throw Err("a collective needs an all-gather function");
+  Handle& H = x->h;
+  H.coll.rank = rank;
+  H.coll.world = world;
+  H.coll.fn = reinterpret_cast<CollFn>(fn);
+  H.coll.ctx = ctx;
+  API_END
 }
 
 int exs_run_units(exs_handle x, const char* const* texts, const uint64_t* lens, uint64_t n_units,

@@ -1,4 +1,6 @@
-"""Multi-GPU file sharding.
+"""Multi-GPU sharding.
+
+Configs C2/C5 (many files):
 
 Units never resolve symbols across files (sema.py:152-218 works on one unit),
 so a corpus shards across ranks with no data-path collective: each rank takes
@@ -7,6 +9,12 @@ its own GPU, and the ordered per-file results are gathered to rank 0 in rank
 order -- which is path order, the order ``Diagnostic.sort_key`` imposes
 (diagnostics.py:73-74).  One process per GPU, ``torch.distributed`` for the
 plumbing (NCCL on the GPU box, gloo in the CPU tests).
+
+Config C4 (one huge unit): ``analyze_unit_sharded`` -- every rank runs the
+front end on the unit, walks its share of each level's work items, and the
+library exchanges the levels' new instances, the edge slots, launch seeds and
+diagnostics through an all-gather this module supplies
+(``torch.distributed.all_gather``; include/exspace_b200.h exs_set_collective).
 """
 from __future__ import annotations
 
@@ -132,3 +140,77 @@ def analyze_sharded(units: Sequence, rank: int, world: int, analyze_batch: Optio
         mode = u[3] if len(u) > 3 else X.Mode.CLASSIC
         out.append(X.Analysis(u[0], prof, mode, res, f))
     return out
+
+
+class _CudaBytes:
+    """A raw device pointer as a uint8 CUDA array (torch.as_tensor reads it)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False), "version": 2}
+
+
+def make_allgather(device=None, group=None):
+    """An exs_allgather_fn over torch.distributed: variable-size byte buffers,
+    padded to the largest, all-gathered, then packed in rank order.  device
+    None: the buffers are host memory (gloo; the EMU build in the CPU tests);
+    else CUDA memory on that device (NCCL)."""
+    import ctypes as C
+    import numpy as np
+    from ._native import ALLGATHER_FN
+
+    def fn(ctx, send, nbytes, recv, sizes):
+        try:
+            import torch
+            import torch.distributed as dist
+            world = dist.get_world_size(group)
+            szs = [int(sizes[r]) for r in range(world)]
+            mx = max(szs + [1])
+            if device is None:
+                t = torch.zeros(mx, dtype=torch.uint8)
+                if nbytes:
+                    t[:nbytes] = torch.from_numpy(np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send)).copy())
+                outs = [torch.empty(mx, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(outs, t, group=group)
+                if sum(szs):
+                    dst = np.ctypeslib.as_array((C.c_uint8 * sum(szs)).from_address(recv))
+                    off = 0
+                    for r in range(world):
+                        dst[off:off + szs[r]] = outs[r][:szs[r]].numpy()
+                        off += szs[r]
+            else:
+                dev = torch.device(device)
+                t = torch.zeros(mx, dtype=torch.uint8, device=dev)
+                if nbytes:
+                    t[:nbytes].copy_(torch.as_tensor(_CudaBytes(send, nbytes), device=dev))
+                outs = [torch.empty(mx, dtype=torch.uint8, device=dev) for _ in range(world)]
+                dist.all_gather(outs, t, group=group)
+                if sum(szs):
+                    dst = torch.as_tensor(_CudaBytes(recv, sum(szs)), device=dev)
+                    off = 0
+                    for r in range(world):
+                        dst[off:off + szs[r]].copy_(outs[r][:szs[r]])
+                        off += szs[r]
+                torch.cuda.synchronize(dev)
+            return 0
+        except Exception:  # the library reports a failed collective
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    return ALLGATHER_FN(fn)
+
+
+def analyze_unit_sharded(text: str, path: str, rank: int, world: int, profile=None, mode=None, cfg=None,
+                         engine=None, device=None, want_walks: bool = False):
+    """One unit analysed by `world` ranks together (the walk split across
+    them); every rank returns the same Analysis.  device: CUDA device of the
+    collective's buffers (None for host memory: gloo with the EMU build)."""
+    from . import exspace as X
+    eng = engine or X.get_engine(rank if device is None else device)
+    eng.handle.set_collective(rank, world, make_allgather(device))
+    try:
+        unit = (text, path, profile or X.CompileProfile(), mode or X.Mode.CLASSIC, cfg or X.TraitConfig())
+        return eng.run_batch([unit], want_walks=want_walks)[0]
+    finally:
+        eng.handle.set_collective(0, 1, None)
+

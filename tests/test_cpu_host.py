@@ -193,3 +193,74 @@ def test_bench_gpus_n_relaunches_one_rank_per_gpu():
     assert len(lines) == 1, out.stdout
     line = json.loads(lines[0])
     assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+SHARD_WORKER = r"""
+import os, sys, json
+sys.path.insert(0, @ROOT@); sys.path.insert(0, @TESTS@)
+import torch.distributed as dist
+from paper_2309_03912_b200 import exspace as X
+from paper_2309_03912_b200.shard import analyze_unit_sharded
+from shard_units import UNITS
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:@PORT@", rank=rank, world_size=world)
+eng = X.Engine(0, @LIB@)
+out = []
+for name, text, mode in UNITS:
+    a = analyze_unit_sharded(text, name, rank, world, mode=X.Mode(mode), engine=eng, want_walks=True)
+    out.append(ROW(a))
+if rank == 0:
+    print(json.dumps(out))
+dist.destroy_process_group()
+"""
+
+ROW_SRC = r"""
+def ROW(a):
+    rows = [[d.code, d.loc.line, d.loc.col, d.message, d.suppressed] for d in a.all_diagnostics]
+    walks = {k.value: [w.n_instances, w.n_edges, w.n_demands, sorted(w.instances),
+                       sorted([k2, v] for k2, v in w.edges.items()),
+                       sorted([k2, d, l[0], l[1]] for k2, (d, l) in w.demands.items())]
+             for k, w in a.walks.items()}
+    return [rows, walks]
+"""
+
+
+def _emu_lib():
+    lib = ROOT / "build" / "libexspace_emu.so"
+    if not lib.exists():
+        if subprocess.run(["make", "-C", str(ROOT / "tests" / "emu")], capture_output=True).returncode:
+            pytest.skip("the EMU build needs nvcc")
+    return lib
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_one_unit_walk_sharded_over_gloo_equals_one_rank(world):
+    """One unit walked by `world` ranks (exs_set_collective; shard.analyze_unit_sharded):
+    each rank walks its share of every level's work items and the ranks exchange new
+    instances, edge slots, launch seeds and diagnostics through a gloo all-gather.  The
+    kernels' logic runs as host code (the EMU build of the same sources; tests/emu), so the
+    exchange protocol is checked here on CPU: diagnostics, walk counts and walk keys equal the
+    single-rank run on deep chains (65 levels), call graphs, stressors, sema-diagnostic units."""
+    import json
+    lib = _emu_lib()
+    port = _free_port()
+    code = (ROW_SRC + SHARD_WORKER).replace("@ROOT@", repr(str(ROOT))).replace("@TESTS@", repr(str(ROOT / "tests")))
+    code = code.replace("@PORT@", str(port)).replace("@LIB@", repr(str(lib)))
+    procs = []
+    for rank in range(world):
+        env = dict(os.environ, RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+                   CUDA_VISIBLE_DEVICES="")
+        procs.append(subprocess.Popen([sys.executable, "-c", code], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=900) for p in procs]
+    assert all(p.returncode == 0 for p in procs), [o[1][-2000:] for o in outs]
+    got = json.loads(outs[0][0].strip().splitlines()[-1])
+    sys.path.insert(0, str(ROOT / "tests"))
+    from shard_units import UNITS
+    from paper_2309_03912_b200 import exspace as X
+    ns = {}
+    exec(ROW_SRC, ns)
+    eng = X.Engine(0, str(lib))
+    want = [ns["ROW"](eng.run_batch([(t, n, X.CompileProfile(), X.Mode(m), X.TraitConfig())], want_walks=True)[0])
+            for n, t, m in UNITS]
+    assert json.loads(json.dumps(want)) == got

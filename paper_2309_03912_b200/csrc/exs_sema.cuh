@@ -37,7 +37,9 @@ EXS_HD inline bool val_eq(const Val& a, const Val& b) {
 }
 
 // Struct and function records (one per declaration, view-local order)
-enum { FR_DUP = 1, FR_OWNER = 2, FR_MEMBER = 4, FR_VARDECL = 8 };
+// FR_BODY: an instance has something to walk (statements or parameters);
+// FR_MAIN: the free function main (instances read both without the node/token)
+enum { FR_DUP = 1, FR_OWNER = 2, FR_MEMBER = 4, FR_VARDECL = 8, FR_BODY = 16, FR_MAIN = 32 };
 struct FnRec {
   u32 node, view, rec, order;  // rec: containing struct record (NONE for free)
   u64 sig, name;               // signature hash (sema.py:144-149), name hash

@@ -270,6 +270,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
         r.name = nd[node].hv; r.sig = 0; r.sig_rep = f; r.ncalls = 0;
         r.nstmts = (nd[node].n & FF_BODY) ? (u32)(nd[node + 1].hv & 0xFFFFFFFFu) : 0;  // counted by the parser
         r.flags = rec == NONE ? 0 : FR_MEMBER;
+        if ((nd[node].n & FF_BODY) && (r.nstmts || nd[node].c1 != NONE)) r.flags |= FR_BODY;
         nd[node + 1].tok = f;  // FNX.tok -> decl record
         f++;
       };
@@ -309,6 +310,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       FnRec& r = fr[i];
       u32 owner_tok = NONE;
       if (r.rec != NONE && !rr[r.rec].dup) { r.flags |= FR_OWNER; owner_tok = nd[rr[r.rec].node].tok; }
+      if (tk[nd[r.node].tok].id == W_MAIN && !(r.flags & FR_OWNER)) r.flags |= FR_MAIN;
       bool p2 = (cfgs[vf[r.view]] & CFG_MODE_MASK) == MODE_P2;
       r.sig = sig_hash(nd, tk, s, sp, r.node, owner_tok, p2);
     }, st);

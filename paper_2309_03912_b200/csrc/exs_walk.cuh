@@ -202,7 +202,6 @@ EXS_HD inline IKey make_ikey(u32 sig_rep, const Val& tb, const Val& hb, const Va
 EXS_HD inline void fill_instance(Inst& I, const Tables* T, const IKey& k, u32 fi, const Val& tb, const Val& hb,
                                  u8 side, u32 orec, const Val& ot, u32 at_tok, u32 walk, u8 sp, u32 slot) {
   const FnRec& fr = T->fns[fi];
-  const Node& fnn = T->nodes[fr.node];
   I.ka = k.a; I.kb = k.b;
   I.ckey = ~0ull; I.fn = fi; I.orec = orec; I.walk = walk; I.at = at_tok;
   I.ebase = 0; I.ecnt = 0;
@@ -210,8 +209,8 @@ EXS_HD inline void fill_instance(Inst& I, const Tables* T, const IKey& k, u32 fi
   I.side = side; I.spaces = sp; I.pad = 0; I.slot = slot;
   // IF_BODY: a body to walk -- statements or parameter types to resolve (an
   // empty, parameterless body creates nothing and reports nothing)
-  I.flags = ((fnn.n & FF_BODY) && (fr.nstmts || fnn.c1 != NONE)) ? IF_BODY : 0;
-  if (T->toks[fnn.tok].id == W_MAIN && !(fr.flags & FR_OWNER)) I.flags |= IF_MAIN;
+  I.flags = (fr.flags & FR_BODY) ? IF_BODY : 0;
+  if (fr.flags & FR_MAIN) I.flags |= IF_MAIN;
 }
 // key insertion without an id (the level-0 roots allocate ids by a scan
 // afterwards instead of one shared counter): the slot, NONE if the table is full

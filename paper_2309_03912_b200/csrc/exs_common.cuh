@@ -237,6 +237,19 @@ EXS_HD inline u32 at_inc_agg(u32* p) {
   u32 o = *p; *p = o + 1; return o;
 #endif
 }
+// Warp-aggregated add: the active lanes that add to the same counter issue
+// one atomicAdd of their sum (per-walk statistics: every instance of a huge
+// unit adds to the same two counters)
+EXS_HD inline void at_add_agg(u32* p, u32 v) {
+#if EXS_DEV_PATH
+  const u32 mask = __activemask();
+  const u32 peers = __match_any_sync(mask, (unsigned long long)p);
+  const u32 sum = __reduce_add_sync(peers, v);
+  if ((threadIdx.x & 31) == (u32)(__ffs(peers) - 1) && sum) atomicAdd(p, sum);
+#else
+  *p += v;
+#endif
+}
 EXS_HD inline u32 at_min(u32* p, u32 v) {
 #if EXS_DEV_PATH
   return atomicMin(p, v);

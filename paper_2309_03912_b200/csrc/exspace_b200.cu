@@ -415,7 +415,7 @@ static void run_demands(Handle& H, bool emit_e1201) {
       walks[s] = e.walk;
       if (e.rank < best[s]) { best[s] = e.rank; besti[s] = idx[j]; }
     }
-    for (u32 s = 0; s < 2; s++) if (walks[s] != NONE) at_add(&dem[walks[s]], 1);
+    for (u32 s = 0; s < 2; s++) if (walks[s] != NONE) at_add_agg(&dem[walks[s]], 1);
     if (!emit_e1201 || sides == 3) return;
     u32 s = sides == 1 ? 0 : 1;
     const DemEnt& e = ent[besti[s]];
@@ -887,8 +887,8 @@ static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, 
     dzero(we, 4ull * (2 * F + 1), st);
     const Inst* in = H.W.inst;
     par_for(H.W.n_inst, [=] EXS_HD (i64 i) {
-      at_add(&wi[in[i].walk], 1);
-      at_add(&we[in[i].walk], in[i].ecnt);
+      at_add_agg(&wi[in[i].walk], 1);
+      at_add_agg(&we[in[i].walk], in[i].ecnt);
     }, st);
     if (F) {
       d2h(H.walk_inst.data(), wi, 8ull * F, st);

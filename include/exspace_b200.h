@@ -178,6 +178,12 @@ typedef struct {
 int exs_results_view(exs_handle h, const exs_result** recs, uint64_t* n, const char** text,
                      uint64_t* text_bytes, const uint64_t** unit_first, uint64_t* n_units);
 
+/* Keep the current results: their buffers are not reused by later runs (which
+ * fill another set) until exs_results_release(lease); the views of
+ * exs_results_view stay valid that long.  For zero-copy consumers. */
+int exs_results_lease(exs_handle h, uint64_t* lease);
+int exs_results_release(exs_handle h, uint64_t lease);
+
 /* Copy the results of the last run into caller memory (sizes from
  * exs_results_view; any pointer may be null), with several host threads. */
 int exs_results_copy(exs_handle h, exs_result* recs, char* text, uint64_t* unit_first);

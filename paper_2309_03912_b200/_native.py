@@ -61,6 +61,7 @@ EXPORTS = [
     "exs_get_walk_stats", "exs_describe", "exs_set_option", "exs_stage_times", "exs_profile_text",
     "exs_get_decls", "exs_get_structs", "exs_get_instances", "exs_get_edges", "exs_get_nodes",
     "exs_get_token_range", "exs_run_units", "exs_results_view", "exs_results_copy", "exs_set_collective",
+    "exs_results_lease", "exs_results_release",
 ]
 
 # exs_allgather_fn (include/exspace_b200.h)
@@ -169,6 +170,8 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     lib.exs_stage_times.argtypes = [vp, C.POINTER(C.c_float)]
     lib.exs_run_units.argtypes = [vp, vp, vp, C.c_uint64, vp]
     lib.exs_results_copy.argtypes = [vp, vp, vp, vp]
+    lib.exs_results_lease.argtypes = [vp, u64p]
+    lib.exs_results_release.argtypes = [vp, C.c_uint64]
     lib.exs_set_collective.argtypes = [vp, C.c_int, C.c_int, ALLGATHER_FN, vp]
     lib.exs_results_view.argtypes = [vp, C.POINTER(C.c_void_p), u64p, C.POINTER(C.c_void_p), u64p,
                                      C.POINTER(C.c_void_p), u64p]
@@ -181,6 +184,22 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
 
 def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
+
+
+class ResultsLease:
+    """Keeps a run's result buffers (and their handle) alive; released when
+    the last view of them is garbage-collected."""
+
+    def __init__(self, handle: "Handle", lease: int):
+        self.handle = handle
+        self.lease = lease
+
+    def __del__(self):
+        try:
+            if self.handle.h:
+                self.handle.lib.exs_results_release(self.handle.h, self.lease)
+        except Exception:
+            pass
 
 
 class Handle:
@@ -229,6 +248,16 @@ class Handle:
         cfg = np.ascontiguousarray(cfg, dtype=np.uint8)
         self._check(self.lib.exs_run_units(self.h, _ptr(ptrs), _ptr(lens), len(ptrs), _ptr(cfg)))
         del keep
+
+    def lease_results(self):
+        """Zero-copy results of the last run: (records, message bytes,
+        unit_first, lease).  The views stay valid while `lease` lives (the
+        handle's later runs fill other buffers)."""
+        n = C.c_uint64()
+        self._check(self.lib.exs_results_lease(self.h, C.byref(n)))
+        lease = ResultsLease(self, n.value)
+        recs, text, first = self.results(copy=False)
+        return recs, text, first, lease
 
     def results(self, copy: bool = True):
         """(records, message bytes, unit_first) of the last run.  copy=False

@@ -238,10 +238,19 @@ struct Handle {
   bool diag_sort_two_pass = false;  // force the two-key diagnostic sort (parity tests)
   bool keep_records = false;        // also keep the raw records (exs_get_diags / exs_diags_view)
   Coll coll;                        // one batch walked across ranks (exs_set_collective)
-  // rendered results of the last run (all its batches), in unit order
-  PinnedBuf res, text;
-  u64 n_res = 0, text_bytes = 0, static_bytes = 0;
-  std::vector<u64> unit_first;      // n_units + 1
+  // rendered results of a run (all its batches), in unit order.  A run fills
+  // a free set; a caller may lease the current one (zero-copy views that stay
+  // valid until it releases them) and later runs then use another
+  struct ResultSet {
+    PinnedBuf res, text;
+    u64 n_res = 0, text_bytes = 0;
+    std::vector<u64> unit_first;    // n_units + 1
+    bool leased = false;
+  };
+  std::vector<std::unique_ptr<ResultSet>> sets;
+  ResultSet* cur = nullptr;
+  std::string static_txt;           // the static message section (start of every text arena)
+  u64 static_bytes = 0;
   u32* d_static = nullptr;          // per static message key: (offset, length)
   // results sink: the handle whose result buffers render_results appends to
   // (this one, or the owner of a pipeline), batch by batch in batch order
@@ -457,8 +466,7 @@ static void static_init(Handle& H) {
       txt += m;
     }
     H.static_bytes = txt.size();
-    H.text.ensure(H.static_bytes, 0);
-    memcpy(H.text.p, txt.data(), txt.size());
+    H.static_txt = txt;
     H.d_static = dalloc<u32>(2 * EXS_STATIC_KEYS);
     h2d(H.d_static, tab.data(), 8ull * EXS_STATIC_KEYS, H.st);
     sync(H.st);
@@ -466,9 +474,19 @@ static void static_init(Handle& H) {
 }
 static void results_reset(Handle& H, u64 n_units) {
   static_init(H);
-  H.n_res = 0;
-  H.text_bytes = H.static_bytes;
-  H.unit_first.assign(n_units + 1, 0);
+  Handle::ResultSet* rs = nullptr;
+  for (auto& x : H.sets)
+    if (!x->leased) { rs = x.get(); break; }
+  if (!rs) {
+    H.sets.emplace_back(new Handle::ResultSet());
+    rs = H.sets.back().get();
+  }
+  H.cur = rs;
+  rs->n_res = 0;
+  rs->text.ensure(H.static_bytes, 0);
+  memcpy(rs->text.p, H.static_txt.data(), H.static_bytes);
+  rs->text_bytes = H.static_bytes;
+  rs->unit_first.assign(n_units + 1, 0);
 }
 
 // Render the ordered records dd[0, nd) of one batch (units unit_base ..),
@@ -520,7 +538,8 @@ static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u
     if (R.turn.abort) throw Err("another pipeline failed");
   }
   // message bytes of record i, wherever they live
-  const u64 tbase = R.text_bytes;
+  Handle::ResultSet& RS = *R.cur;
+  const u64 tbase = RS.text_bytes;
   auto msg_of = [=] EXS_HD (u32 i, const char*& p, u32& n, u64& glob) {
     const int k = static_key(dd[i]);
     if (k >= 0) { glob = stab[2 * k]; n = stab[2 * k + 1]; p = nullptr; }
@@ -532,7 +551,7 @@ static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u
   u8* keep = dalloc<u8>((u64)nd + 1);
   char* stxt = nullptr;  // the static section on the device (for comparisons)
   stxt = dalloc<char>(H.static_bytes + 1);
-  h2d(stxt, H.text.p, H.static_bytes, st);
+  h2d(stxt, H.static_txt.data(), H.static_bytes, st);
   const char* sx = stxt;
   EXS_TAG("finish_runs");
   par_for(nd, [=] EXS_HD (i64 i) {
@@ -602,16 +621,16 @@ static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u
       if (j + 1 == (i64)nk || rc[j + 1].unit != rc[j].unit) fcnt[2 * f + 1] = (u32)j + 1;
     }, st);
   }
-  R.res.ensure((R.n_res + nk) * sizeof(ResRec), R.n_res * sizeof(ResRec));
-  R.text.ensure(R.text_bytes + total, R.text_bytes);
+  RS.res.ensure((RS.n_res + nk) * sizeof(ResRec), RS.n_res * sizeof(ResRec));
+  RS.text.ensure(RS.text_bytes + total, RS.text_bytes);
   std::vector<u32> fc(2ull * n_files);
-  d2h(R.res.p + R.n_res * sizeof(ResRec), rr, (u64)nk * sizeof(ResRec), st);
-  if (total) d2h(R.text.p + R.text_bytes, txt, total, st);
+  d2h(RS.res.p + RS.n_res * sizeof(ResRec), rr, (u64)nk * sizeof(ResRec), st);
+  if (total) d2h(RS.text.p + RS.text_bytes, txt, total, st);
   d2h(fc.data(), fcnt, 8ull * n_files, st);
   sync(st);
-  for (u32 f = 0; f < n_files; f++) R.unit_first[unit_base + f + 1] = fc[2 * f + 1] - fc[2 * f];
-  R.n_res += nk;
-  R.text_bytes += total;
+  for (u32 f = 0; f < n_files; f++) RS.unit_first[unit_base + f + 1] = fc[2 * f + 1] - fc[2 * f];
+  RS.n_res += nk;
+  RS.text_bytes += total;
   if (R.turn.on) {
     R.turn.next++;
     turn_lock.unlock();
@@ -622,7 +641,8 @@ static void render_results(Handle& H, const Diag* dd, u32 nd, const u8* d_src, u
 
 // unit_first: per-unit counts -> first result index per unit
 static void results_close(Handle& H) {
-  for (u64 u = 0; u + 1 < H.unit_first.size(); u++) H.unit_first[u + 1] += H.unit_first[u];
+  std::vector<u64>& uf = H.cur->unit_first;
+  for (u64 u = 0; u + 1 < uf.size(); u++) uf[u + 1] += uf[u];
 }
 
 static void run_batch(Handle& H, const u8* d_src, u64 n_bytes, const u64* foff, u32 n_files,
@@ -1289,9 +1309,11 @@ int exs_results_copy(exs_handle x, exs_result* recs, char* text, uint64_t* unit_
   const Handle& H = x->h;
   const int nt = H.pack_threads > 0 ? H.pack_threads
                                     : (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
-  if (recs) copy_threads(recs, H.res.p, H.n_res * sizeof(ResRec), nt);
-  if (text) copy_threads(text, H.text.p, H.text_bytes, nt);
-  if (unit_first && !H.unit_first.empty()) memcpy(unit_first, H.unit_first.data(), 8 * H.unit_first.size());
+  if (!H.cur) throw Err("no results: nothing was run");
+  const Handle::ResultSet& RS = *H.cur;
+  if (recs) copy_threads(recs, RS.res.p, RS.n_res * sizeof(ResRec), nt);
+  if (text) copy_threads(text, RS.text.p, RS.text_bytes, nt);
+  if (unit_first && !RS.unit_first.empty()) memcpy(unit_first, RS.unit_first.data(), 8 * RS.unit_first.size());
   API_END
 }
 
@@ -1299,12 +1321,33 @@ int exs_results_view(exs_handle x, const exs_result** recs, uint64_t* n, const c
                      uint64_t* text_bytes, const uint64_t** unit_first, uint64_t* n_units) {
   API_TRY
   const Handle& H = x->h;
-  *recs = reinterpret_cast<const exs_result*>(H.res.p);
-  *n = H.n_res;
-  *text = reinterpret_cast<const char*>(H.text.p);
-  *text_bytes = H.text_bytes;
-  *unit_first = H.unit_first.data();
-  *n_units = H.unit_first.empty() ? 0 : H.unit_first.size() - 1;
+  if (!H.cur) throw Err("no results: nothing was run");
+  const Handle::ResultSet& RS = *H.cur;
+  *recs = reinterpret_cast<const exs_result*>(RS.res.p);
+  *n = RS.n_res;
+  *text = reinterpret_cast<const char*>(RS.text.p);
+  *text_bytes = RS.text_bytes;
+  *unit_first = RS.unit_first.data();
+  *n_units = RS.unit_first.empty() ? 0 : RS.unit_first.size() - 1;
+  API_END
+}
+
+int exs_results_lease(exs_handle x, uint64_t* lease) {
+  API_TRY
+  Handle& H = x->h;
+  if (!H.cur) throw Err("no results: nothing was run");
+  H.cur->leased = true;
+  u64 k = 0;
+  while (H.sets[k].get() != H.cur) k++;
+  *lease = k + 1;
+  API_END
+}
+
+int exs_results_release(exs_handle x, uint64_t lease) {
+  API_TRY
+  Handle& H = x->h;
+  if (lease == 0 || lease > H.sets.size()) throw Err("unknown results lease");
+  H.sets[lease - 1]->leased = false;
   API_END
 }
 

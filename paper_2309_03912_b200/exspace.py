@@ -280,11 +280,12 @@ class CorpusResults:
     and their message bytes.  Diagnostic objects are built per unit on first
     access (a corpus of 1 GB has ~4M diagnostics)."""
 
-    def __init__(self, recs: np.ndarray, text: np.ndarray, unit_first: np.ndarray, paths: list):
+    def __init__(self, recs: np.ndarray, text: np.ndarray, unit_first: np.ndarray, paths: list, lease=None):
         self.recs = recs
         self.text = text
         self.unit_first = unit_first
         self.paths = paths
+        self._lease = lease  # zero-copy views of the library's buffers stay valid while this lives
 
     def n_diagnostics(self, unit: int) -> int:
         return int(self.unit_first[unit + 1] - self.unit_first[unit])
@@ -432,10 +433,10 @@ class Engine:
                 self.handle.set_option(7, 2047)
             self.handle.set_option(1, 1 if want_walks else 0)
             self.handle.run_units(texts, cfg)
-            recs, text, first = self.handle.results(copy=True)
+            recs, text, first, lease = self.handle.lease_results()
             self.last_stats = self.handle.stats()
             self.last_result_bytes = recs.nbytes + text.nbytes + first.nbytes
-            results = CorpusResults(recs, text, first, paths)
+            results = CorpusResults(recs, text, first, paths, lease)
             walks = status = batch = None
             if want_walks:
                 if self.last_stats["batches"] != 1:

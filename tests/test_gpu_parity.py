@@ -368,3 +368,20 @@ def test_logical_shards_merge_to_the_one_shard_run(X, n_shards):
         rows = lambda r: [(d.code, d.loc.line, d.loc.col, d.message, d.suppressed) for d in r.diagnostics(u)]  # noqa
         assert rows(res_m) == rows(res_w)
 
+
+
+def test_leased_results_survive_later_runs(X):
+    """analyze_corpus hands out zero-copy views of the library's result buffers
+    (exs_results_lease): a run's diagnostics read after two later runs on the
+    same engine equal a fresh run's."""
+    from paper_2309_03912_b200 import synth
+    eng = X.Engine(0)
+    t1 = [synth.gen_c2_file(s, 5000) for s in range(6)]
+    t2 = [synth.gen_c5_file(s, 5000, 0.5) for s in range(6)]
+    mk = lambda ts, m: [(t, "a.cu", X.CompileProfile(), m, X.TraitConfig()) for t in ts]  # noqa: E731
+    first = eng.run_batch(mk(t1, X.Mode.SOUND))
+    eng.run_batch(mk(t2, X.Mode.SOUND))
+    eng.run_batch(mk(t2, X.Mode.CLASSIC))
+    again = eng.run_batch(mk(t1, X.Mode.SOUND))
+    assert [as_rows(a) for a in first] == [as_rows(a) for a in again]
+    assert sum(len(a.all_diagnostics) for a in first) > 0

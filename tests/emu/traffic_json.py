@@ -20,6 +20,7 @@ ROOT = Path(__file__).resolve().parents[2]
 def main():
     src, dst = Path(sys.argv[1]), Path(sys.argv[2])
     config = sys.argv[3] if len(sys.argv) > 3 else "c2"
+    command = sys.argv[4] if len(sys.argv) > 4 else f"bench.py --config {config} --steps 1 --warmup 1 --no-cpu-baseline"
     rows = [r for r in csv.reader(open(src)) if r]
     hdr = next(r for r in rows if r[0] == "ID")
     ti = next(i for i, h in enumerate(hdr) if "Push/Pop_Range" in h)
@@ -44,7 +45,7 @@ def main():
     shutil.copy(src, dst)
     rel = dst.relative_to(ROOT) if dst.is_absolute() else dst
     source = ("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-              f"--clock-control none on `bench.py --config {config} --steps 1 --warmup 1 --no-cpu-baseline`; "
+              f"--clock-control none on `{command}`; "
               f"mean over the launches of the run (warm-up, step and e2e runs); {rel}")
     out = {}
     for tag, a in sorted(agg.items()):

@@ -331,16 +331,16 @@ struct Walker {
   u32 ebase, ecnt;           // edge slots of this instance, legal edges written
   u32 stmt_cs_base, cs_ord;  // edge slot of the current statement, edges in it so far
   bool silent;               // replaying declarations of earlier chunks: no side effects
-  Env env;                   // owner bindings + bindings
-  // locals (scoped dict)
-  u32 nloc;
-  u64 lname[MAX_LOCALS];
-  Val lval[MAX_LOCALS];
-  int wdepth;
   bool contract;
-  // argument types of the calls being walked (a stack shared by all frames)
-  u32 asp;
-  Val astk[MAX_ARGS];
+  int wdepth;
+  u32 nloc;                  // locals in scope
+  u32 asp;                   // argument-stack depth
+  Env env;                   // owner bindings + bindings
+  // the arrays last: a statement without locals or arguments (most of them)
+  // touches only the lines above (the walker lives in local memory)
+  u64 lname[MAX_LOCALS];     // locals (scoped dict)
+  Val lval[MAX_LOCALS];
+  Val astk[MAX_ARGS];        // argument types of the calls being walked (shared by all frames)
 
   EXS_HD const Node& N(u32 id) const { return T->nodes[id]; }
   EXS_HD const Tok& K(u32 t) const { return T->toks[t]; }

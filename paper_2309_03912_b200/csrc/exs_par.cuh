@@ -157,6 +157,15 @@ extern thread_local i64 g_select_flagged_min;
 #define EXS_TAG(name) (::exs::g_tag = (name))
 #endif
 
+// threads of one full par_for grid (one index per thread): kernels whose work
+// count is on the device loop over it in strides of this, 256-lane groups
+// (t >> 8) taking the heavy items
+#ifndef EXS_EMU
+inline i64 grid_threads() { return (i64)g_sm_count * 16 * 256; }
+#else
+inline i64 grid_threads() { return 256; }
+#endif
+
 template <class F>
 void par_for(i64 n, F f, cudaStream_t s, int block = 256, const char* fn = __builtin_FUNCTION(),
              int line = __builtin_LINE()) {

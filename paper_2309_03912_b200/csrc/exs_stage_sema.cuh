@@ -426,6 +426,12 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
     u32* cpre = dalloc<u32>(NSt + 1);
     u32* sn = S.stmt_node; u32* scs = S.stmt_cs;
     const u32* sroot = P.seg_root;
+    // split bodies of many statements are tabulated by a 256-lane group each
+    // (a main of 5,150 statements, C3), the rest by one thread per body
+    constexpr u32 HEAVY = 64;
+    u32* hn = dalloc<u32>(1);
+    u32* hl = dalloc<u32>((u64)NSt / HEAVY + 2);
+    dzero(hn, 4, st);
     EXS_TAG("sema_body_table");
     par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
@@ -435,6 +441,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       bool var = false;
       const u64 x = nd[r.node + 1].hv;
       if (x >> 32) {
+        if (r.nstmts > HEAVY) { hl[at_inc_agg(hn)] = (u32)i; return; }
         // a split body: its statements are listed by segment (no list walk)
         const u32* sg = sroot + ((x >> 32) - 1);
         for (u32 t = 0; t < r.nstmts; t++) {
@@ -452,6 +459,35 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       }
       if (var) r.flags |= FR_VARDECL;
     }, st);
+    {
+      const i64 G = grid_threads();
+      u32* hv = dalloc<u32>((u64)NSt / HEAVY + 2);
+      dzero(hv, 4ull * (NSt / HEAVY + 2), st);
+      EXS_TAG("sema_body_table_heavy");
+      par_for(G, [=] EXS_HD (i64 t) {
+        const i64 nh = *hn;
+        for (i64 h = t >> 8; h < nh; h += G >> 8) {
+          const u32 i = hl[h];
+          const FnRec& r = fr[i];
+          const u32* sg = sroot + ((nd[r.node + 1].hv >> 32) - 1);
+          const u32 k = r.stmt_base;
+          for (u32 q = (u32)(t & 255); q < r.nstmts; q += 256) {
+            const u32 s = sg[q];
+            sn[k + q] = s;
+            sfn[k + q] = i;
+            if (nd[s].kind == N_SVAR) hv[h] = 1;  // same value from every writer
+          }
+        }
+      }, st);
+      par_for(G, [=] EXS_HD (i64 t) {
+        const i64 nh = *hn;
+        for (i64 h = t; h < nh; h += G)
+          if (hv[h]) fr[hl[h]].flags |= FR_VARDECL;
+      }, st);
+      dfree(hv);
+    }
+    dfree(hn);
+    dfree(hl);
     EXS_TAG("sema_bodyscan");
     par_for_walk(NSt + 1, [=] EXS_HD (i64 k) {
       if (k == NSt) { scnt[k] = 0; return; }

@@ -10,6 +10,9 @@ namespace exs {
 #ifndef EXS_WALK_SORT
 #define EXS_WALK_SORT 1  // order walk work items by statement shape (C2 1 GB: walk 137 -> 76 us/MB)
 #endif
+#ifndef EXS_WALK_SORT_MIN
+#define EXS_WALK_SORT_MIN (1u << 16)  // levels with fewer work items walk unsorted
+#endif
 #ifndef EXS_KCH
 #define EXS_KCH 1  // top-level statements per walk_chunks thread (measured: 1 beats 2 and 4 at 1 GB)
 #endif
@@ -551,6 +554,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   // ---- levels
   u32 prev_n = 0;
   u32 level = 0;
+  u64 rank_lim = (u64)CK_FIELD_MAX + 1;  // bound on the parent ranks of the next frontier's keys
   u32* front = nullptr;
   u64 front_cap = 0;
   u64 edges_used = 0;
@@ -600,25 +604,49 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
                       fr_tmp, L.cnt, sc, st);
       u64* keys = dalloc<u64>(nf + 1);
       par_for(nf, [=] EXS_HD (i64 j) { fr_tmp[j] += base; keys[j] = in[fr_tmp[j]].ckey; }, st);
-      sort_pairs(keys, fr_tmp, nf, sc, st, CK_LEVEL_SHIFT);  // the level bits are equal in a frontier
+      // the level bits are equal in a frontier, and parent ranks are below the
+      // previous frontier's size
+      int end_bit = CK_RANK_SHIFT;
+      while (end_bit < CK_LEVEL_SHIFT && (rank_lim >> (end_bit - CK_RANK_SHIFT))) end_bit++;
+      sort_pairs(keys, fr_tmp, nf, sc, st, end_bit);
       d2d(front, fr_tmp, 4ull * nf, st);
-      sync(st);
-      dfree(keys);
+      dfree(keys);  // blocks are reused in stream order (cache_alloc): no wait
       dfree(fr_tmp);
     }
     prev_n = n_now;
     const u32 nnew_prev = nnew;  // new instances per level track the next level's
     if (!nf) break;
     prof_mark(st);
-    // edge bases: scan of call-site counts
+    // edge bases (scan of call-site counts) and work items (scan of statement
+    // chunks), both totals read back in one round trip
+    const u32 KCH = EXS_KCH;
     u32* ec = dalloc<u32>(nf + 1);
     u32* eb = dalloc<u32>(nf + 1);
+    u32* wc = dalloc<u32>(nf + 1);
+    u32* wb = dalloc<u32>(nf + 1);
+    u32* tot = dalloc<u32>(2);
     {
       const Inst* in = W.inst; const FnRec* fr = S.fns; const u32* fl = front;
-      par_for(nf + 1, [=] EXS_HD (i64 j) { ec[j] = j < nf ? fr[in[fl[j]].fn].ncalls : 0; }, st);
+      par_for(nf + 1, [=] EXS_HD (i64 j) {
+        if (j < nf) {
+          const FnRec& r = fr[in[fl[j]].fn];
+          ec[j] = r.ncalls;
+          wc[j] = r.nstmts ? (r.nstmts + KCH - 1) / KCH : 1;
+        } else {
+          ec[j] = 0;
+          wc[j] = 0;
+        }
+      }, st);
     }
     excl_scan_u32(ec, eb, nf + 1, sc, st);
-    u64 S_level = get1(eb + nf, st);
+    excl_scan_u32(wc, wb, nf + 1, sc, st);
+    par_for(1, [=] EXS_HD (i64) { tot[0] = eb[nf]; tot[1] = wb[nf]; }, st);
+    u32 tot_h[2];
+    d2h(tot_h, tot, sizeof tot_h, st);
+    sync(st);
+    dfree(tot);
+    u64 S_level = tot_h[0];
+    const u32 nwi = tot_h[1];
     W.callsites += S_level;
     grow(W.edges, edge_cap, edges_used + S_level + 1, edges_used, st);
     // the creation log holds the creators that did not insert (several creators
@@ -643,16 +671,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     prof_mark(st);
     // walk the frontier: one thread per (instance, chunk of top-level statements)
     {
-      const u32 KCH = EXS_KCH;
-      u32* wc = dalloc<u32>(nf + 1);
-      u32* wb = dalloc<u32>(nf + 1);
       const Inst* in = W.inst; const FnRec* fr = S.fns; const u32* fl = front;
-      par_for(nf + 1, [=] EXS_HD (i64 j) {
-        u32 n = j < nf ? fr[in[fl[j]].fn].nstmts : 0;
-        wc[j] = j < nf ? (n ? (n + KCH - 1) / KCH : 1) : 0;
-      }, st);
-      excl_scan_u32(wc, wb, nf + 1, sc, st);
-      u32 nwi = get1(wb + nf, st);
       WalkCfg Cc = C;
       u32* ct = B.contract;
       const u32* sn = S.stmt_node; const u32* scs = S.stmt_cs;
@@ -669,7 +688,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       // (creation keys and edge slots are order-free).
       u32* perm = nullptr;
 #if EXS_WALK_SORT
-      {
+      if (nwi >= EXS_WALK_SORT_MIN) {  // a small level: the sort costs more than it saves
         perm = dalloc<u32>(nwi + 1);
         u64* key = dalloc<u64>(nwi + 1);
         const Node* nd = P.nodes;
@@ -686,7 +705,6 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
           perm[i] = (u32)i;
         }, st);
         sort_pairs(key, perm, nwi, sc, st, 16);
-        sync(st);
         dfree(key);
       }
 #endif
@@ -734,9 +752,6 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         if (w.ecnt) at_add(&B.inst[fl[j]].ecnt, w.ecnt);
         if (w.contract) at_or(&ct[w.file], 1);
       }, st);
-      sync(st);
-      dfree(wc);
-      dfree(wb);
       dfree(perm);
       dfree(frank);
       dfree(itj);
@@ -744,6 +759,9 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     }
     dfree(ec);
     dfree(eb);
+    dfree(wc);
+    dfree(wb);
+    rank_lim = std::min<u64>(nf, (u64)CK_FIELD_MAX + 1);
     prof_mark(st);
     level++;
   }
@@ -906,36 +924,65 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       u32 j = at_add(&qn[0], 1);
       q0[j] = t;
     }, st);
-    u32 nq = get1(qn, st);
+    // BFS steps in rounds of RS launches with the queue lengths on the device:
+    // one host round trip per round, not per step (C3: 66 steps); a step past
+    // the end reads a zero length and returns
     const u32* ed = W.edges;
     const FnRec* fr_ = S.fns;
-    while (nq) {
-      dzero(qn + 1, 4, st);
-      const u32* qa = q0; u32* qb = q1;
-      EXS_TAG("walk_reach");
-      par_for(nq, [=] EXS_D (i64 j) {
-        const Inst& I = in[qa[j]];
-        u8 native = (u8)(I.walk & 1);
-        u32 ns = fr_[I.fn].ncalls;
-        for (u32 e = 0; e < ns; e++) {
-          u32 c = ed[I.ebase + e];
-          if (c == NONE || in[c].side != native) continue;
+    // instances with many call sites (a main calling every chain head, C3) are
+    // expanded by a 256-lane group each, not by one thread
+    constexpr int RS = 8;
+    constexpr u32 HEAVY = 64;
+    const i64 G = grid_threads();
+    u32* qc = dalloc<u32>(2 * RS + 1);  // queue lengths per step, then heavy-list lengths
+    u32* hq = dalloc<u32>((u64)n + 1);
+    d2d(qc, qn, 4, st);  // the seeds' queue length
+    for (;;) {
+      dzero(qc + 1, 4 * 2 * RS, st);
+      for (int r = 0; r < RS; r++) {
+        const u32* qa = q0; u32* qb = q1;
+        const u32* cin = qc + r; u32* cout = qc + r + 1; u32* hn = qc + RS + 1 + r;
+        // the newly reached callees of one instance, from edge slot e0 in steps of de
+        auto expand = [=] EXS_D (const Inst& I, u32 e0, u32 de) {
+          const u8 native = (u8)(I.walk & 1);
+          const u32 ns = fr_[I.fn].ncalls;
+          for (u32 e = e0; e < ns; e += de) {
+            u32 c = ed[I.ebase + e];
+            if (c == NONE || in[c].side != native) continue;
 #ifndef EXS_EMU
-          u32* wp = (u32*)(vis + (c & ~3u));
-          u32 sh = (c & 3u) * 8;
-          u32 old = atomicOr(wp, 1u << sh);
-          if ((old >> sh) & 0xFF) continue;
+            u32* wp = (u32*)(vis + (c & ~3u));
+            u32 sh = (c & 3u) * 8;
+            u32 old = atomicOr(wp, 1u << sh);
+            if ((old >> sh) & 0xFF) continue;
 #else
-          if (vis[c]) continue;
-          vis[c] = 1;
+            if (vis[c]) continue;
+            vis[c] = 1;
 #endif
-          u32 k = at_inc_agg(&qn[1]);  // warp-aggregated: one atomic per warp
-          qb[k] = c;
-        }
-      }, st);
-      nq = get1(qn + 1, st);
-      std::swap(q0, q1);
+            u32 k = at_inc_agg(cout);  // warp-aggregated: one atomic per warp
+            qb[k] = c;
+          }
+        };
+        EXS_TAG("walk_reach");
+        par_for(G, [=] EXS_D (i64 t) {
+          const i64 nq = *cin;
+          for (i64 j = t; j < nq; j += G) {
+            const Inst& I = in[qa[j]];
+            if (fr_[I.fn].ncalls > HEAVY) { hq[at_inc_agg(hn)] = qa[j]; continue; }
+            expand(I, 0, 1);
+          }
+        }, st);
+        EXS_TAG("walk_reach_heavy");
+        par_for(G, [=] EXS_D (i64 t) {
+          const i64 nh = *hn;
+          for (i64 h = t >> 8; h < nh; h += G >> 8) expand(in[hq[h]], (u32)(t & 255), 256);
+        }, st);
+        std::swap(q0, q1);
+      }
+      if (!get1(qc + RS, st)) break;
+      d2d(qc, qc + RS, 4, st);
     }
+    dfree(qc);
+    dfree(hq);
     sync(st);
     dfree(q0); dfree(q1); dfree(qn);
   }

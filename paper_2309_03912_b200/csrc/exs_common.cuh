@@ -250,6 +250,16 @@ EXS_HD inline void at_add_agg(u32* p, u32 v) {
   *p += v;
 #endif
 }
+// Warp-aggregated max into one counter (all active lanes name the same p)
+EXS_HD inline void at_max_agg(u32* p, u32 v) {
+#if EXS_DEV_PATH
+  const u32 mask = __activemask();
+  const u32 m = __reduce_max_sync(mask, v);
+  if ((threadIdx.x & 31) == (u32)(__ffs(mask) - 1) && m) atomicMax(p, m);
+#else
+  if (v > *p) *p = v;
+#endif
+}
 EXS_HD inline u32 at_min(u32* p, u32 v) {
 #if EXS_DEV_PATH
   return atomicMin(p, v);

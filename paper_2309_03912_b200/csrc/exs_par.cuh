@@ -361,23 +361,23 @@ u32 select_idx(i64 n, P pred, u32* out, u32* d_count, Scratch& sc, cudaStream_t 
 #endif
 }
 
-// stable sort of (u64 key, u32 value) pairs; results written back in place
-inline void sort_pairs(u64* keys, u32* vals, i64 n, Scratch& sc, cudaStream_t s, int end_bit = 64) {
+// stable sort of (u64 or u32 key, u32 value) pairs; results written back in place
+template <class K>
+void sort_pairs(K* keys, u32* vals, i64 n, Scratch& sc, cudaStream_t s, int end_bit = 8 * sizeof(K)) {
   if (n <= 1) return;
 #ifndef EXS_EMU
-  u64* k2 = dalloc<u64>(n);
+  K* k2 = dalloc<K>(n);
   u32* v2 = dalloc<u32>(n);
   // double-buffered: the passes ping-pong between the two buffers and the
   // result is copied back only when it ends in the scratch pair
-  cub::DoubleBuffer<u64> dk(keys, k2);
+  cub::DoubleBuffer<K> dk(keys, k2);
   cub::DoubleBuffer<u32> dv(vals, v2);
   size_t tb = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)n, 0, end_bit, s));
   CK(cub::DeviceRadixSort::SortPairs(sc.get(tb), tb, dk, dv, (int)n, 0, end_bit, s));
-  if (dk.Current() != keys) CK(cudaMemcpyAsync(keys, dk.Current(), n * 8, cudaMemcpyDeviceToDevice, s));
+  if (dk.Current() != keys) CK(cudaMemcpyAsync(keys, dk.Current(), n * sizeof(K), cudaMemcpyDeviceToDevice, s));
   if (dv.Current() != vals) CK(cudaMemcpyAsync(vals, dv.Current(), n * 4, cudaMemcpyDeviceToDevice, s));
-  sync(s);
-  dfree(k2);
+  dfree(k2);  // reused in stream order (cache_alloc)
   dfree(v2);
   g_launches += 2;
 #else
@@ -386,9 +386,10 @@ inline void sort_pairs(u64* keys, u32* vals, i64 n, Scratch& sc, cudaStream_t s,
   // sorts by its truncated value here too, so the emulation catches it
   const u64 m = end_bit >= 64 ? ~0ull : ((1ull << end_bit) - 1);
   std::vector<std::pair<u64, u32>> v(n);
+  static_assert(sizeof(K) <= 8, "key type");
   for (i64 i = 0; i < n; i++) v[i] = {keys[i], vals[i]};
   std::stable_sort(v.begin(), v.end(), [m](auto& a, auto& b) { return (a.first & m) < (b.first & m); });
-  for (i64 i = 0; i < n; i++) { keys[i] = v[i].first; vals[i] = v[i].second; }
+  for (i64 i = 0; i < n; i++) { keys[i] = (K)v[i].first; vals[i] = v[i].second; }
 #endif
 }
 

@@ -138,7 +138,6 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
       if (h) at_add(nh, h);
     }, st);
     incl_scan(rec, S.wsc, W, WScanOp(), sc, st);
-    sync(st);
     dfree(rec);
   }
   X.wsc = S.wsc;
@@ -219,13 +218,12 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
   const u32 D = S.D;
   S.dirs = dalloc<DirRec>(D + 1);
   if (D) {
-    u64* dk = dalloc<u64>(D);
+    u32* dk = dalloc<u32>(D);
     u32* dv = dalloc<u32>(D);
     par_for(D, [=] EXS_HD (i64 i) { dk[i] = drec[i].pos; dv[i] = (u32)i; }, st);
     sort_pairs(dk, dv, D, sc, st, 32);
     DirRec* ds = S.dirs;
     par_for(D, [=] EXS_HD (i64 i) { ds[i] = drec[dv[i]]; }, st);
-    sync(st);
     dfree(dk); dfree(dv);
   }
   dfree(drec);
@@ -314,7 +312,6 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
     EXS_TAG("lex_emit");
     par_for(W, [=] EXS_HD (i64 w) { lex_word<true>(Xc, (u32)w, tk + wt[w], wt[w]); }, st);
   }
-  sync(st);
   dfree(wmask);
   X.wm = nullptr;
   if (S.NS) {

@@ -117,7 +117,6 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       u32* vt = P.vtok;
       par_for(T, [=] EXS_HD (i64 t) { vt[t] = (u32)t; }, st);
     }
-    sync(st);
     dfree(fvc); dfree(fvb); dfree(split);
   } else {
     dfree(tview);
@@ -209,7 +208,6 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
         }
       }, st);
     }
-    sync(st);
     dfree(s0); dfree(s1); dfree(vcnt); dfree(fvc); dfree(fvb); dfree(split);
   }
   // 3. segmentation: depth scan and item starts (depth over ( ) { })
@@ -345,7 +343,6 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     prof_mark(st);
     NSS = select_idx(VT, pred, ss, L.cnt, sc, st);
     prof_mark(st);
-    sync(st);
     dfree(tit0);
   }
   dfree(depth_after);
@@ -361,7 +358,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     // items in (header length bucket, first token) order: similar items per warp
     u32* iperm = dalloc<u32>(I + 1);
     {
-      u64* key = dalloc<u64>(I + 1);
+      u32* key = dalloc<u32>(I + 1);
       const u32* ib = ibody;
       par_for(I, [=] EXS_HD (i64 j) {
         u32 v = iv[j];
@@ -369,13 +366,12 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
         u32 len = (ib[j] != NONE ? ib[j] + 1 : next) - is[j];  // tokens this thread parses
         u32 lb = 0;
         while ((1u << lb) < len && lb < 31) lb++;
-        key[j] = ((u64)lb << 16) | vk[is[j]];
+        key[j] = (lb << 16) | vk[is[j]];
         iperm[j] = (u32)j;
       }, st);
       prof_mark(st);
       sort_pairs(key, iperm, I, sc, st, 24);
       prof_mark(st);
-      sync(st);
       dfree(key);
     }
     const u32* ipm = iperm;
@@ -406,7 +402,6 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       ier[j] = p.e;
       if (stt || vb[v] + p.pos != next) at_min(&vbad[v], (u32)j);
     }, st);
-    sync(st);
     dfree(iperm);
   }
   // 4b. statements of the split bodies, in parallel; merged into item status
@@ -427,7 +422,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     // segments in first-token order: warps parse statements of the same shape
     u32* sperm = dalloc<u32>(NSS + 1);
     {
-      u64* key = dalloc<u64>(NSS + 1);
+      u32* key = dalloc<u32>(NSS + 1);
       par_for(NSS, [=] EXS_HD (i64 k) {
         key[k] = vk[ssc[k]];
         sperm[k] = (u32)k;
@@ -576,7 +571,6 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       fcnt[v] = n;
       vs[v] = 2;
     }, st);
-    sync(st);
     dfree(fbl);
   }
   // 6. final ordered item lists
@@ -602,7 +596,6 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       fit[i] = vs[v] == 0 ? ir[vfst[v] + k] : fbi[fbase[v] + k];
       fiv[i] = v;
     }, st);
-    sync(st);
     dfree(cnt);
   }
 }

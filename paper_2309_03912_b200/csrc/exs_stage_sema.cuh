@@ -249,7 +249,6 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
   excl_scan_u32(cr, S.item_rec, FI + 1, sc, st);
   S.NF = get1(S.item_fn + FI, st);
   S.NR = get1(S.item_rec + FI, st);
-  sync(st);
   dfree(cf);
   dfree(cr);
   const u32 NF = S.NF, NR = S.NR;
@@ -383,7 +382,6 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       cnt[i] = j - (u32)i;
       map_insert_min(fme, mask, keys[i], (u32)i);
     }, st);
-    sync(st);
     dfree(keys);
   }
   // tables for the evaluator
@@ -533,7 +531,6 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       else if (stt == ST_SEMA) emit_diag(B, mkdiag(vf[v], S2.err.line, S2.err.col, S2.err.code, S2.err.msg, S2.err.a0, S2.err.a1, S2.err.a2));
       else if (!(out.k == V_BOOL && out.x == 1)) emit_diag(B, mkdiag(vf[v], t.line, t.col, C_E0104, M_S_ASSERT_FAIL));
     }, st);
-    sync(st);
     dfree(dt);
   }
 }

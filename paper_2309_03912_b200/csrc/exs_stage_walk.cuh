@@ -183,7 +183,6 @@ void grow(T*& p, u64& cap_or_dummy, u64 need, u64 used, cudaStream_t st) {
   u64 nc = need + need / 2 + 1024;
   T* q = dalloc<T>(nc);
   if (p && used) d2d(q, p, used * sizeof(T), st);
-  sync(st);
   dfree(p);
   p = q;
   cap_or_dummy = nc;
@@ -389,13 +388,13 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       par_for(NF, [=] EXS_HD (i64 i) { at_min(&v0[fr[i].view], (u32)i); }, st);
     }
     if (NRC) {
-      u64* key = dalloc<u64>(NRC);
+      u32* key = dalloc<u32>(NRC);
       const u32* rcc = rcand;
       par_for(NRC, [=] EXS_HD (i64 k) {
         const FnRec& r = fr[rcc[k] >> 1];
         const Node& fn = nd[r.node];
-        key[k] = (u64)(fn.n & (FF_H | FF_D | FF_G | FF_HPRED | FF_DPRED | FF_CX)) |
-                 ((u64)(r.rec != NONE) << 16) | ((u64)(cfgs[vf[r.view]] & CFG_MODE_MASK) << 17);
+        key[k] = (u32)(fn.n & (FF_H | FF_D | FF_G | FF_HPRED | FF_DPRED | FF_CX)) |
+                 ((u32)(r.rec != NONE) << 16) | ((u32)(cfgs[vf[r.view]] & CFG_MODE_MASK) << 17);
       }, st);
       sort_pairs(key, rcand, NRC, sc, st, 20);
       sync(st);
@@ -554,7 +553,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   // ---- levels
   u32 prev_n = 0;
   u32 level = 0;
-  u64 rank_lim = (u64)CK_FIELD_MAX + 1;  // bound on the parent ranks of the next frontier's keys
+  u64 rank_lim = (u64)CK_FIELD_MAX + 1;   // bounds on the parent ranks and locals
+  u64 local_lim = (u64)CK_FIELD_MAX + 1;  // of the next frontier's creation keys
   u32* front = nullptr;
   u64 front_cap = 0;
   u64 edges_used = 0;
@@ -594,57 +594,86 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     // frontier: new instances with a body to walk (IF_BODY: an empty,
     // parameterless body is left out -- creation keys only order the creators
     // among themselves, so dropping non-creators keeps them), by creation key
+    // (no host round trip: body instances sort first, the count stays on the
+    // device until the totals below are read)
     grow(front, front_cap, nnew + 1, 0, st);
-    u32 nf;
+    u32* tot = dalloc<u32>(4);  // edge slots, work items, frontier size, most call sites of a body
+    dzero(tot, 16, st);
     {
       const Inst* in = W.inst;
       u32 base = prev_n;
       u32* fr_tmp = dalloc<u32>(nnew + 1);
-      nf = select_idx(nnew, [=] EXS_HD (u32 j) -> bool { return (in[base + j].flags & IF_BODY) != 0; },
-                      fr_tmp, L.cnt, sc, st);
-      u64* keys = dalloc<u64>(nf + 1);
-      par_for(nf, [=] EXS_HD (i64 j) { fr_tmp[j] += base; keys[j] = in[fr_tmp[j]].ckey; }, st);
-      // the level bits are equal in a frontier, and parent ranks are below the
-      // previous frontier's size
-      int end_bit = CK_RANK_SHIFT;
-      while (end_bit < CK_LEVEL_SHIFT && (rank_lim >> (end_bit - CK_RANK_SHIFT))) end_bit++;
-      sort_pairs(keys, fr_tmp, nf, sc, st, end_bit);
-      d2d(front, fr_tmp, 4ull * nf, st);
-      dfree(keys);  // blocks are reused in stream order (cache_alloc): no wait
+      // sort keys: (parent rank, local) of the creation key -- the level bits
+      // are equal in a frontier, parent ranks are below the previous frontier's
+      // size and locals below twice its largest body's call sites -- and a flag
+      // bit above them that puts non-body instances last; 32-bit keys when
+      // they fit (fewer radix passes)
+      auto nbits = [](u64 lim) { int b = 0; while (b < 26 && (lim - 1) >> b) b++; return b; };
+      const int rbits = nbits(rank_lim), lbits = nbits(local_lim);
+      const int kbits = rbits + lbits + 1;
+      u32* nfd = tot + 2;
+      auto key_of = [=] EXS_HD (const Inst& I) -> u64 {
+        if (!(I.flags & IF_BODY)) return 1ull << (rbits + lbits);
+        const u64 rank = (I.ckey >> CK_RANK_SHIFT) & CK_FIELD_MAX, local = I.ckey & CK_FIELD_MAX;
+        return (rank << lbits) | local;
+      };
+      if (kbits <= 32) {
+        u32* keys = dalloc<u32>(nnew + 1);
+        par_for(nnew, [=] EXS_D (i64 j) {
+          const Inst& I = in[base + j];
+          keys[j] = (u32)key_of(I);
+          fr_tmp[j] = base + (u32)j;
+          if (I.flags & IF_BODY) at_inc_agg(nfd);
+        }, st);
+        sort_pairs(keys, fr_tmp, nnew, sc, st, kbits);
+        dfree(keys);  // blocks are reused in stream order (cache_alloc): no wait
+      } else {
+        u64* keys = dalloc<u64>(nnew + 1);
+        par_for(nnew, [=] EXS_D (i64 j) {
+          const Inst& I = in[base + j];
+          keys[j] = key_of(I);
+          fr_tmp[j] = base + (u32)j;
+          if (I.flags & IF_BODY) at_inc_agg(nfd);
+        }, st);
+        sort_pairs(keys, fr_tmp, nnew, sc, st, kbits);
+        dfree(keys);
+      }
+      d2d(front, fr_tmp, 4ull * nnew, st);
       dfree(fr_tmp);
     }
     prev_n = n_now;
     const u32 nnew_prev = nnew;  // new instances per level track the next level's
-    if (!nf) break;
     prof_mark(st);
     // edge bases (scan of call-site counts) and work items (scan of statement
-    // chunks), both totals read back in one round trip
+    // chunks) over the frontier; the three totals come back in one round trip
     const u32 KCH = EXS_KCH;
-    u32* ec = dalloc<u32>(nf + 1);
-    u32* eb = dalloc<u32>(nf + 1);
-    u32* wc = dalloc<u32>(nf + 1);
-    u32* wb = dalloc<u32>(nf + 1);
-    u32* tot = dalloc<u32>(2);
+    u32* ec = dalloc<u32>(nnew + 1);
+    u32* eb = dalloc<u32>(nnew + 1);
+    u32* wc = dalloc<u32>(nnew + 1);
+    u32* wb = dalloc<u32>(nnew + 1);
     {
-      const Inst* in = W.inst; const FnRec* fr = S.fns; const u32* fl = front;
-      par_for(nf + 1, [=] EXS_HD (i64 j) {
-        if (j < nf) {
+      const Inst* in = W.inst; const FnRec* fr = S.fns; const u32* fl = front; const u32* nfd = tot + 2;
+      par_for(nnew + 1, [=] EXS_HD (i64 j) {
+        if (j < *nfd) {
           const FnRec& r = fr[in[fl[j]].fn];
           ec[j] = r.ncalls;
           wc[j] = r.nstmts ? (r.nstmts + KCH - 1) / KCH : 1;
+          at_max_agg(tot + 3, r.ncalls);
         } else {
           ec[j] = 0;
           wc[j] = 0;
         }
       }, st);
     }
-    excl_scan_u32(ec, eb, nf + 1, sc, st);
-    excl_scan_u32(wc, wb, nf + 1, sc, st);
-    par_for(1, [=] EXS_HD (i64) { tot[0] = eb[nf]; tot[1] = wb[nf]; }, st);
-    u32 tot_h[2];
+    excl_scan_u32(ec, eb, nnew + 1, sc, st);
+    excl_scan_u32(wc, wb, nnew + 1, sc, st);
+    par_for(1, [=] EXS_HD (i64) { tot[0] = eb[nnew]; tot[1] = wb[nnew]; }, st);
+    u32 tot_h[4];
     d2h(tot_h, tot, sizeof tot_h, st);
     sync(st);
     dfree(tot);
+    const u32 nf = tot_h[2];
+    if (!nf) { dfree(ec); dfree(eb); dfree(wc); dfree(wb); break; }
     u64 S_level = tot_h[0];
     const u32 nwi = tot_h[1];
     W.callsites += S_level;
@@ -690,16 +719,16 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
 #if EXS_WALK_SORT
       if (nwi >= EXS_WALK_SORT_MIN) {  // a small level: the sort costs more than it saves
         perm = dalloc<u32>(nwi + 1);
-        u64* key = dalloc<u64>(nwi + 1);
+        u32* key = dalloc<u32>(nwi + 1);
         const Node* nd = P.nodes;
         par_for(nwi, [=] EXS_HD (i64 i) {
           const FnRec& r = fr[in[fl[itj[i]]].fn];
           u32 k = itc[i] * KCH;
-          u64 shape = 0;
+          u32 shape = 0;
           if (k < r.nstmts) {
             const Node& s = nd[sn[r.stmt_base + k]];
             u32 sub = s.c0 != NONE ? nd[s.c0].kind : 0;
-            shape = ((u64)s.kind << 8) | sub;
+            shape = ((u32)s.kind << 8) | sub;
           }
           key[i] = shape;
           perm[i] = (u32)i;
@@ -762,6 +791,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     dfree(wc);
     dfree(wb);
     rank_lim = std::min<u64>(nf, (u64)CK_FIELD_MAX + 1);
+    local_lim = std::min<u64>(std::max<u64>(2ull * tot_h[3], 1), (u64)CK_FIELD_MAX + 1);
     prof_mark(st);
     level++;
   }

@@ -366,34 +366,37 @@ class Analysis:
 
 class AnalysisList(Sequence):
     """The Analysis of every unit of one run, in input order, each built on
-    first access (a corpus run returns ~10k of them per GB)."""
+    first access (a corpus run returns ~10k of them per GB).  ``settings`` is
+    one (profile, mode) for every unit or a list of them."""
 
-    def __init__(self, units: list, results: CorpusResults):
-        self._units = units
+    def __init__(self, paths: list, settings, results: CorpusResults):
+        self._paths = paths
+        self._settings = settings
+        self._uniform = isinstance(settings, tuple)
         self._results = results
         self._made: dict = {}
 
     def __len__(self):
-        return len(self._units)
+        return len(self._paths)
 
     def _get(self, i: int) -> "Analysis":
         a = self._made.get(i)
         if a is None:
-            u = self._units[i]
-            a = self._made[i] = Analysis(u[1], u[2], u[3], self._results, i)
+            prof, mode = self._settings if self._uniform else self._settings[i]
+            a = self._made[i] = Analysis(self._paths[i], prof, mode, self._results, i)
         return a
 
     def __getitem__(self, i):
         if isinstance(i, slice):
-            return [self._get(k) for k in range(*i.indices(len(self._units)))]
+            return [self._get(k) for k in range(*i.indices(len(self._paths)))]
         if i < 0:
-            i += len(self._units)
-        if not 0 <= i < len(self._units):
+            i += len(self._paths)
+        if not 0 <= i < len(self._paths):
             raise IndexError(i)
         return self._get(i)
 
     def __iter__(self):
-        return (self._get(i) for i in range(len(self._units)))
+        return (self._get(i) for i in range(len(self._paths)))
 
 
 # ---------------------------------------------------------------------------
@@ -410,6 +413,16 @@ class Engine:
         self.batch_mib = batch_mib
         self.handle.set_option(7, batch_mib)
 
+    def _run(self, texts: list, paths: list, cfg: np.ndarray, settings) -> "AnalysisList":
+        """Streamed run without walk records; ``settings`` as in AnalysisList."""
+        with self.lock:
+            self.handle.set_option(1, 0)
+            self.handle.run_units(texts, cfg)
+            recs, text, first, lease = self.handle.lease_results()
+            self.last_stats = self.handle.stats()
+            self.last_result_bytes = recs.nbytes + text.nbytes + first.nbytes
+        return AnalysisList(paths, settings, CorpusResults(recs, text, first, paths, lease))
+
     def run_batch(self, units: list, want_walks: bool = False):
         """units: list of (text, path, CompileProfile, Mode, TraitConfig).
 
@@ -420,54 +433,52 @@ class Engine:
         memo: dict = {}
 
         def cb(u):
-            k = (u[2], u[3], u[4])
+            k = (id(u[2]), id(u[3]), id(u[4]))  # the units hold these objects: ids are stable
             b = memo.get(k)
             if b is None:
-                b = memo[k] = cfg_byte(*k)
+                b = memo[k] = cfg_byte(u[2], u[3], u[4])
             return b
         cfg = np.fromiter(map(cb, units), dtype=np.uint8, count=len(units))
         paths = [u[1] for u in units]
+        if not want_walks:
+            return self._run(texts, paths, cfg, [(u[2], u[3]) for u in units])
         with self.lock:
-            if want_walks:
-                # walk arrays describe one batch: keep the whole run in one
-                self.handle.set_option(7, 2047)
-            self.handle.set_option(1, 1 if want_walks else 0)
-            self.handle.run_units(texts, cfg)
+            # walk arrays describe one batch: keep the whole run in one
+            self.handle.set_option(7, 2047)
+            self.handle.set_option(1, 1)
+            try:
+                self.handle.run_units(texts, cfg)
+            finally:
+                self.handle.set_option(7, self.batch_mib)
             recs, text, first, lease = self.handle.lease_results()
             self.last_stats = self.handle.stats()
             self.last_result_bytes = recs.nbytes + text.nbytes + first.nbytes
             results = CorpusResults(recs, text, first, paths, lease)
-            walks = status = batch = None
-            if want_walks:
-                if self.last_stats["batches"] != 1:
-                    raise ValueError("want_walks needs the units to fit one batch (< 2 GiB)")
-                walks = self.handle.walk_stats(len(units))
-                status = self.handle.pass_status(len(units))
-                blobs = [t.encode("utf-8", "surrogateescape") if isinstance(t, str) else bytes(t) for t in texts]
-                offsets = [0]
-                for b in blobs:
-                    offsets.append(offsets[-1] + len(b))
-                ren = Renderer(b"".join(blobs), offsets, self.handle.arena(), self.handle.describe)
-                # the walk arrays stay valid until the next run on this engine:
-                # snapshot them now (lazily rendered afterwards)
-                batch = BatchWalks(self.handle, ren, status, [u[3] for u in units])
-                batch._load()
-                self.handle.set_option(7, self.batch_mib)
-        if walks is None:
-            return AnalysisList(units, results)
+            if self.last_stats["batches"] != 1:
+                raise ValueError("want_walks needs the units to fit one batch (< 2 GiB)")
+            walks = self.handle.walk_stats(len(units))
+            status = self.handle.pass_status(len(units))
+            blobs = [t.encode("utf-8", "surrogateescape") if isinstance(t, str) else bytes(t) for t in texts]
+            offsets = [0]
+            for b in blobs:
+                offsets.append(offsets[-1] + len(b))
+            ren = Renderer(b"".join(blobs), offsets, self.handle.arena(), self.handle.describe)
+            # the walk arrays stay valid until the next run on this engine:
+            # snapshot them now (lazily rendered afterwards)
+            batch = BatchWalks(self.handle, ren, status, [u[3] for u in units])
+            batch._load()
         out = []
         for f, u in enumerate(units):
             a = Analysis(u[1], u[2], u[3], results, f, batch)
-            if walks is not None:
-                for p, side in ((0, HOST), (1, DEVICE)):
-                    w = walks[2 * f + p]
-                    if w["exists"]:
-                        a.walks[side] = WalkSummary(side, int(w["instances"]), int(w["edges"]),
-                                                    int(w["demands"]), batch, (f, p))
-                for p, kind in enumerate(u[2].pass_kinds()):
-                    s = status[2 * f + p]
-                    a.passes[kind] = {"pp_line": int(s["pp_line"]), "lex_line": int(s["lex_line"]),
-                                      "parse_failed": bool(s["parse_failed"])}
+            for p, side in ((0, HOST), (1, DEVICE)):
+                w = walks[2 * f + p]
+                if w["exists"]:
+                    a.walks[side] = WalkSummary(side, int(w["instances"]), int(w["edges"]),
+                                                int(w["demands"]), batch, (f, p))
+            for p, kind in enumerate(u[2].pass_kinds()):
+                s = status[2 * f + p]
+                a.passes[kind] = {"pp_line": int(s["pp_line"]), "lex_line": int(s["lex_line"]),
+                                  "parse_failed": bool(s["parse_failed"])}
             out.append(a)
         return out
 
@@ -505,13 +516,14 @@ def analyze_corpus(units: Iterable, profile: CompileProfile = CompileProfile(),
     ``units`` yields (path, text) or (path, text, profile, mode, cfg); any
     total size (the library streams them in batches).  Returns one Analysis
     per unit, in input order."""
-    packed = []
-    for u in units:
-        if len(u) == 2:
-            packed.append((u[1], u[0], profile, mode, cfg))
-        else:
-            packed.append((u[1], u[0], u[2], u[3], u[4]))
-    return (engine or get_engine(device)).run_batch(packed, want_walks=want_walks)
+    units = units if isinstance(units, list) else list(units)
+    eng = engine or get_engine(device)
+    if not want_walks and all(len(u) == 2 for u in units):
+        # one setting for every unit: no per-unit tuples or cfg lookups
+        cfg_all = np.full(len(units), cfg_byte(profile, mode, cfg), dtype=np.uint8)
+        return eng._run([u[1] for u in units], [u[0] for u in units], cfg_all, (profile, mode))
+    packed = [(u[1], u[0], profile, mode, cfg) if len(u) == 2 else (u[1], u[0], u[2], u[3], u[4]) for u in units]
+    return eng.run_batch(packed, want_walks=want_walks)
 
 
 def declared_spaces(spec: int) -> frozenset:

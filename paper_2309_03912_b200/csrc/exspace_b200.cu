@@ -1117,23 +1117,61 @@ static void run_units_pipelined(Handle& H, const char* const* texts, const uint6
   exs_stats acc{};
   float t_stage[4] = {0, 0, 0, 0};
   auto t0 = std::chrono::steady_clock::now();
-  auto worker = [&](Handle& P, size_t first, std::string& err) {
+  static const bool trace = getenv("EXS_TRACE_UNITS") != nullptr;
+  auto ms_since = [t0]() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
+  // batches are claimed from a shared counter (a pipeline that finishes early
+  // takes the next one) and a pipeline packs its next batch into its second
+  // staging buffer while the device analyses the current one; results are
+  // appended in batch order (turn counter)
+  std::atomic<size_t> next_batch{0};
+  auto worker = [&](Handle& P, int id, std::string& err) {
     try {
       bind_stream(P);
       static_init(P);
       P.sink = &H;
       P.stage[0].ensure(maxb + 64, 0);
+      P.stage[1].ensure(maxb + 64, 0);
       ensure_slot(P, 0, maxb + 64);
-      for (size_t b = first; b < plan.size(); b += 2) {
+      double a0 = 0, a1 = 0;
+      auto pack = [&](size_t b, int k) {
         const BatchPlan& B = plan[b];
-        pack_units(texts, lens, B.u0, B.u1, B.off.data(), P.stage[0].p, nthreads);
-        memset(P.stage[0].p + B.bytes, 0, 64);
-        h2d(P.d_slot[0], P.stage[0].p, B.bytes + 64, P.st);  // same stream as the analysis
-        P.cur_batch = b;
-        run_batch(P, P.d_slot[0], B.bytes, B.off.data(), (u32)(B.u1 - B.u0), cfg + B.u0, B.u0);
-        std::lock_guard<std::mutex> g(acc_mu);
-        add_stats(acc, P.stats);
-        for (int q = 0; q < 4; q++) t_stage[q] += P.t_stage[q];
+        pack_units(texts, lens, B.u0, B.u1, B.off.data(), P.stage[k].p, nthreads);
+        memset(P.stage[k].p + B.bytes, 0, 64);
+      };
+      size_t b = next_batch.fetch_add(1);
+      int k = 0;
+      if (b < plan.size()) { a0 = ms_since(); pack(b, k); a1 = ms_since(); }
+      while (b < plan.size()) {
+        const BatchPlan& B = plan[b];
+        h2d(P.d_slot[0], P.stage[k].p, B.bytes + 64, P.st);  // same stream as the analysis
+        const size_t nb = next_batch.fetch_add(1);
+        std::thread ahead;
+        std::string ahead_err;
+        double n0 = 0, n1 = 0;
+        if (nb < plan.size())
+          ahead = std::thread([&, nb, k]() {
+            try { n0 = ms_since(); pack(nb, 1 - k); n1 = ms_since(); } catch (const std::exception& e) { ahead_err = e.what(); }
+          });
+        try {
+          P.cur_batch = b;
+          run_batch(P, P.d_slot[0], B.bytes, B.off.data(), (u32)(B.u1 - B.u0), cfg + B.u0, B.u0);
+        } catch (...) {
+          if (ahead.joinable()) ahead.join();
+          throw;
+        }
+        if (ahead.joinable()) ahead.join();
+        if (!ahead_err.empty()) throw Err(ahead_err);
+        if (trace)
+          fprintf(stderr, "[run_units] pipeline %d batch %zu (%.1f MB): packed %.1f..%.1f, analysed by %.1f ms (device %.1f)\n",
+                  id, b, B.bytes / 1e6, a0, a1, ms_since(), P.stats.ms_total);
+        {
+          std::lock_guard<std::mutex> g(acc_mu);
+          add_stats(acc, P.stats);
+          for (int q = 0; q < 4; q++) t_stage[q] += P.t_stage[q];
+        }
+        b = nb; k = 1 - k; a0 = n0; a1 = n1;
       }
     } catch (const std::exception& e) {
       err = e.what();

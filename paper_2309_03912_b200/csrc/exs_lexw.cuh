@@ -151,6 +151,28 @@ EXS_HD inline u32 word_of(const u32 r[8], u32 k) {  // r[k] without local memory
                : (k < 6 ? (k == 4 ? r[4] : r[5]) : (k == 6 ? r[6] : r[7]));
 }
 EXS_HD inline u8 byte_of(const u32 r[8], u32 j) { return (u8)(word_of(r, j >> 2) >> (8 * (j & 3))); }
+EXS_HD inline u32 ffs32(u32 x) {  // index of the lowest set bit (x != 0)
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  return (u32)__ffs((int)x) - 1;
+#else
+  return (u32)__builtin_ctz(x);
+#endif
+}
+EXS_HD inline u32 hib32(u32 x) {  // index of the highest set bit (x != 0)
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  return 31u - (u32)__clz((int)x);
+#else
+  return 31u - (u32)__builtin_clz(x);
+#endif
+}
+EXS_HD inline u32 popc32(u32 x) {
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  return (u32)__popc(x);
+#else
+  return (u32)__builtin_popcount(x);
+#endif
+}
+
 // sequential reader of a token's bytes: registers inside the word (one select
 // chain per 4 bytes), global memory past it
 struct ByteCursor {
@@ -201,6 +223,51 @@ EXS_HD inline bool is_single(u8 c) {
   return c == '{' || c == '}' || c == '(' || c == ')' || c == ',' || c == ';' || c == '.';
 }
 
+// The comment DFA over one word from state st, event-driven: between the
+// bytes where the current state can change -- '"' or '/' in code, '"' or '\n'
+// in a string, '\n' in a line comment, '*' in a block comment, any byte after
+// a '/' in code or a '*' in a block comment, and file starts (reset to code);
+// never a spliced byte -- the state is constant, so a word costs one step per
+// such byte instead of one per byte.  Q, SL, ST, NL: byte masks of '"', '/',
+// '*', '\n'; only bytes of `lim` are events.  With MASKS, the state before
+// every byte is reported as bl (comment text and openers), sm (string),
+// sbb (block comment) -- the per-byte loop it replaces: lex_word phase 1.
+// Returns the state after the word.
+template <bool MASKS>
+EXS_HD inline u32 dfa_word(u32 st, const u32 r[8], u32 Q, u32 SL, u32 ST, u32 NL, u32 spw, u32 fsw, u32 lim,
+                           u32& bl, u32& sm, u32& sbb) {
+  const u32 ns = ~spw;
+  u32 p = 0;
+  while (true) {
+    u32 evs;
+    if (st == S_CODE) evs = (Q | SL) & ns;
+    else if (st == S_STR) evs = (Q | NL) & ns;
+    else if (st == S_LINE) evs = NL & ns;
+    else if (st == S_BLOCK) evs = ST & ns;
+    else evs = ns;  // S_SLASH, S_STAR: the next byte decides
+    const u32 cand = (evs | fsw) & lim & (p >= 32 ? 0u : (~0u << p));
+    const u32 e = cand ? ffs32(cand) : 32u;
+    if (MASKS && e > p) {
+      const u32 run = (e >= 32 ? ~0u : ((1u << e) - 1)) & ~((1u << p) - 1);
+      if (st >= S_LINE) bl |= run;
+      if (st == S_STR) sm |= run;
+      if (st == S_BLOCK) sbb |= run;
+    }
+    if (e >= 32) break;
+    const u32 b = 1u << e;
+    if (fsw & b) st = S_CODE;
+    if (MASKS) {
+      if (st >= S_LINE) bl |= b;
+      if (st == S_STR) sm |= b;
+      if (st == S_BLOCK) sbb |= b;
+      if (st == S_SLASH && (ns & b) && ((SL | ST) & b)) bl |= b | (b >> 1);  // opener
+    }
+    if (ns & b) st = (dfa_class_map(byte_of(r, e)) >> (4 * st)) & 15u;
+    p = e + 1;
+  }
+  return st;
+}
+
 // K2: per-word scan record and special flag
 EXS_HD inline WScan word_info(const LexW& X, u32 w, u8& special, u32& nhash) {
   WScan o{MAP_ID, 0, 0};
@@ -210,28 +277,36 @@ EXS_HD inline WScan word_info(const LexW& X, u32 w, u8& special, u32& nhash) {
   u32 r[8];
   load_word(X, base, r);
   const u32 spw = X.sp[w], fsw = X.fs[w];
-  u32 s0 = 0, s1 = 1, s2 = 2, s3 = 3, s4 = 4, s5 = 5;
-  u32 nls = 0, nnl = 0, spec = 0, nh = 0;
-  bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
+  const bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
   const u32 m = X.n - base < 32 ? X.n - base : 32;
+  const u32 valid = m == 32 ? ~0u : ((1u << m) - 1);
+  // byte masks (branch-uniform, unrolled)
+  u32 Q = 0, SL = 0, ST = 0, NL = 0, HS = 0, HI = 0;
 #pragma unroll
   for (u32 j = 0; j < 32; j++) {
-    if (j < m) {
-      const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
-      const bool spl = (spw >> j) & 1u, fsb = (fsw >> j) & 1u;
-      if (fsb) { s0 = s1 = s2 = s3 = s4 = s5 = S_CODE; }
-      if (fsb || prev_nl) { nls++; o.lsp = base + j; }
-      nnl += c == '\n';
-      spec |= (u32)(spl || c >= 0x80 || c == '#');
-      nh += c == '#';
-      if (!spl) {
-        const u32 mp = dfa_class_map(c);
-        s0 = (mp >> (4 * s0)) & 15u; s1 = (mp >> (4 * s1)) & 15u; s2 = (mp >> (4 * s2)) & 15u;
-        s3 = (mp >> (4 * s3)) & 15u; s4 = (mp >> (4 * s4)) & 15u; s5 = (mp >> (4 * s5)) & 15u;
-      }
-      prev_nl = c == '\n' && !spl;
-    }
+    const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
+    const u32 b = 1u << j;
+    if (c == '"') Q |= b;
+    if (c == '/') SL |= b;
+    if (c == '*') ST |= b;
+    if (c == '\n') NL |= b;
+    if (c == '#') HS |= b;
+    if (c >= 0x80) HI |= b;
   }
+  Q &= valid; SL &= valid; ST &= valid; NL &= valid; HS &= valid; HI &= valid;
+  // logical line starts: file starts and bytes after a non-spliced newline
+  const u32 ls = (fsw | ((NL & ~spw) << 1) | (prev_nl ? 1u : 0u)) & valid;
+  if (ls) o.lsp = base + hib32(ls);
+  const u32 nls = popc32(ls), nnl = popc32(NL);
+  const u32 spec = ((spw & valid) | HS | HI) != 0, nh = popc32(HS);
+  // the comment-DFA transfer map: one event-driven pass per start state
+  u32 d0 = 0, d1 = 0, d2 = 0;
+  const u32 s0 = dfa_word<false>(0, r, Q, SL, ST, NL, spw, fsw & valid, valid, d0, d1, d2);
+  const u32 s1 = dfa_word<false>(1, r, Q, SL, ST, NL, spw, fsw & valid, valid, d0, d1, d2);
+  const u32 s2 = dfa_word<false>(2, r, Q, SL, ST, NL, spw, fsw & valid, valid, d0, d1, d2);
+  const u32 s3 = dfa_word<false>(3, r, Q, SL, ST, NL, spw, fsw & valid, valid, d0, d1, d2);
+  const u32 s4 = dfa_word<false>(4, r, Q, SL, ST, NL, spw, fsw & valid, valid, d0, d1, d2);
+  const u32 s5 = dfa_word<false>(5, r, Q, SL, ST, NL, spw, fsw & valid, valid, d0, d1, d2);
   special = (u8)spec; nhash = nh;
   o.map = s0 | (s1 << 4) | (s2 << 8) | (s3 << 12) | (s4 << 16) | (s5 << 20);
   o.lc = ((u64)nls << 32) | nnl;
@@ -261,28 +336,6 @@ EXS_HD inline u32 logical_line_end(const LexW& X, u32 lo, u32 fend) {
   u32 q = lo;
   while (q < fend && !(X.src[q] == '\n' && !bit_get(X.sp, q))) q++;
   return q;
-}
-
-EXS_HD inline u32 ffs32(u32 x) {  // index of the lowest set bit (x != 0)
-#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
-  return (u32)__ffs((int)x) - 1;
-#else
-  return (u32)__builtin_ctz(x);
-#endif
-}
-EXS_HD inline u32 hib32(u32 x) {  // index of the highest set bit (x != 0)
-#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
-  return 31u - (u32)__clz((int)x);
-#else
-  return 31u - (u32)__builtin_clz(x);
-#endif
-}
-EXS_HD inline u32 popc32(u32 x) {
-#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
-  return (u32)__popc(x);
-#else
-  return (u32)__builtin_popcount(x);
-#endif
 }
 
 // K3: count (EMIT=false) or emit (EMIT=true) the tokens attributed to word w.
@@ -320,26 +373,17 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
     DGc = M.DGc; IDc = M.IDc; qs = M.qs; qt = M.qt; sm = M.sm; pst = M.pst; sbb = 0;
     fend = X.foff[f + 1];
   } else {
-  bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
-  // ---- phase 1
+  const bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
+  // ---- phase 1: byte-class masks (branch-uniform, unrolled), then the
+  // comment-DFA states before every byte, event-driven (dfa_word)
   u32 bl = 0;
-  sm = 0; sbb = 0; nl = 0; lsb = 0; qt = 0;
-  u32 id = 0, dg = 0, ws = 0, ps = 0, sg = 0, sl = 0;
+  sm = 0; sbb = 0; nl = 0; qt = 0;
+  u32 id = 0, dg = 0, ws = 0, ps = 0, sg = 0, sl = 0, star = 0;
 #pragma unroll
   for (u32 j = 0; j < 32; j++) {
     const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
     const u32 b = 1u << j;
-    const bool spl = (spw & b) != 0, fsb = (fsw & b) != 0;
-    if (fsb) st = S_CODE;
-    const u32 sb = st;
-    if (!spl) st = (dfa_class_map(c) >> (4 * st)) & 15u;
-    if (sb >= S_LINE) bl |= b;                                     // comment text
-    if (sb == S_SLASH && (c == '/' || c == '*') && !spl) bl |= b | (b >> 1);  // opener
-    if (sb == S_STR) sm |= b;                                      // string text and closing quote
-    if (sb == S_BLOCK) sbb |= b;
     if (c == '\n') nl |= b;
-    if (fsb || prev_nl) lsb |= b;
-    prev_nl = c == '\n' && !spl;
     if (is_ident_char(c)) id |= b;
     if (is_digit(c)) dg |= b;
     if (c == ' ' || c == '\t' || c == '\r') ws |= b;
@@ -347,7 +391,10 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
     if (is_single(c)) sg |= b;
     if (c == '"') qt |= b;
     if (c == '/') sl |= b;
+    if (c == '*') star |= b;
   }
+  lsb = fsw | ((nl & ~spw) << 1) | (prev_nl ? 1u : 0u);
+  dfa_word<true>(st, r, qt, sl, star, nl, spw, fsw, ~0u, bl, sm, sbb);
   lsb &= valid; nl &= valid;
   // ---- special lines: bytes excluded from the plain tokenizer; owned ones
   u32 spm = 0;

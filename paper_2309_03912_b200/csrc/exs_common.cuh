@@ -195,6 +195,28 @@ static_assert(sizeof(Diag) == 48, "diag record is 48 bytes");
 
 EXS_HD inline u64 fnv_init() { return 1469598103934665603ull; }
 EXS_HD inline u64 fnv_step(u64 h, u8 c) { return (h ^ c) * 1099511628211ull; }
+
+// Name hash of a token's text (identifiers, string contents, pragma names):
+// FNV-1a steps over 4-byte little-endian chunks of the text (the last one
+// zero-padded), then the length, then a final avalanche.  Every step is a
+// bijection of the state, so two different texts of the same length never
+// share a hash.  The word-parallel lexer feeds whole chunks from registers
+// (four bytes per step); the line lexer streams bytes into the same chunks.
+EXS_HD constexpr u64 nh_mix(u64 h, u32 x) { return (h ^ x) * 1099511628211ull; }
+EXS_HD constexpr u64 nh_fin(u64 h, u32 len) {
+  h = nh_mix(h, len);
+  h ^= h >> 33; h *= 0xff51afd7ed558ccdull; h ^= h >> 33;
+  return h;
+}
+struct NameHash {
+  u64 h = 1469598103934665603ull;
+  u32 acc = 0, n = 0;
+  EXS_HD void step(u8 c) {
+    acc |= (u32)c << (8 * (n & 3));
+    if ((++n & 3) == 0) { h = nh_mix(h, acc); acc = 0; }
+  }
+  EXS_HD u64 done() const { return nh_fin((n & 3) ? nh_mix(h, acc) : h, n); }
+};
 EXS_HD inline u64 mix64(u64 x) {
   x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ull;
   x ^= x >> 27; x *= 0x94d049bb133111ebull;

@@ -168,18 +168,25 @@ __constant__ char kVocabDev[] = EXS_VOCAB_TEXT;
 #endif
 static const char kVocabHost[] = EXS_VOCAB_TEXT;
 
-// compile-time FNV-1a of a vocabulary word (same function the lexer streams)
-constexpr u64 fnv_c(const char* s, u64 h = 1469598103934665603ull) {
-  return *s ? fnv_c(s + 1, (h ^ (u8)*s) * 1099511628211ull) : h;
-}
 constexpr u32 len_c(const char* s) { return *s ? 1 + len_c(s + 1) : 0; }
+// compile-time name hash of a vocabulary word (NameHash: the lexer's function)
+constexpr u64 name_hash_c(const char* s) {
+  u64 h = 1469598103934665603ull;
+  const u32 n = len_c(s);
+  for (u32 q = 0; q < n; q += 4) {
+    u32 x = 0;
+    for (u32 k = 0; k < 4 && q + k < n; k++) x |= (u32)(u8)s[q + k] << (8 * k);
+    h = nh_mix(h, x);
+  }
+  return nh_fin(h, n);
+}
 
 // Vocabulary id from the token's text hash and length: a perfect hash over
 // the 38 words (multiplier found offline: slot = (hv * K) >> 57, collision-
 // free) -- one table load, no divergent compare tree.
 struct VEnt { u64 hv; u32 len; u32 id; };
 struct VTable { VEnt e[128]; };
-constexpr u64 kVocabK = 0x326324dfb695ffbull;
+constexpr u64 kVocabK = 0x83595d744d2f1383ull;  // tests/emu/vocab_k.py
 EXS_HD constexpr u32 vocab_slot(u64 hv) { return (u32)((hv * kVocabK) >> 57); }
 constexpr VTable make_vtable() {
   VTable t{};
@@ -196,7 +203,7 @@ constexpr VTable make_vtable() {
                     W_ABORT, W_CUDASYNC, W_HD_WARNING_DISABLE, W_NV_EXEC_CHECK_DISABLE, W_BANG_STR,
                     W_LPAREN_STR};
   for (u32 i = 0; i < sizeof(ids); i++) {
-    const u64 h = fnv_c(ws[i]);
+    const u64 h = name_hash_c(ws[i]);
     t.e[vocab_slot(h)] = VEnt{h, len_c(ws[i]), ids[i]};
   }
   return t;
@@ -494,7 +501,7 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
       u32 consumed = 1;
       int nw = 0; bool inword = false, first_ok = true;
       u8 wbuf[8]; u32 wl = 0;
-      u32 name_pos = 0, name_end = 0; u64 h = fnv_init(); u32 nl = 0;
+      u32 name_pos = 0, name_end = 0; NameHash nh; u32 nl = 0;
       have = b.next(c, pos, w);
       bool acc = true;
       // lexer.py:67-70: isalnum, '_', ' ' and '\t' continue the directive
@@ -508,7 +515,7 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
         if (!spc) {
           if (!inword) { nw++; inword = true; if (nw == 2) name_pos = pos; }
           if (nw == 1) { if (wl < 8) wbuf[wl] = c; wl++; }
-          if (nw == 2) { h = fnv_step(h, c); nl++; name_end = pos + 1; }
+          if (nw == 2) { nh.step(c); nl++; name_end = pos + 1; }
         } else {
           inword = false;
         }
@@ -523,6 +530,7 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
       if (out) {
         Tok t;
         TokStore ts_{out + n, &t};
+        const u64 h = nh.done();
         t.pos = name_pos; t.end = name_end; t.line = line_no; t.col = tcol; t.hv = h;
         t.kind = TK_PRAGMA; t.id = vocab_hash(h, nl); t.mask = mask; t.flags = 0; t.file = file;
       }
@@ -532,7 +540,7 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
     }
     if (c == '"') {
       u32 cw = 1;
-      u64 h = fnv_init(); u32 nl = 0;
+      NameHash nh; u32 nl = 0;
       u32 cstart = NONE, cend = 0;
       bool closed = false;
       have = b.next(c, pos, w);
@@ -540,7 +548,7 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
         if (c == '"' && w) { closed = true; cw += 1; break; }
         if (cstart == NONE) cstart = pos;
         cend = pos + 1;
-        h = fnv_step(h, c);
+        nh.step(c);
         nl++;
         cw += w;
         have = b.next(c, pos, w);
@@ -553,6 +561,7 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
         Tok t;
         TokStore ts_{out + n, &t};
         t.pos = cstart == NONE ? pos : cstart; t.end = cstart == NONE ? pos : cend;
+        const u64 h = nh.done();
         t.line = line_no; t.col = tcol; t.hv = h;
         t.kind = TK_STRING; t.id = vocab_hash(h, nl); t.mask = mask; t.flags = 0; t.file = file;
       }
@@ -567,7 +576,7 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
     const u8 k0 = char_class(s, c, pos, hi);
     if ((k0 & (UC_DIGIT | UC_ALPHA)) || c == '_') {
       bool digits = (k0 & UC_DIGIT) != 0;
-      u64 h = fnv_init(), val = 0; bool ovf = false;
+      NameHash nh; u64 val = 0; bool ovf = false;
       u32 nl = 0, ncp = 0; u32 last = pos; bool spl = false;
       u32 prevpos = pos;
       bool acc = true;  // the current code point is part of the token
@@ -593,13 +602,14 @@ EXS_HD inline u32 lex_line(const u8* s, const u32* sp, u32 lo, u32 hi, u8 st, u3
         if (!ok) break;
         if (pos != prevpos + 1 && nl) spl = true;
         prevpos = pos;
-        h = fnv_step(h, c);
+        nh.step(c);
         nl++;
         ncp += w;
         last = pos;
         have = b.next(c, pos, w);
       }
       if (out) {
+        const u64 h = nh.done();
         Tok t;
         TokStore ts_{out + n, &t};
         t.pos = tpos; t.end = last + 1; t.line = line_no; t.col = tcol;

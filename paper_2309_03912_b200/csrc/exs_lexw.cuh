@@ -188,6 +188,40 @@ struct ByteCursor {
   }
 };
 
+// bytes [q, q + 4) as a little-endian word: from the registers inside the
+// word at `base`, else two aligned loads (the batch ends in 64 zero bytes)
+EXS_HD inline u32 chunk_at(const LexW& X, const u32 r[8], u32 base, u32 q) {
+  const u32 o = q - base, sh = 8 * (q & 3);
+  u32 lo, hi;
+  if (o + 4 <= 32) {
+    lo = word_of(r, o >> 2);
+    hi = (o >> 2) < 7 ? word_of(r, (o >> 2) + 1) : 0u;
+  } else if (X.vec) {
+    const u32* s32 = reinterpret_cast<const u32*>(X.src);
+    lo = s32[q >> 2];
+    hi = s32[(q >> 2) + 1];
+  } else {
+    u32 x = 0;
+    for (u32 k = 0; k < 4; k++) x |= (u32)X.src[q + k] << (8 * k);
+    return x;
+  }
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  return __funnelshift_r(lo, hi, sh);
+#else
+  return sh ? (lo >> sh) | (hi << (32 - sh)) : lo;
+#endif
+}
+// NameHash of the bytes [lo, hi), four at a step
+EXS_HD inline u64 name_hash_range(const LexW& X, const u32 r[8], u32 base, u32 lo, u32 hi) {
+  u64 h = 1469598103934665603ull;
+  for (u32 q = lo; q < hi; q += 4) {
+    u32 x = chunk_at(X, r, base, q);
+    if (hi - q < 4) x &= (1u << (8 * (hi - q))) - 1;
+    h = nh_mix(h, x);
+  }
+  return nh_fin(h, hi - lo);
+}
+
 // bit k (k < 4) set where byte k of x equals c
 EXS_HD inline u32 byte_eq_mask(u32 x, u8 c) {
 #if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
@@ -316,18 +350,32 @@ EXS_HD inline WScan word_info(const LexW& X, u32 w, u8& special, u32& nhash) {
 // K2b: flag the logical lines holding a special byte (word w has one)
 EXS_HD inline void mark_special(const LexW& X, u32 w) {
   const u32 base = w * 32;
-  u32 li = w ? (u32)(X.wsc[w - 1].lc >> 32) - 1 : NONE;
-  bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
+  const u32 li0 = w ? (u32)(X.wsc[w - 1].lc >> 32) - 1 : NONE;  // NONE + 1 wraps to line 0
+  const bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
   const u32 spw = X.sp[w], fsw = X.fs[w];
-  for (u32 j = 0; j < 32 && base + j < X.n; j++) {
-    u8 c = X.src[base + j];
-    bool spl = (spw >> j) & 1u;
-    if (((fsw >> j) & 1u) || prev_nl) li++;
-    if ((spl || c >= 0x80 || c == '#') && !X.special[li]) {
+  const u32 m = X.n - base < 32 ? X.n - base : 32;
+  const u32 valid = m == 32 ? ~0u : ((1u << m) - 1);
+  u32 r[8];
+  load_word(X, base, r);
+  u32 NL = 0, SPC = 0;
+#pragma unroll
+  for (u32 j = 0; j < 32; j++) {
+    const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
+    if (c == '\n') NL |= 1u << j;
+    if (c >= 0x80 || c == '#') SPC |= 1u << j;
+  }
+  const u32 ls = (fsw | ((NL & ~spw) << 1) | (prev_nl ? 1u : 0u)) & valid;
+  u32 spc = (SPC | spw) & valid;
+  while (spc) {  // the first special byte of each logical line
+    const u32 j = ffs32(spc);
+    const u32 upto = j == 31 ? ~0u : ((2u << j) - 1);
+    const u32 li = li0 + popc32(ls & upto);
+    if (!X.special[li]) {
       X.special[li] = 1;
       at_add(X.nspecial, 1u);
     }
-    prev_nl = c == '\n' && !spl;
+    const u32 later = ls & ~upto;  // skip to the next line start
+    spc &= later ? ~((1u << ffs32(later)) - 1) : 0u;
   }
 }
 
@@ -580,22 +628,21 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
         end = base + 32;
         while (end < fend && (num ? is_digit(X.src[end]) : is_ident_char(X.src[end]))) end++;
       }
-      u64 h = fnv_init(), v = 0;
-      bool ovf = false;
-      ByteCursor bc{r, X.src, base, 8u, 0u};
-      for (u32 q = i; q < end; q++) {
-        const u8 ch = bc.at(q);
-        if (num) {
-          const u64 nv = v * 10 + (ch - '0');
+      t.end = end;
+      if (num) {
+        u64 v = 0;
+        bool ovf = false;
+        ByteCursor bc{r, X.src, base, 8u, 0u};
+        for (u32 q = i; q < end; q++) {
+          const u64 nv = v * 10 + (bc.at(q) - '0');
           if (v > 1844674407370955161ull || nv < v) ovf = true;
           v = nv;
-        } else {
-          h = fnv_step(h, ch);
         }
+        t.kind = TK_INT; t.hv = v; t.flags = ovf ? TF_INT_OVERFLOW : 0;
+      } else {
+        const u64 h = name_hash_range(X, r, base, i, end);
+        t.kind = TK_IDENT; t.hv = h; t.id = vocab_hash(h, end - i);
       }
-      t.end = end;
-      if (num) { t.kind = TK_INT; t.hv = v; t.flags = ovf ? TF_INT_OVERFLOW : 0; }
-      else { t.kind = TK_IDENT; t.hv = h; t.id = vocab_hash(h, end - i); }
     } else if (qs & bj) {
       // the closing quote: first quote in string state after i, unless a newline
       // or the file end comes first (unterminated: an error and a dead slot)
@@ -613,9 +660,7 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
       }
       t.kind = TK_STRING;
       if (term) {
-        u64 h = fnv_init();
-        ByteCursor bc{r, X.src, base, 8u, 0u};
-        for (u32 q = i + 1; q < close; q++) h = fnv_step(h, bc.at(q));
+        const u64 h = name_hash_range(X, r, base, i + 1, close);
         const u32 len = close - i - 1;
         t.pos = len ? i + 1 : close; t.end = close; t.hv = h; t.id = vocab_hash(h, len);
       } else {

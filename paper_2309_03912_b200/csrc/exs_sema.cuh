@@ -11,11 +11,17 @@ namespace exs {
 
 enum { ST_OK = 0, ST_SUBST = 1, ST_SEMA = 2 };
 enum { V_NONE = 0, V_TYPE, V_HDC, V_BOOL, V_INT };
-// builtin type name hashes are FNV of the words (lexer computes the same)
+// name hashes of fixed words (NameHash: the lexer computes the same for tokens)
 EXS_HD constexpr inline u64 word_hash(const char* w) {
+  u32 n = 0;
+  while (w[n]) n++;
   u64 h = 1469598103934665603ull;
-  while (*w) h = (h ^ (u8)*w++) * 1099511628211ull;
-  return h;
+  for (u32 q = 0; q < n; q += 4) {
+    u32 x = 0;
+    for (u32 k = 0; k < 4 && q + k < n; k++) x |= (u32)(u8)w[q + k] << (8 * k);
+    h = nh_mix(h, x);
+  }
+  return nh_fin(h, n);
 }
 constexpr u64 H_INT = word_hash("int"), H_BOOL = word_hash("bool"), H_HDC_MEMBER = word_hash("hdc"),
               H_STD = word_hash("std::");

@@ -553,8 +553,10 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   // ---- levels
   u32 prev_n = 0;
   u32 level = 0;
-  u64 rank_lim = (u64)CK_FIELD_MAX + 1;   // bounds on the parent ranks and locals
-  u64 local_lim = (u64)CK_FIELD_MAX + 1;  // of the next frontier's creation keys
+  // bounds on the parent ranks and locals of the next frontier's creation
+  // keys; the roots': decl indices and the side order
+  u64 rank_lim = std::min<u64>(std::max<u64>(NF, 1), (u64)CK_FIELD_MAX + 1);
+  u64 local_lim = 2;
   u32* front = nullptr;
   u64 front_cap = 0;
   u64 edges_used = 0;
@@ -605,15 +607,18 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       u32* fr_tmp = dalloc<u32>(nnew + 1);
       // sort keys: (parent rank, local) of the creation key -- the level bits
       // are equal in a frontier, parent ranks are below the previous frontier's
-      // size and locals below twice its largest body's call sites -- and a flag
-      // bit above them that puts non-body instances last; 32-bit keys when
-      // they fit (fewer radix passes)
+      // size and locals below twice its largest body's call sites -- with the
+      // non-body instances last; 32-bit keys when they fit (fewer radix passes)
       auto nbits = [](u64 lim) { int b = 0; while (b < 26 && (lim - 1) >> b) b++; return b; };
       const int rbits = nbits(rank_lim), lbits = nbits(local_lim);
-      const int kbits = rbits + lbits + 1;
+      // non-body instances: the all-ones key when no body key reaches it
+      // (a bound below its field's power of two), else a flag bit above
+      const bool spare = rank_lim < (1ull << rbits) || local_lim < (1ull << lbits);
+      const int kbits = rbits + lbits + (spare ? 0 : 1);
+      const u64 last = spare ? (1ull << (rbits + lbits)) - 1 : 1ull << (rbits + lbits);
       u32* nfd = tot + 2;
       auto key_of = [=] EXS_HD (const Inst& I) -> u64 {
-        if (!(I.flags & IF_BODY)) return 1ull << (rbits + lbits);
+        if (!(I.flags & IF_BODY)) return last;
         const u64 rank = (I.ckey >> CK_RANK_SHIFT) & CK_FIELD_MAX, local = I.ckey & CK_FIELD_MAX;
         return (rank << lbits) | local;
       };

@@ -20,13 +20,15 @@
 
 namespace exs {
 
-struct DepthOp {  // segmented sum of (depth delta) with reset flag in bit 40
-  EXS_HD i64 operator()(i64 a, i64 b) const {
-    if (b & (1ll << 40)) return b;
-    i64 v = (a & 0xFFFFFFFFll) + (b & 0xFFFFFFFFll);
-    return (a & (1ll << 40)) | (v & 0xFFFFFFFFll);
+// segmented sum of depth deltas: the depth mod 2^31 in bits 0-30, the segment
+// (view) reset flag in bit 31; depths are only compared with 0 and 1
+struct DepthOp {
+  EXS_HD u32 operator()(u32 a, u32 b) const {
+    if (b & 0x80000000u) return b;
+    return (a & 0x80000000u) | ((a + b) & 0x7FFFFFFFu);
   }
 };
+EXS_HD inline u32 depth_of(u32 x) { return x & 0x7FFFFFFFu; }
 
 struct LexState {
   u32 N = 0, F = 0, W = 0, L = 0, D = 0, T = 0, NS = 0;

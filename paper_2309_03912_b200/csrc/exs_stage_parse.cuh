@@ -211,22 +211,22 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     dfree(s0); dfree(s1); dfree(vcnt); dfree(fvc); dfree(fvb); dfree(split);
   }
   // 3. segmentation: depth scan and item starts (depth over ( ) { })
-  i64* depth_after = nullptr;
+  u32* depth_after = nullptr;
   {
-    i64* el = dalloc<i64>(VT + 1);
-    i64* inc = dalloc<i64>(VT + 1);
+    u32* el = dalloc<u32>(VT + 1);
+    u32* inc = dalloc<u32>(VT + 1);
     const u32* vv = P.vview; const u32* vb = P.vbase;
     const u16* vk = P.vkid;  // 2-byte kind/id per view position (not the 32-byte token)
     par_for(VT, [=] EXS_HD (i64 i) {
       const u16 t = vk[i];
-      i64 d = 0;
+      u32 d = 0;
       if ((t >> 8) == TK_PUNCT) {
         const u8 id = (u8)t;
         if (id == P_LPAREN || id == P_LBRACE) d = 1;
-        else if (id == P_RPAREN || id == P_RBRACE) d = -1;
+        else if (id == P_RPAREN || id == P_RBRACE) d = 0x7FFFFFFFu;  // -1 mod 2^31
       }
       bool head = vb[vv[i]] == (u32)i;
-      el[i] = (d & 0xFFFFFFFFll) | (head ? (1ll << 40) : 0);
+      el[i] = d | (head ? 0x80000000u : 0u);
     }, st);
     prof_mark(st);
     incl_scan(el, inc, VT, DepthOp(), sc, st);
@@ -234,7 +234,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
     u8* endf = (u8*)el;  // reuse as end flags (VT bytes)
     par_for(VT, [=] EXS_HD (i64 i) {
       const u16 t = vk[i];
-      int dep = (int)(u32)(inc[i] & 0xFFFFFFFFll);
+      const u32 dep = depth_of(inc[i]);
       bool e = false;
       if (dep == 0 && (t >> 8) == TK_PUNCT) {
         if ((u8)t == P_SEMI) e = true;
@@ -291,17 +291,17 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   u32* titem = nullptr;             // item of every view position (kept through step 4b)
   {
     const u32* vb = P.vbase; const u16* vk = P.vkid;
-    const u32* is = P.item_start; const u32* iv = P.item_view; const i64* da = depth_after;
+    const u32* is = P.item_start; const u32* iv = P.item_view; const u32* da = depth_after;
     par_for(I, [=] EXS_HD (i64 j) {
       u32 v = iv[j];
       u32 next = (j + 1 < I && iv[j + 1] == v) ? is[j + 1] : vb[v + 1];
       ibody[j] = NONE;
       if (next - is[j] < BIG) return;
       // last token must be the body's '}' returning to depth 0
-      if (!(vk[next - 1] == (u16)((TK_PUNCT << 8) | P_RBRACE) && (u32)(da[next - 1] & 0xFFFFFFFFll) == 0)) return;
+      if (!(vk[next - 1] == (u16)((TK_PUNCT << 8) | P_RBRACE) && depth_of(da[next - 1]) == 0)) return;
       for (u32 i = is[j]; i < next; i++) {
         const u16 t = vk[i];
-        int dep_before = i == vb[v] ? 0 : (int)(u32)(da[i - 1] & 0xFFFFFFFFll);
+        const u32 dep_before = i == vb[v] ? 0 : depth_of(da[i - 1]);
         if (dep_before != 0) continue;
         const u8 kind = (u8)(t >> 8), id = (u8)t;
         if (kind == TK_IDENT && (id == W_STRUCT || id == W_CLASS || id == W_ENUM || id == W_STATIC_ASSERT)) return;
@@ -327,7 +327,7 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
       if (i >= next - 1) return false;  // the closing '}'
       if (i == bo + 1) return true;
       const u16 pt = vk[i - 1];
-      if ((u32)(da[i - 1] & 0xFFFFFFFFll) != 1 || (pt >> 8) != TK_PUNCT) return false;
+      if (depth_of(da[i - 1]) != 1 || (pt >> 8) != TK_PUNCT) return false;
       if ((u8)pt == P_SEMI) return true;
       if ((u8)pt == P_RBRACE) {
         // a block ends a statement unless 'else' or an operator follows (a

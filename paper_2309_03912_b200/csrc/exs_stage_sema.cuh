@@ -48,10 +48,11 @@ struct HashPrinter {
   int depth;
   EXS_HD void s(const char* t) { while (*t) h = fnv_step(h, (u8)*t++); }
   EXS_HD void c(u8 ch) { h = fnv_step(h, ch); }
+  // a name or string token: its NameHash stands for its text (one load, not
+  // a byte loop over the source with the splice bitmap)
   EXS_HD void tok_text(u32 t) {
-    const Tok& k = toks[t];
-    for (u32 p = k.pos; p < k.end; p++)
-      if (!((splice[p >> 5] >> (p & 31)) & 1u)) h = fnv_step(h, src[p]);
+    const u64 v = toks[t].hv;
+    h = nh_mix(nh_mix(h, (u32)v), (u32)(v >> 32));
   }
   EXS_HD void u64dec(u64 v) {
     char b[24]; int n = 0;

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(128, EXS_WALK_MINB) k_for_walk(F f, i64 n) {
 // the recursive parser: its per-thread state lives in local memory, so the
 // resident thread count sets the L1/L2 footprint of that state
 #ifndef EXS_PARSE_MINB
-#define EXS_PARSE_MINB 8  // measured on C2 1 GB: 8 beats 16 (-8% parse), 4, 2
+#define EXS_PARSE_MINB 6  // C2 1 GB: parse_items 6.3 ms at 6 (80 registers), 6.8 at 8; 8 beat 16, 4, 2
 #endif
 template <class F>
 __global__ void __launch_bounds__(128, EXS_PARSE_MINB) k_for_parse(F f, i64 n) {

@@ -215,6 +215,8 @@ int exs_get_walk_stats(exs_handle h, exs_walk_stats* out, uint64_t cap);
 int exs_describe(exs_handle h, const uint32_t* ids, const uint8_t* kinds, uint32_t n,
                  exs_desc* out);
 /* options: 1 = also compute per-walk demand counts (Analysis.walks parity);
+ * 2 = device timing of later runs (exs_profile_text): 1 the named launches
+ *     (CUDA events around each), 2 every launch and the timeline marks, 0 off;
  * 3 = statement-parallel body parsing threshold (tokens, >= 4);
  * 4 = ordered selections of at least this many indices use a flag pass +
  *     flagged compaction (default 4M; 0 forces it, for the parity tests);
@@ -226,7 +228,8 @@ int exs_describe(exs_handle h, const uint32_t* ids, const uint8_t* kinds, uint32
  * 9 = exs_run_units pipelines: 2 (default) analyses every other batch on a
  *     second stream concurrently, 1 runs the batches one after the other */
 int exs_set_option(exs_handle h, int key, int value);
-/* with EXS_PROFILE=1 in the environment: per-launch-site device times of the last run */
+/* with option 2 (or EXS_PROFILE=1 in the environment: level 2): per-launch-site
+ * device times of the last run, one "site ms xcount" line each */
 const char* exs_profile_text(void);
 /* per-stage device time of the last run (ms): lex, parse, sema, walk */
 int exs_stage_times(exs_handle h, float* out4);

@@ -148,8 +148,9 @@ extern int g_sm_count;
 extern thread_local u64 g_launches;  // per host thread (pipelines run on several)
 // optional per-launch device timing (EXS_PROFILE=1): (site, start, stop) events
 struct ProfRec { const char* fn; int line; cudaEvent_t a, b; };
-extern bool g_profile;
+extern int g_profile;  // 0 off, 1 named launches (EXS_TAG), 2 every launch and timeline mark
 extern std::vector<ProfRec> g_prof;
+cudaEvent_t prof_event();  // from a reused pool (no create/destroy per launch)
 extern thread_local const char* g_tag;  // name of the next launch (EXS_TAG)
 // select_idx switches to a flag pass + DeviceSelect::Flagged at this many indices
 // (set per run from the handle: exs_set_option key 4)
@@ -176,15 +177,16 @@ void par_for(i64 n, F f, cudaStream_t s, int block = 256, const char* fn = __bui
   int grid = (int)(want < cap ? want : cap);
   ProfRec pr{g_tag ? g_tag : fn, g_tag ? 0 : line, nullptr, nullptr};
   g_tag = nullptr;
-  if (g_profile) {
-    cudaEventCreate(&pr.a); cudaEventCreate(&pr.b);
+  const bool timed = g_profile > 1 || (g_profile && pr.line == 0);
+  if (timed) {
+    pr.a = prof_event(); pr.b = prof_event();
     cudaEventRecord(pr.a, s);
   }
   if (pr.line == 0) nvtxRangePushA(pr.fn);
   k_for<<<grid, block, 0, s>>>(f, n);
   if (pr.line == 0) nvtxRangePop();
   CK(cudaGetLastError());
-  if (g_profile) { cudaEventRecord(pr.b, s); g_prof.push_back(pr); }
+  if (timed) { cudaEventRecord(pr.b, s); g_prof.push_back(pr); }
   g_launches++;
 #else
   (void)fn; (void)line;
@@ -204,8 +206,9 @@ void par_for_walk(i64 n, F f, cudaStream_t s, const char* fn = __builtin_FUNCTIO
   int grid = (int)(want < cap ? want : cap);
   ProfRec pr{g_tag ? g_tag : fn, g_tag ? 0 : line, nullptr, nullptr};
   g_tag = nullptr;
-  if (g_profile) {
-    cudaEventCreate(&pr.a); cudaEventCreate(&pr.b);
+  const bool timed = g_profile > 1 || (g_profile && pr.line == 0);
+  if (timed) {
+    pr.a = prof_event(); pr.b = prof_event();
     cudaEventRecord(pr.a, s);
   }
   if (pr.line == 0) nvtxRangePushA(pr.fn);  // named launches are NVTX ranges (ncu --nvtx-include)
@@ -219,7 +222,7 @@ void par_for_walk(i64 n, F f, cudaStream_t s, const char* fn = __builtin_FUNCTIO
   k_for_walk<<<grid, 128, 0, s>>>(f, n);
   if (pr.line == 0) nvtxRangePop();
   CK(cudaGetLastError());
-  if (g_profile) { cudaEventRecord(pr.b, s); g_prof.push_back(pr); }
+  if (timed) { cudaEventRecord(pr.b, s); g_prof.push_back(pr); }
   g_launches++;
 #else
   (void)s; (void)fn; (void)line;
@@ -237,15 +240,16 @@ void par_for_parse(i64 n, F f, cudaStream_t s, const char* fn = __builtin_FUNCTI
   int grid = (int)(want < cap ? want : cap);
   ProfRec pr{g_tag ? g_tag : fn, g_tag ? 0 : line, nullptr, nullptr};
   g_tag = nullptr;
-  if (g_profile) {
-    cudaEventCreate(&pr.a); cudaEventCreate(&pr.b);
+  const bool timed = g_profile > 1 || (g_profile && pr.line == 0);
+  if (timed) {
+    pr.a = prof_event(); pr.b = prof_event();
     cudaEventRecord(pr.a, s);
   }
   if (pr.line == 0) nvtxRangePushA(pr.fn);
   k_for_parse<<<grid, 128, 0, s>>>(f, n);
   if (pr.line == 0) nvtxRangePop();
   CK(cudaGetLastError());
-  if (g_profile) { cudaEventRecord(pr.b, s); g_prof.push_back(pr); }
+  if (timed) { cudaEventRecord(pr.b, s); g_prof.push_back(pr); }
   g_launches++;
 #else
   (void)s; (void)fn; (void)line;
@@ -257,9 +261,9 @@ void par_for_parse(i64 n, F f, cudaStream_t s, const char* fn = __builtin_FUNCTI
 // marks includes host-side gaps (allocation, synchronisation, launch latency)
 inline void prof_mark(cudaStream_t s, const char* fn = __builtin_FUNCTION(), int line = __builtin_LINE()) {
 #ifndef EXS_EMU
-  if (!g_profile) return;
+  if (g_profile < 2) return;
   ProfRec pr{fn, -line, nullptr, nullptr};
-  cudaEventCreate(&pr.a);
+  pr.a = prof_event();
   cudaEventRecord(pr.a, s);
   g_prof.push_back(pr);
 #else

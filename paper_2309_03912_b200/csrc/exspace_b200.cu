@@ -19,7 +19,7 @@ namespace exs {
 int g_sm_count = 148;
 thread_local u64 g_launches = 0;
 thread_local cudaStream_t g_alloc_stream = 0;
-bool g_profile = getenv("EXS_PROFILE") != nullptr;
+int g_profile = getenv("EXS_PROFILE") != nullptr ? 2 : 0;
 std::vector<ProfRec> g_prof;
 thread_local const char* g_tag = nullptr;
 thread_local i64 g_select_flagged_min = EXS_SELECT_FLAGGED_MIN;
@@ -127,6 +127,17 @@ static void cache_release(cudaStream_t s) {
   }
 }
 
+static std::vector<cudaEvent_t> g_prof_pool;
+static size_t g_prof_used = 0;
+cudaEvent_t prof_event() {
+  if (g_prof_used == g_prof_pool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    g_prof_pool.push_back(e);
+  }
+  return g_prof_pool[g_prof_used++];
+}
+
 // fold the recorded launch events into "site ms count" lines
 static void collect_profile() {
   if (!g_profile) return;
@@ -141,13 +152,10 @@ static void collect_profile() {
       if (last_mark) cudaEventElapsedTime(&ms, last_mark, p.a);
       k = "[" + last_name + " .. " + std::to_string(-p.line) + "]";
       last_name = std::string(p.fn) + ":" + std::to_string(-p.line);
-      if (last_mark) cudaEventDestroy(last_mark);
       last_mark = p.a;
       if (k == "[ .. " + std::to_string(-p.line) + "]") continue;
     } else {
       cudaEventElapsedTime(&ms, p.a, p.b);
-      cudaEventDestroy(p.a);
-      cudaEventDestroy(p.b);
       k = p.line ? std::string(p.fn) + ":" + std::to_string(p.line) : std::string(p.fn);
     }
     bool found = false;
@@ -156,6 +164,7 @@ static void collect_profile() {
     if (!found) acc.push_back({k, {ms, 1}});
   }
   g_prof.clear();
+  g_prof_used = 0;  // the pool's events are recorded again by the next run
   g_prof_text.clear();
   for (auto& e : acc) {
     char b[256];
@@ -1399,7 +1408,7 @@ int exs_set_option(exs_handle x, int key, int value) {
   API_TRY
   if (key == 1) x->h.want_demands = value != 0;
 #ifndef EXS_EMU
-  else if (key == 2) g_profile = value != 0;  // per-launch device timing of later runs
+  else if (key == 2) g_profile = value <= 0 ? 0 : (value >= 2 ? 2 : 1);  // device timing of later runs: 1 named launches, 2 all
 #endif
   else if (key == 3) x->h.split_min = value < 4 ? 4u : (u32)value;  // statement-split threshold (tokens)
   else if (key == 4) x->h.select_flagged_min = value < 0 ? 0 : value;  // flag-pass selection threshold

@@ -74,7 +74,7 @@ struct Tok {
   u32 pos;    // raw byte offset of the token text (pragma: of its NAME word)
   u32 end;    // raw end (exclusive); may include spliced bytes
   u32 line, col;  // reference SrcLoc (1-based, code points)
-  u64 hv;     // ident/string/pragma: FNV-1a of logical text; int: value
+  u64 hv;     // ident/string/pragma: NameHash of the logical text; int: value
   u8 kind, id, mask, flags;  // mask: bit0 host pass, bit1 device pass
   u32 file;
 };

@@ -42,8 +42,6 @@ inline MapEnt* alloc_map(u32 mask, cudaStream_t st) {
 struct HashPrinter {
   const Node* nodes;
   const Tok* toks;
-  const u8* src;
-  const u32* splice;
   u64 h;
   int depth;
   EXS_HD void s(const char* t) { while (*t) h = fnv_step(h, (u8)*t++); }
@@ -115,9 +113,8 @@ struct HashPrinter {
 };
 
 // signature_key hash (sema.py:144-149) with the spaces string under P2 (133-141)
-EXS_HD inline u64 sig_hash(const Node* nodes, const Tok* toks, const u8* src, const u32* sp,
-                           u32 fn_node, u32 owner_name_tok, bool p2) {
-  HashPrinter hp{nodes, toks, src, sp, fnv_init(), 0};
+EXS_HD inline u64 sig_hash(const Node* nodes, const Tok* toks, u32 fn_node, u32 owner_name_tok, bool p2) {
+  HashPrinter hp{nodes, toks, fnv_init(), 0};
   const Node& f = nodes[fn_node];
   const Node& x = nodes[fn_node + 1];
   if (owner_name_tok != NONE) hp.tok_text(owner_name_tok);
@@ -304,7 +301,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
   // 3. owner flags, signature hashes
   {
     FnRec* fr = S.fns; const RecRec* rr = S.recs; const Node* nd = P.nodes; const Tok* tk = L.toks;
-    const u8* s = L.src; const u32* sp = L.splice; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
+    const u32* vf = P.vfile; const u8* cfgs = L.cfg;
     EXS_TAG("sema_sig_hash");
     par_for(NF, [=] EXS_HD (i64 i) {
       FnRec& r = fr[i];
@@ -312,7 +309,7 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
       if (r.rec != NONE && !rr[r.rec].dup) { r.flags |= FR_OWNER; owner_tok = nd[rr[r.rec].node].tok; }
       if (tk[nd[r.node].tok].id == W_MAIN && !(r.flags & FR_OWNER)) r.flags |= FR_MAIN;
       bool p2 = (cfgs[vf[r.view]] & CFG_MODE_MASK) == MODE_P2;
-      r.sig = sig_hash(nd, tk, s, sp, r.node, owner_tok, p2);
+      r.sig = sig_hash(nd, tk, r.node, owner_tok, p2);
     }, st);
   }
   // 4. duplicates among free functions and members of kept structs (sema.py:161-195)

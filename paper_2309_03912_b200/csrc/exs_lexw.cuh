@@ -211,6 +211,36 @@ EXS_HD inline u32 chunk_at(const LexW& X, const u32 r[8], u32 base, u32 q) {
   return sh ? (lo >> sh) | (hi << (32 - sh)) : lo;
 #endif
 }
+// SWAR byte classes of a little-endian word: 0x80 in every byte that is an
+// ASCII digit / identifier character (bytes >= 0x80 never match)
+EXS_HD inline u32 swar_range(u32 x, u32 lo, u32 hi) {  // lo <= b <= hi, for b < 0x80
+  const u32 ge = ((x | 0x80808080u) - lo * 0x01010101u) & 0x80808080u;
+  const u32 le = ((0x80u + hi) * 0x01010101u - (x & 0x7F7F7F7Fu)) & 0x80808080u;
+  return ge & le;
+}
+EXS_HD inline u32 swar_digit(u32 x) { return swar_range(x, 0x30, 0x39) & ~x; }
+EXS_HD inline u32 swar_ident(u32 x) {
+  const u32 t = x ^ 0x5F5F5F5Fu;  // '_'
+  const u32 us = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u;
+  return (swar_range(x, 0x30, 0x39) | swar_range(x | 0x20202020u, 0x61, 0x7A) | us) & ~x;
+}
+// end of the digit / identifier run continuing at q (a word boundary, so
+// 4-aligned) before the file end: four bytes per step
+EXS_HD inline u32 run_end(const LexW& X, u32 q, u32 fend, bool num) {
+  if (X.vec) {
+    const u32* s32 = reinterpret_cast<const u32*>(X.src);
+    while (q < fend) {
+      const u32 x = s32[q >> 2];
+      const u32 miss = ~(num ? swar_digit(x) : swar_ident(x)) & 0x80808080u;
+      if (miss) { q += ffs32(miss) >> 3; break; }
+      q += 4;
+    }
+    return q < fend ? q : fend;
+  }
+  while (q < fend && (num ? is_digit(X.src[q]) : is_ident_char(X.src[q]))) q++;
+  return q;
+}
+
 // NameHash of the bytes [lo, hi), four at a step
 EXS_HD inline u64 name_hash_range(const LexW& X, const u32 r[8], u32 base, u32 lo, u32 hi) {
   u64 h = 1469598103934665603ull;
@@ -625,8 +655,7 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
       if (stop) {
         end = base + ffs32(stop);
       } else {
-        end = base + 32;
-        while (end < fend && (num ? is_digit(X.src[end]) : is_ident_char(X.src[end]))) end++;
+        end = run_end(X, base + 32, fend, num);
       }
       t.end = end;
       if (num) {

@@ -547,7 +547,7 @@ def main():
     ap.add_argument("--files", type=int, default=10_000)
     ap.add_argument("--file-bytes", type=int, default=100_000)
     ap.add_argument("--batch-mib", type=int, default=256)
-    ap.add_argument("--pipelines", type=int, default=2, help="concurrent batch pipelines on the GPU (1 or 2)")
+    ap.add_argument("--pipelines", type=int, default=2, help="concurrent batch pipelines on the GPU (1-4)")
     ap.add_argument("--c3-structs", type=int, default=10_300)
     ap.add_argument("--c4-funcs", type=int, default=10_000_000)
     ap.add_argument("--c5-gb", type=float, default=8.0)

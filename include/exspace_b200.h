@@ -225,8 +225,9 @@ int exs_describe(exs_handle h, const uint32_t* ids, const uint8_t* kinds, uint32
  * 6 = nonzero: also keep the raw records (exs_get_diags / exs_diags_view);
  * 7 = exs_run_units batch capacity in MiB (default 1024, at most 2047);
  * 8 = host threads packing a batch into page-locked memory (0 = automatic);
- * 9 = exs_run_units pipelines: 2 (default) analyses every other batch on a
- *     second stream concurrently, 1 runs the batches one after the other */
+ * 9 = exs_run_units pipelines, 1-4: P > 1 analyses P batches concurrently, each
+ *     on its own stream with its own buffers (default 2); 1 runs the batches one
+ *     after the other */
 int exs_set_option(exs_handle h, int key, int value);
 /* with option 2 (or EXS_PROFILE=1 in the environment: level 2): per-launch-site
  * device times of the last run, one "site ms xcount" line each */

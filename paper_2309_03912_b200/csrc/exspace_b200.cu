@@ -273,9 +273,9 @@ struct Handle {
     bool abort = false;  // a pipeline failed: the others stop waiting
   } turn;
   // streaming driver (exs_run_units): two host staging slots, two device slots;
-  // with pipelines = 2, a second handle (own stream, own buffers) analyses
-  // every other batch concurrently on the same device
-  std::unique_ptr<Handle> peer;
+  // with pipelines = P > 1, P - 1 more handles (own stream, own buffers)
+  // analyse batches concurrently on the same device
+  std::vector<std::unique_ptr<Handle>> peers;
   int pipelines = 2;
   u64 batch_cap = 1ull << 30;
   int pack_threads = 0;             // 0: hardware threads (<= 16)
@@ -1099,22 +1099,24 @@ static void add_stats(exs_stats& acc, const exs_stats& s) {
 }
 
 #ifndef EXS_EMU
-// Two pipelines on one device: this handle takes the even batches, a peer
-// handle (own stream, own device buffers) the odd ones, each in its own host
-// thread: pack -> copy -> analyse.  The device runs one pipeline's kernels in
+// P pipelines on one device: this handle and P - 1 peer handles (own stream,
+// own device buffers), each in its own host thread: pack -> copy -> analyse.  The device runs one pipeline's kernels in
 // the other's host round trips and low-occupancy phases (sorts, scans, small
 // grids); results are appended in batch order (Handle::turn).
 static void run_units_pipelined(Handle& H, const char* const* texts, const uint64_t* lens, u64 n_units,
                                 const u8* cfg, const std::vector<BatchPlan>& plan, u64 maxb) {
-  if (!H.peer) {
-    H.peer.reset(new Handle());
-    Handle& Q = *H.peer;
+  const int np = std::max(2, H.pipelines);
+  while ((int)H.peers.size() < np - 1) {
+    H.peers.emplace_back(new Handle());
+    Handle& Q = *H.peers.back();
     Q.device = H.device;
     CK(cudaStreamCreateWithFlags(&Q.st, cudaStreamNonBlocking));
   }
-  Handle& Q = *H.peer;
-  Q.want_demands = H.want_demands; Q.split_min = H.split_min; Q.select_flagged_min = H.select_flagged_min;
-  Q.diag_sort_two_pass = H.diag_sort_two_pass; Q.keep_records = false;
+  for (int q = 0; q < np - 1; q++) {
+    Handle& Q = *H.peers[q];
+    Q.want_demands = H.want_demands; Q.split_min = H.split_min; Q.select_flagged_min = H.select_flagged_min;
+    Q.diag_sort_two_pass = H.diag_sort_two_pass; Q.keep_records = false;
+  }
   const int nthreads = H.pack_threads > 0 ? H.pack_threads
                                           : (int)std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency() / 2));
   results_reset(H, n_units);
@@ -1189,16 +1191,21 @@ static void run_units_pipelined(Handle& H, const char* const* texts, const uint6
       H.turn.cv.notify_all();
     }
   };
-  std::string e0, e1;
-  std::thread second([&]() { worker(Q, 1, e1); });
-  worker(H, 0, e0);
-  second.join();
+  std::vector<std::string> errs(np);
+  std::vector<std::thread> others;
+  for (int q = 1; q < np; q++) others.emplace_back([&, q]() { worker(*H.peers[q - 1], q, errs[q]); });
+  worker(H, 0, errs[0]);
+  for (auto& t : others) t.join();
   bind_stream(H);
-  H.peer->sink = H.peer.get();
+  for (int q = 0; q < np - 1; q++) H.peers[q]->sink = H.peers[q].get();
   H.sink = &H;
   H.turn.on = false;
-  const char* aborted = "another pipeline failed";
-  if (!e0.empty() || !e1.empty()) throw Err(!e0.empty() && e0 != aborted ? e0 : (!e1.empty() ? e1 : e0));
+  // the first real error (a pipeline that saw another fail reports that)
+  const std::string aborted = "another pipeline failed";
+  std::string err;
+  for (auto& e : errs)
+    if (!e.empty() && (err.empty() || err == aborted)) err = e;
+  if (!err.empty()) throw Err(err);
   results_close(H);
   acc.batches = plan.size();
   acc.ms_wall = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1416,7 +1423,7 @@ int exs_set_option(exs_handle x, int key, int value) {
   else if (key == 6) x->h.keep_records = value != 0;        // keep raw records (exs_get_diags)
   else if (key == 7) x->h.batch_cap = (u64)std::min(2047, std::max(1, value)) << 20;  // batch MiB
   else if (key == 8) x->h.pack_threads = value;               // host packing threads (0 = auto)
-  else if (key == 9) x->h.pipelines = value < 2 ? 1 : 2;      // concurrent batch pipelines
+  else if (key == 9) x->h.pipelines = value < 2 ? 1 : (value > 4 ? 4 : value);  // concurrent batch pipelines
   else throw Err("unknown option");
   API_END
 }

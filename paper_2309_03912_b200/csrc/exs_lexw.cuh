@@ -287,6 +287,87 @@ EXS_HD inline bool is_single(u8 c) {
   return c == '{' || c == '}' || c == '(' || c == ')' || c == ',' || c == ';' || c == '.';
 }
 
+// Byte classes of a whole word, eight at a time: a 256-entry table gives each
+// byte its class bits, eight class bytes are packed into 64 bits and one 8x8
+// bit transpose turns them into eight 8-bit position masks (one per class).
+// About 10 ALU operations per byte for eight classes, where a compare chain per
+// byte and class took ~45 (the masks phase was ALU-bound).
+enum : u32 {  // kTokClass bits (lex_count / lex_emit)
+  TC_ID = 1, TC_DG = 2, TC_WS = 4, TC_PS = 8, TC_SG = 16, TC_QT = 32, TC_SL = 64, TC_ST = 128
+};
+enum : u32 {  // kLineClass bits (lex_words / mark_special)
+  LC_QT = 1, LC_SL = 2, LC_ST = 4, LC_NL = 8, LC_HS = 16, LC_HI = 32
+};
+struct ClassTable { u8 c[256]; };
+constexpr ClassTable make_tok_class() {
+  ClassTable t{};
+  for (u32 c = 0; c < 256; c++) {
+    u32 v = 0;
+    const bool dg = c >= '0' && c <= '9';
+    const bool al = (c >= 'a' && c <= 'z') || (c >= 'A' && c <= 'Z');
+    if (al || dg || c == '_') v |= TC_ID;
+    if (dg) v |= TC_DG;
+    if (c == ' ' || c == '\t' || c == '\r') v |= TC_WS;
+    if (c == '<' || c == '>' || c == ':' || c == '=' || c == '!' || c == '&' || c == '|' || c == '+') v |= TC_PS;
+    if (c == '{' || c == '}' || c == '(' || c == ')' || c == ',' || c == ';' || c == '.') v |= TC_SG;
+    if (c == '"') v |= TC_QT;
+    if (c == '/') v |= TC_SL;
+    if (c == '*') v |= TC_ST;
+    t.c[c] = (u8)v;
+  }
+  return t;
+}
+constexpr ClassTable make_line_class() {
+  ClassTable t{};
+  for (u32 c = 0; c < 256; c++) {
+    u32 v = 0;
+    if (c == '"') v |= LC_QT;
+    if (c == '/') v |= LC_SL;
+    if (c == '*') v |= LC_ST;
+    if (c == '\n') v |= LC_NL;
+    if (c == '#') v |= LC_HS;
+    if (c >= 0x80) v |= LC_HI;
+    t.c[c] = (u8)v;
+  }
+  return t;
+}
+#ifndef EXS_EMU
+__device__ const ClassTable kTokClassDev = make_tok_class();
+__device__ const ClassTable kLineClassDev = make_line_class();
+#endif
+static constexpr ClassTable kTokClassHost = make_tok_class();
+static constexpr ClassTable kLineClassHost = make_line_class();
+
+// 8x8 bit transpose: bit i of byte k of the result = bit k of byte i of x
+EXS_HD inline u64 transpose8(u64 x) {
+  u64 t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull; x ^= t ^ (t << 7);
+  t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull; x ^= t ^ (t << 14);
+  t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull; x ^= t ^ (t << 28);
+  return x;
+}
+// per-class 32-bit position masks of the word r: m[k] bit j = class bit k of byte j
+template <bool TOK>
+EXS_HD inline void word_classes(const u32 r[8], u32 m[8]) {
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  const u8* tab = TOK ? kTokClassDev.c : kLineClassDev.c;
+#else
+  const u8* tab = TOK ? kTokClassHost.c : kLineClassHost.c;
+#endif
+#pragma unroll
+  for (u32 k = 0; k < 8; k++) m[k] = 0;
+#pragma unroll
+  for (u32 g = 0; g < 4; g++) {
+    const u32 a = r[2 * g], b = r[2 * g + 1];
+    const u32 lo = (u32)tab[a & 0xFFu] | ((u32)tab[(a >> 8) & 0xFFu] << 8) | ((u32)tab[(a >> 16) & 0xFFu] << 16) |
+                   ((u32)tab[a >> 24] << 24);
+    const u32 hi = (u32)tab[b & 0xFFu] | ((u32)tab[(b >> 8) & 0xFFu] << 8) | ((u32)tab[(b >> 16) & 0xFFu] << 16) |
+                   ((u32)tab[b >> 24] << 24);
+    const u64 x = transpose8(((u64)hi << 32) | lo);
+#pragma unroll
+    for (u32 k = 0; k < 8; k++) m[k] |= (u32)((x >> (8 * k)) & 0xFFu) << (8 * g);
+  }
+}
+
 // The comment DFA over one word from state st, event-driven: between the
 // bytes where the current state can change -- '"' or '/' in code, '"' or '\n'
 // in a string, '\n' in a line comment, '*' in a block comment, any byte after
@@ -344,20 +425,11 @@ EXS_HD inline WScan word_info(const LexW& X, u32 w, u8& special, u32& nhash) {
   const bool prev_nl = base > 0 && X.src[base - 1] == '\n' && !bit_get(X.sp, base - 1);
   const u32 m = X.n - base < 32 ? X.n - base : 32;
   const u32 valid = m == 32 ? ~0u : ((1u << m) - 1);
-  // byte masks (branch-uniform, unrolled)
-  u32 Q = 0, SL = 0, ST = 0, NL = 0, HS = 0, HI = 0;
-#pragma unroll
-  for (u32 j = 0; j < 32; j++) {
-    const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
-    const u32 b = 1u << j;
-    if (c == '"') Q |= b;
-    if (c == '/') SL |= b;
-    if (c == '*') ST |= b;
-    if (c == '\n') NL |= b;
-    if (c == '#') HS |= b;
-    if (c >= 0x80) HI |= b;
-  }
-  Q &= valid; SL &= valid; ST &= valid; NL &= valid; HS &= valid; HI &= valid;
+  // byte masks (table + bit transpose)
+  u32 cm[8];
+  word_classes<false>(r, cm);
+  const u32 Q = cm[0] & valid, SL = cm[1] & valid, ST = cm[2] & valid, NL = cm[3] & valid,
+            HS = cm[4] & valid, HI = cm[5] & valid;
   // logical line starts: file starts and bytes after a non-spliced newline
   const u32 ls = (fsw | ((NL & ~spw) << 1) | (prev_nl ? 1u : 0u)) & valid;
   if (ls) o.lsp = base + hib32(ls);
@@ -387,13 +459,9 @@ EXS_HD inline void mark_special(const LexW& X, u32 w) {
   const u32 valid = m == 32 ? ~0u : ((1u << m) - 1);
   u32 r[8];
   load_word(X, base, r);
-  u32 NL = 0, SPC = 0;
-#pragma unroll
-  for (u32 j = 0; j < 32; j++) {
-    const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
-    if (c == '\n') NL |= 1u << j;
-    if (c >= 0x80 || c == '#') SPC |= 1u << j;
-  }
+  u32 cm[8];
+  word_classes<false>(r, cm);
+  const u32 NL = cm[3], SPC = cm[4] | cm[5];
   const u32 ls = (fsw | ((NL & ~spw) << 1) | (prev_nl ? 1u : 0u)) & valid;
   u32 spc = (SPC | spw) & valid;
   while (spc) {  // the first special byte of each logical line
@@ -456,21 +524,12 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
   // comment-DFA states before every byte, event-driven (dfa_word)
   u32 bl = 0;
   sm = 0; sbb = 0; nl = 0; qt = 0;
-  u32 id = 0, dg = 0, ws = 0, ps = 0, sg = 0, sl = 0, star = 0;
+  u32 cm[8];
+  word_classes<true>(r, cm);
+  const u32 id = cm[0], dg = cm[1], ws = cm[2], ps = cm[3], sg = cm[4], sl = cm[6], star = cm[7];
+  qt = cm[5];
 #pragma unroll
-  for (u32 j = 0; j < 32; j++) {
-    const u8 c = (u8)(r[j >> 2] >> (8 * (j & 3)));
-    const u32 b = 1u << j;
-    if (c == '\n') nl |= b;
-    if (is_ident_char(c)) id |= b;
-    if (is_digit(c)) dg |= b;
-    if (c == ' ' || c == '\t' || c == '\r') ws |= b;
-    if (is_pset(c)) ps |= b;
-    if (is_single(c)) sg |= b;
-    if (c == '"') qt |= b;
-    if (c == '/') sl |= b;
-    if (c == '*') star |= b;
-  }
+  for (u32 k = 0; k < 8; k++) nl |= byte_eq_mask(r[k], '\n') << (4 * k);
   lsb = fsw | ((nl & ~spw) << 1) | (prev_nl ? 1u : 0u);
   dfa_word<true>(st, r, qt, sl, star, nl, spw, fsw, ~0u, bl, sm, sbb);
   lsb &= valid; nl &= valid;

@@ -188,29 +188,6 @@ struct ByteCursor {
   }
 };
 
-// bytes [q, q + 4) as a little-endian word: from the registers inside the
-// word at `base`, else two aligned loads (the batch ends in 64 zero bytes)
-EXS_HD inline u32 chunk_at(const LexW& X, const u32 r[8], u32 base, u32 q) {
-  const u32 o = q - base, sh = 8 * (q & 3);
-  u32 lo, hi;
-  if (o + 4 <= 32) {
-    lo = word_of(r, o >> 2);
-    hi = (o >> 2) < 7 ? word_of(r, (o >> 2) + 1) : 0u;
-  } else if (X.vec) {
-    const u32* s32 = reinterpret_cast<const u32*>(X.src);
-    lo = s32[q >> 2];
-    hi = s32[(q >> 2) + 1];
-  } else {
-    u32 x = 0;
-    for (u32 k = 0; k < 4; k++) x |= (u32)X.src[q + k] << (8 * k);
-    return x;
-  }
-#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
-  return __funnelshift_r(lo, hi, sh);
-#else
-  return sh ? (lo >> sh) | (hi << (32 - sh)) : lo;
-#endif
-}
 // SWAR byte classes of a little-endian word: 0x80 in every byte that is an
 // ASCII digit / identifier character (bytes >= 0x80 never match)
 EXS_HD inline u32 swar_range(u32 x, u32 lo, u32 hi) {  // lo <= b <= hi, for b < 0x80
@@ -242,12 +219,31 @@ EXS_HD inline u32 run_end(const LexW& X, u32 q, u32 fend, bool num) {
 }
 
 // NameHash of the bytes [lo, hi), four at a step
+// aligned source word a (absolute word index): registers inside the word at
+// `base`, else global memory (the batch ends in 64 zero bytes)
+EXS_HD inline u32 word_at(const LexW& X, const u32 r[8], u32 base, u32 a) {
+  const u32 k = a - (base >> 2);
+  if (k < 8) return word_of(r, k);
+  if (X.vec) return reinterpret_cast<const u32*>(X.src)[a];
+  u32 x = 0;
+  for (u32 i = 0; i < 4; i++) x |= (u32)X.src[4 * a + i] << (8 * i);
+  return x;
+}
 EXS_HD inline u64 name_hash_range(const LexW& X, const u32 r[8], u32 base, u32 lo, u32 hi) {
   u64 h = 1469598103934665603ull;
+  const u32 sh = 8 * (lo & 3);
+  u32 a = lo >> 2;
+  u32 w0 = word_at(X, r, base, a);
   for (u32 q = lo; q < hi; q += 4) {
-    u32 x = chunk_at(X, r, base, q);
+    const u32 w1 = word_at(X, r, base, ++a);  // one word per chunk: the next chunk's low word
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+    u32 x = __funnelshift_r(w0, w1, sh);
+#else
+    u32 x = sh ? (w0 >> sh) | (w1 << (32 - sh)) : w0;
+#endif
     if (hi - q < 4) x &= (1u << (8 * (hi - q))) - 1;
     h = nh_mix(h, x);
+    w0 = w1;
   }
   return nh_fin(h, hi - lo);
 }

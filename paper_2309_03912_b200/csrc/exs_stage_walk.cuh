@@ -126,6 +126,16 @@ struct RootCand {
   u16 sf;                // specifier bits of the owning struct
   Val ot;
 };
+// what step 2 of the roots needs of a fast candidate, written by step 1 (one
+// coalesced record instead of re-reading the decl, node, token and struct)
+struct RootStash {
+  u64 otx;          // owner type name (ot.x) when rec != NONE
+  u32 walk, at;     // walk, declaration token
+  u32 rec, otrec;   // owner struct record, canonical owner record (ot.rec)
+  u8 sp[2];         // static spaces per side
+  u8 iflags, pad;   // IF_BODY / IF_MAIN
+  u32 pad2;
+};
 
 // build a walker for an existing instance
 EXS_HD inline void walker_for(Walker& w, const WalkCfg& C, const WalkBufs& B, u32 id, u64 rank) {
@@ -431,9 +441,11 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     // and log lowering non-inserters by SLOT; ids come from a scan (no shared
     // counter: at this rate one counter serialises the kernel)
     u32* rslot = dalloc<u32>(2ull * NRC + 1);
+    RootStash* rstash = dalloc<RootStash>((u64)NRC + 1);
     const u32 nlog0 = get1(B.n_log, st);
     {
       u32* rs = rslot;
+      RootStash* rst = rstash;
       EXS_TAG("walk_roots");
       u32* ro = rot;
       par_for_walk(NRC, [=] EXS_HD (i64 kk) {
@@ -444,6 +456,15 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         const FnRec& r = fr[q.i];
         const u16 fl = nd[r.node].n;
         const u8 sides = (fl & FF_G) ? 2 : (static_spaces(fl, q.free_main, q.sf, q.mode, 0) & 3);
+        {
+          RootStash z;
+          z.otx = q.ot.x; z.walk = q.walk; z.at = nd[r.node].tok; z.rec = r.rec; z.otrec = q.ot.rec;
+          z.sp[0] = static_spaces(fl, q.free_main, q.sf, q.mode, 0);
+          z.sp[1] = static_spaces(fl, q.free_main, q.sf, q.mode, 1);
+          z.iflags = (u8)(((r.flags & FR_BODY) ? IF_BODY : 0) | ((r.flags & FR_MAIN) ? IF_MAIN : 0));
+          z.pad = 0; z.pad2 = 0;
+          rst[kk] = z;
+        }
         u32 k = 0;
         for (u8 sd = 0; sd < 2; sd++) {
           if (!((sides >> sd) & 1)) continue;
@@ -477,19 +498,25 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       excl_scan_u32(ins, ids, NS2 + 1, sc, st);
       const u32 total = get1(ids + NS2, st);
       const u32* id_of = ids;
+      const RootStash* rst = rstash;
       par_for(NS2, [=] EXS_HD (i64 j) {
         const u32 slot = rs[j];
         if (slot >= NONE - 1) return;
         const u32 id = id_of[j];
         if (id >= B.cap_inst) { at_or(B.overflow, 1u); return; }
-        const RootCand q = cand(rcc[j >> 1], (u32)(j >> 1), false);
+        const RootStash z = rst[j >> 1];
         const u8 sd = (u8)(j & 1);
-        const FnRec& r = fr[q.i];
-        const Node& fn = nd[r.node];
-        const IKey key = make_ikey(r.sig_rep, vnone(), vnone(), q.ot, q.walk, sd);
-        fill_instance(B.inst[id], tab, key, q.i, vnone(), vnone(), sd, r.rec, q.ot, fn.tok, q.walk,
-                      static_spaces(fn.n, q.free_main, q.sf, q.mode, sd), slot);
-        B.slots[slot].sid = id;
+        Val ot = vnone();
+        if (z.rec != NONE) { ot.k = V_TYPE; ot.x = z.otx; ot.rec = z.otrec; ot.bt = BT_NONE; ot.targ = 0; }
+        Slot& S_ = B.slots[slot];
+        Inst& I = B.inst[id];
+        I.ka = S_.k.a; I.kb = S_.k.b;  // the key step 1 inserted (make_ikey of the decl, owner, walk, side)
+        I.ckey = ~0ull; I.fn = rcc[j >> 1] >> 1; I.orec = z.rec; I.walk = z.walk; I.at = z.at;
+        I.ebase = 0; I.ecnt = 0;
+        I.tb = vnone(); I.hb = vnone(); I.ot = ot;
+        I.side = sd; I.spaces = z.sp[sd]; I.pad = 0; I.slot = slot;
+        I.flags = z.iflags;  // fill_instance's flags, from the decl record
+        S_.sid = id;
       }, st);
       u32* ni = B.n_inst;
       par_for(1, [=] EXS_HD (i64) { *ni = total; }, st);
@@ -546,6 +573,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     sync(st);
     dfree(rcand);
     dfree(rslot);
+    dfree(rstash);
     dfree(rot);
     dfree(vd0);
   }

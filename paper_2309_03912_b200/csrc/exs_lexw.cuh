@@ -151,6 +151,9 @@ EXS_HD inline u32 word_of(const u32 r[8], u32 k) {  // r[k] without local memory
                : (k < 6 ? (k == 4 ? r[4] : r[5]) : (k == 6 ? r[6] : r[7]));
 }
 EXS_HD inline u8 byte_of(const u32 r[8], u32 j) { return (u8)(word_of(r, j >> 2) >> (8 * (j & 3))); }
+// dynamic-index reads of a word mirrored in shared memory (lex_word): one load
+// where the register select chain of word_of takes seven selects
+EXS_HD inline u8 byte_at(const u32* R, u32 j) { return (u8)(R[j >> 2] >> (8 * (j & 3))); }
 EXS_HD inline u32 ffs32(u32 x) {  // index of the lowest set bit (x != 0)
 #if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
   return (u32)__ffs((int)x) - 1;
@@ -181,7 +184,7 @@ struct ByteCursor {
   EXS_HD u8 at(u32 q) {
     if (q < base + 32) {
       const u32 j = q - base;
-      if ((j >> 2) != cur) { cur = j >> 2; wv = word_of(r, cur); }
+      if ((j >> 2) != cur) { cur = j >> 2; wv = r[cur]; }
       return (u8)(wv >> (8 * (j & 3)));
     }
     return src[q];
@@ -221,15 +224,15 @@ EXS_HD inline u32 run_end(const LexW& X, u32 q, u32 fend, bool num) {
 // NameHash of the bytes [lo, hi), four at a step
 // aligned source word a (absolute word index): registers inside the word at
 // `base`, else global memory (the batch ends in 64 zero bytes)
-EXS_HD inline u32 word_at(const LexW& X, const u32 r[8], u32 base, u32 a) {
+EXS_HD inline u32 word_at(const LexW& X, const u32* r, u32 base, u32 a) {
   const u32 k = a - (base >> 2);
-  if (k < 8) return word_of(r, k);
+  if (k < 8) return r[k];
   if (X.vec) return reinterpret_cast<const u32*>(X.src)[a];
   u32 x = 0;
   for (u32 i = 0; i < 4; i++) x |= (u32)X.src[4 * a + i] << (8 * i);
   return x;
 }
-EXS_HD inline u64 name_hash_range(const LexW& X, const u32 r[8], u32 base, u32 lo, u32 hi) {
+EXS_HD inline u64 name_hash_range(const LexW& X, const u32* r, u32 base, u32 lo, u32 hi) {
   u64 h = 1469598103934665603ull;
   const u32 sh = 8 * (lo & 3);
   u32 a = lo >> 2;
@@ -495,6 +498,16 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
   if (base >= X.n) return 0;
   u32 r[8];
   load_word(X, base, r);
+#if defined(__CUDA_ARCH__) && !defined(EXS_EMU)
+  // the word mirrored in this thread's shared-memory row (stride 9 words: no
+  // bank conflicts), for the reads at run-time offsets
+  __shared__ u32 sw_rows[256 * 9];
+  u32* R = sw_rows + threadIdx.x * 9;
+#pragma unroll
+  for (u32 k = 0; k < 8; k++) R[k] = r[k];
+#else
+  const u32* R = r;
+#endif
   const u32 m = X.n - base < 32 ? X.n - base : 32;
   const u32 valid = m == 32 ? ~0u : ((1u << m) - 1);
   const u32 spw = X.sp[w], fsw = X.fs[w] & valid;
@@ -610,12 +623,12 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
       u32 p = ffs32(runs);
       runs &= runs - 1;
       while (p < 32 && ((PSc >> p) & 1u)) {
-        const u8 c = byte_of(r, p);
+        const u8 c = byte_at(R, p);
         u8 c1 = 0, c2 = 0;
-        if (p + 1 < 32) { if (!((fsw >> (p + 1)) & 1u)) c1 = byte_of(r, p + 1); }
+        if (p + 1 < 32) { if (!((fsw >> (p + 1)) & 1u)) c1 = byte_at(R, p + 1); }
         else if (base + p + 1 < fe_last) c1 = X.src[base + p + 1];
         if (c1) {
-          if (p + 2 < 32) { if (!((fsw >> (p + 2)) & 1u)) c2 = byte_of(r, p + 2); }
+          if (p + 2 < 32) { if (!((fsw >> (p + 2)) & 1u)) c2 = byte_at(R, p + 2); }
           else if (base + p + 2 < fe_last) c2 = X.src[base + p + 2];
         }
         u8 pid;
@@ -699,7 +712,7 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
         if ((mask >> p) & 1u) at_min(&X.fp[2 * f + p].lex_pos, i);
     if (!(starts & bj)) continue;
     const u32 tl = 1 + gnl - fnl0, col = i - lsp + 1;
-    const u8 c = byte_of(r, j);
+    const u8 c = byte_at(R, j);
     Tok t;
     t.pos = i; t.line = tl; t.col = col; t.mask = mask; t.flags = 0; t.file = f; t.hv = 0; t.id = 0;
     if (idst & bj) {
@@ -716,7 +729,7 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
       if (num) {
         u64 v = 0;
         bool ovf = false;
-        ByteCursor bc{r, X.src, base, 8u, 0u};
+        ByteCursor bc{R, X.src, base, 8u, 0u};
         for (u32 q = i; q < end; q++) {
           const u64 nv = v * 10 + (bc.at(q) - '0');
           if (v > 1844674407370955161ull || nv < v) ovf = true;
@@ -724,7 +737,7 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
         }
         t.kind = TK_INT; t.hv = v; t.flags = ovf ? TF_INT_OVERFLOW : 0;
       } else {
-        const u64 h = name_hash_range(X, r, base, i, end);
+        const u64 h = name_hash_range(X, R, base, i, end);
         t.kind = TK_IDENT; t.hv = h; t.id = vocab_hash(h, end - i);
       }
     } else if (qs & bj) {
@@ -744,7 +757,7 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
       }
       t.kind = TK_STRING;
       if (term) {
-        const u64 h = name_hash_range(X, r, base, i + 1, close);
+        const u64 h = name_hash_range(X, R, base, i + 1, close);
         const u32 len = close - i - 1;
         t.pos = len ? i + 1 : close; t.end = close; t.hv = h; t.id = vocab_hash(h, len);
       } else {
@@ -755,10 +768,10 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
     } else {
       u8 c1 = 0, c2 = 0;
       if (pst & bj) {
-        if (j + 1 < 32) { if (!((fsw >> (j + 1)) & 1u)) c1 = byte_of(r, j + 1); }
+        if (j + 1 < 32) { if (!((fsw >> (j + 1)) & 1u)) c1 = byte_at(R, j + 1); }
         else if (i + 1 < fend) c1 = X.src[i + 1];
         if (c1) {
-          if (j + 2 < 32) { if (!((fsw >> (j + 2)) & 1u)) c2 = byte_of(r, j + 2); }
+          if (j + 2 < 32) { if (!((fsw >> (j + 2)) & 1u)) c2 = byte_at(R, j + 2); }
           else if (i + 2 < fend) c2 = X.src[i + 2];
         }
       }

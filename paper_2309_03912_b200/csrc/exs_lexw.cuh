@@ -102,7 +102,19 @@ struct LexW {
   // emit pass
   const u32* fdir; const DirRec* dirs; const u8* dlive; FP* fp;
   WordMasks* wm;                   // count pass writes, emit pass reads (nullptr: recompute)
+  // emit passes: the parser's per-token arrays (file, kind << 8 | id) and flags
+  // (tsplit[f]: a token of file f is live in one pass only; tsplit[F]: some
+  // token is not live in all its file's passes) -- no second pass over the records
+  u32* tfile; u16* tkid; u32* tsplit;
 };
+// the parser's arrays for token t (emit passes)
+EXS_HD inline void tok_meta(const LexW& X, u32 t, const Tok& k) {
+  X.tfile[t] = k.file;
+  X.tkid[t] = (u16)(((u32)k.kind << 8) | k.id);
+  const u8 m = k.mask;
+  if (m == 1 || m == 2) at_or(&X.tsplit[k.file], 1u);
+  if (m != ((X.cfg[k.file] & CFG_PLAIN) ? 1 : 3) && !ld_volatile(X.tsplit + X.F)) at_or(X.tsplit + X.F, 1u);
+}
 
 EXS_HD inline u32 upper_file(const u32* foff, u32 F, u32 p) {
   // last f with foff[f] <= p
@@ -782,6 +794,7 @@ EXS_HD inline u32 lex_word(const LexW& X, u32 w, Tok* out, u32 tbase) {
     {
       TokStore ts_{out + ntok, &t};
     }
+    tok_meta(X, tbase + ntok, t);
     ntok++;
   }
   return ntok;

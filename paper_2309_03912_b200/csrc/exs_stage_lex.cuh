@@ -50,13 +50,16 @@ struct LexState {
   u32* stk = nullptr;       // D
   FP* fp = nullptr;         // 2F
   Tok* toks = nullptr;      // T
+  u32* tfile = nullptr;     // T+1 file of every token (handed to the parser)
+  u16* tkid = nullptr;      // T+1 kind << 8 | id (handed to the parser)
+  u32* tsplit = nullptr;    // F+2 pass-split flags per file, [F]: irregular (handed to the parser)
   u8* arena = nullptr;
   u32* arena_top = nullptr;
   u32 arena_cap = 0;
   u32* cnt = nullptr;       // scratch counters
   void free_all() {
     void* ps[] = {fstart, splice, wsc, wflag, special, fnl, wtok, ftok, dirs, srec, fdir, dlive, stk,
-                  fp, toks, arena, arena_top, cnt, foff, cfg};
+                  fp, toks, arena, arena_top, cnt, foff, cfg, tfile, tkid, tsplit};
     for (void* p : ps) dfree(p);
   }
 };
@@ -308,6 +311,11 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
   }
   // emit pass
   S.toks = dalloc<Tok>((size_t)S.T + 1);
+  S.tfile = dalloc<u32>((size_t)S.T + 1);
+  S.tkid = dalloc<u16>((size_t)S.T + 1);
+  S.tsplit = dalloc<u32>((size_t)F + 2);
+  dzero(S.tsplit, 4ull * (F + 2), st);
+  X.tfile = S.tfile; X.tkid = S.tkid; X.tsplit = S.tsplit;
   X.fdir = S.fdir; X.dirs = S.dirs; X.dlive = S.dlive; X.fp = S.fp;
   {
     const LexW Xc = X; const u32* wt = S.wtok; Tok* tk = S.toks;
@@ -327,6 +335,7 @@ inline void run_lex(LexState& S, const WalkBufs& WB, Scratch& sc, cudaStream_t s
       const u32 hi = logical_line_end(Xc, r.pos, fo[r.file + 1]);
       LexErr e;
       lex_line(s, sp, r.pos, hi, r.lst, r.line_no, r.file, r.mask, tk + r.slot, &e);
+      for (u32 q = 0; q < r.count; q++) tok_meta(Xc, r.slot + q, tk[r.slot + q]);
       if (e.msg)
         for (u32 p = 0; p < 2; p++)
           if ((r.mask >> p) & 1u) at_min(&fp[2 * r.file + p].lex_pos, e.pos);

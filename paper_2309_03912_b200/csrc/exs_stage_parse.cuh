@@ -51,24 +51,14 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
                       u32 split_min = 16) {
   const u32 F = L.F, T = L.T;
   // 1. files whose passes see different token sets
-  u32* split = dalloc<u32>(F + 2);
-  dzero(split, (F + 2) * 4, st);
-  u32* irr = split + F + 1;  // some token is not live in all its file's passes, or a pass failed
-  // the one pass over the token records also fills the per-position file and
-  // kind/id arrays of the common one-view-per-file layout (dropped otherwise)
-  u32* tview = dalloc<u32>((u64)T + 1);
-  u16* tkid = dalloc<u16>((u64)T + 1);
-  {
-    const Tok* tk = L.toks; const u8* cf = L.cfg;
-    par_for(T, [=] EXS_HD (i64 t) {
-      const Tok& k = tk[t];
-      const u8 m = k.mask;
-      tview[t] = k.file;
-      tkid[t] = (u16)(((u32)k.kind << 8) | k.id);
-      if (m == 1 || m == 2) at_or(&split[k.file], 1u);
-      if (m != ((cf[k.file] & CFG_PLAIN) ? 1 : 3) && !ld_volatile(irr)) at_or(irr, 1u);
-    }, st);
-  }
+  // the lexer's emit passes wrote, per token, the file and kind/id arrays of
+  // the common one-view-per-file layout (dropped otherwise) and the per-file
+  // pass-split flags; split[F] (irregular) is also set below when a pass failed
+  u32* split = L.tsplit;
+  u32* irr = split + F;  // some token is not live in all its file's passes, or a pass failed
+  u32* tview = L.tfile;
+  u16* tkid = L.tkid;
+  L.tsplit = nullptr; L.tfile = nullptr; L.tkid = nullptr;  // owned here from now on
   // 2. views per file
   u32* fvc = dalloc<u32>(F + 1);
   u32* fvb = dalloc<u32>(F + 1);

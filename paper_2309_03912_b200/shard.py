@@ -149,11 +149,13 @@ class _CudaBytes:
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False), "version": 2}
 
 
-def make_allgather(device=None, group=None):
+def make_allgather(device=None, group=None, stage_host=False):
     """An exs_allgather_fn over torch.distributed: variable-size byte buffers,
     padded to the largest, all-gathered, then packed in rank order.  device
     None: the buffers are host memory (gloo; the EMU build in the CPU tests);
-    else CUDA memory on that device (NCCL)."""
+    else CUDA memory on that device (NCCL), or, with stage_host, CUDA memory
+    exchanged through host copies over a CPU backend (gloo: the functional GPU
+    test that runs two ranks on one device)."""
     import ctypes as C
     import numpy as np
     from ._native import ALLGATHER_FN
@@ -177,6 +179,17 @@ def make_allgather(device=None, group=None):
                     for r in range(world):
                         dst[off:off + szs[r]] = outs[r][:szs[r]].numpy()
                         off += szs[r]
+            elif stage_host:
+                dev = torch.device(device)
+                t = torch.zeros(mx, dtype=torch.uint8)
+                if nbytes:
+                    t[:nbytes] = torch.as_tensor(_CudaBytes(send, nbytes), device=dev).cpu()
+                outs = [torch.empty(mx, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(outs, t, group=group)
+                if sum(szs):
+                    cat = torch.cat([outs[r][:szs[r]] for r in range(world)])
+                    torch.as_tensor(_CudaBytes(recv, sum(szs)), device=dev).copy_(cat.to(dev))
+                torch.cuda.synchronize(dev)
             else:
                 dev = torch.device(device)
                 t = torch.zeros(mx, dtype=torch.uint8, device=dev)
@@ -201,13 +214,14 @@ def make_allgather(device=None, group=None):
 
 
 def analyze_unit_sharded(text: str, path: str, rank: int, world: int, profile=None, mode=None, cfg=None,
-                         engine=None, device=None, want_walks: bool = False):
+                         engine=None, device=None, want_walks: bool = False, stage_host: bool = False):
     """One unit analysed by `world` ranks together (the walk split across
     them); every rank returns the same Analysis.  device: CUDA device of the
-    collective's buffers (None for host memory: gloo with the EMU build)."""
+    collective's buffers (None for host memory: gloo with the EMU build);
+    stage_host: exchange CUDA buffers through host copies (make_allgather)."""
     from . import exspace as X
     eng = engine or X.get_engine(rank if device is None else device)
-    eng.handle.set_collective(rank, world, make_allgather(device))
+    eng.handle.set_collective(rank, world, make_allgather(device, stage_host=stage_host))
     try:
         unit = (text, path, profile or X.CompileProfile(), mode or X.Mode.CLASSIC, cfg or X.TraitConfig())
         return eng.run_batch([unit], want_walks=want_walks)[0]

@@ -385,3 +385,44 @@ def test_leased_results_survive_later_runs(X):
     again = eng.run_batch(mk(t1, X.Mode.SOUND))
     assert [as_rows(a) for a in first] == [as_rows(a) for a in again]
     assert sum(len(a.all_diagnostics) for a in first) > 0
+
+
+EDGE_UNITS = [
+    "",                                   # empty file
+    "\n\n\n",                             # only newlines
+    "   \t  ",                            # whitespace, no newline at the end
+    "// only a comment",
+    "/* unterminated block comment\nint main() { return 0; }\n",
+    "int main() { return 0; }\\",         # a backslash at the very end
+    "int main() { return 0; }\\\n",       # a splice at the end of the file
+    'void f() { printf("unterminated); }\n',
+    "int main() { return 0; }" * 2000,    # one 48 KB line
+    "\n".join("void f%d() {}" % i for i in range(3000)) + "\nint main() { f1(); return 0; }\n",
+    "#pragma hd_warning_disable\n",       # a directive as the last line, no unit body
+    "struct A { __device__ void call() {} };\nint main() { A{}.call(); return 0; }",  # no final newline
+    "int m\\\nain() { return 0; }\n",     # an identifier spliced across lines
+    "__device__ void d() {}\nvoid h() { d(); }\n" * 300,
+]
+
+
+def test_edge_units_vs_oracle(X, eng):
+    """Inputs at the edges of the lexer and the streaming driver: empty and
+    whitespace-only units, a comment or an unterminated comment/string at EOF, a
+    trailing backslash or splice, one very long line, a spliced identifier, a
+    directive as the last line, no final newline -- each against the oracle, in
+    one batch and one unit at a time."""
+    modes = ["classic", "sound", "fidelity", "proposal1", "proposal2"]
+    units = [(t, f"e{i}.cu", X.CompileProfile(), X.Mode(modes[i % 5]), X.TraitConfig()) for i, t in enumerate(EDGE_UNITS)]
+    together = eng.run_batch(units)
+    for i, (t, a) in enumerate(zip(EDGE_UNITS, together)):
+        rows, _, _ = _oracle_rows(t, modes[i % 5])
+        assert as_rows(a) == rows, i
+        alone = eng.run_batch([units[i]])[0]
+        assert as_rows(alone) == rows, i
+
+
+def test_empty_corpus_and_tiny_units(X):
+    assert len(X.analyze_corpus([])) == 0
+    many = [(f"t{i}.cu", "int main() { return 0; }\n" if i % 2 else "") for i in range(20000)]
+    res = X.analyze_corpus(many)
+    assert len(res) == 20000 and all(len(a.diagnostics) == 0 for a in res)

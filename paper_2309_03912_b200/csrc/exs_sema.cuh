@@ -83,6 +83,15 @@ struct Map {
 EXS_HD inline u64 nz(u64 k) { return k ? k : 0x9E3779B97F4A7C15ull; }
 EXS_HD inline u64 vkey(u32 view, u64 h) { return nz(hcombine((u64)view + 0x51ED27ull, h)); }
 
+// the slot holding key k (inserted if absent; its value is left alone)
+EXS_HD inline u32 map_insert_slot(MapEnt* e, u32 mask, u64 k) {
+  u32 h = (u32)mix64(k) & mask;
+  while (true) {
+    unsigned long long prev = at_cas64((unsigned long long*)&e[h].k, 0ull, (unsigned long long)k);
+    if (prev == 0ull || prev == k) return h;
+    h = (h + 1) & mask;
+  }
+}
 EXS_HD inline void map_insert_min(MapEnt* e, u32 mask, u64 k, u32 v) {
   u32 h = (u32)mix64(k) & mask;
   while (true) {

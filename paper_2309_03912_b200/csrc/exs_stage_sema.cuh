@@ -365,20 +365,26 @@ inline void run_sema(LexState& L, ParseState& P, SemaState& S, const WalkBufs& W
     S.NC = select_idx(NF, [=] EXS_HD (u32 i) -> bool { return fr[i].rec == NONE && !(fr[i].flags & FR_DUP); },
                       idx, L.cnt, sc, st);
     const u32 NC = S.NC;
-    u64* keys = dalloc<u64>(NC + 1);
-    par_for(NC, [=] EXS_HD (i64 i) { keys[i] = vkey(fr[idx[i]].view, fr[idx[i]].name); }, st);
-    sort_pairs(keys, idx, NC, sc, st);
-    S.fcand = idx;
-    S.fcand_cnt = dalloc<u32>(NC + 1);
+    // group by the (view, name) key's slot in the name map: a stable radix sort
+    // of 32-bit slot numbers (as many bits as the table) keeps item order inside
+    // a group; the slot's value is then set to its group's start
     S.fmap_mask = pow2_at_least(2ull * NC + 2) - 1;
     S.fmap = alloc_map(S.fmap_mask, st);
-    u32* cnt = S.fcand_cnt; MapEnt* fme = S.fmap; u32 mask = S.fmap_mask;
-    par_for(NC, [=] EXS_D (i64 i) {
+    MapEnt* fme = S.fmap; const u32 mask = S.fmap_mask;
+    u32* keys = dalloc<u32>(NC + 1);
+    par_for(NC, [=] EXS_D (i64 i) { keys[i] = map_insert_slot(fme, mask, vkey(fr[idx[i]].view, fr[idx[i]].name)); }, st);
+    int kb = 1;
+    while (kb < 32 && (mask >> kb)) kb++;
+    sort_pairs(keys, idx, NC, sc, st, kb);
+    S.fcand = idx;
+    S.fcand_cnt = dalloc<u32>(NC + 1);
+    u32* cnt = S.fcand_cnt;
+    par_for(NC, [=] EXS_HD (i64 i) {
       if (i > 0 && keys[i - 1] == keys[i]) return;
       u32 j = (u32)i;
       while (j < NC && keys[j] == keys[i]) j++;
       cnt[i] = j - (u32)i;
-      map_insert_min(fme, mask, keys[i], (u32)i);
+      fme[keys[i]].v = (u32)i;
     }, st);
     dfree(keys);
   }

@@ -331,6 +331,26 @@ void incl_scan(const T* in, T* out, i64 n, Op op, Scratch& sc, cudaStream_t s) {
 #endif
 }
 
+// inclusive scan of f(0), f(1), ..., f(n-1): the input is computed inside the
+// scan (no array written and read back)
+template <class T, class F, class Op>
+void incl_scan_fn(F f, T* out, i64 n, Op op, Scratch& sc, cudaStream_t s) {
+  if (n <= 0) return;
+#ifndef EXS_EMU
+  cub::CountingInputIterator<u32> c(0);
+  cub::TransformInputIterator<T, F, cub::CountingInputIterator<u32>> it(c, f);
+  size_t tb = 0;
+  CK(cub::DeviceScan::InclusiveScan(nullptr, tb, it, out, op, (int)n, s));
+  CK(cub::DeviceScan::InclusiveScan(sc.get(tb), tb, it, out, op, (int)n, s));
+  g_launches += 2;
+#else
+  (void)sc; (void)s;
+  T acc = f(0);
+  out[0] = acc;
+  for (i64 i = 1; i < n; i++) { acc = op(acc, f((u32)i)); out[i] = acc; }
+#endif
+}
+
 // indices i in [0,n) with pred(i) -> out (ordered); returns count
 template <class P>
 u32 select_idx(i64 n, P pred, u32* out, u32* d_count, Scratch& sc, cudaStream_t s) {

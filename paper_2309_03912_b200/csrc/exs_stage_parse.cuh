@@ -203,11 +203,12 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
   // 3. segmentation: depth scan and item starts (depth over ( ) { })
   u32* depth_after = nullptr;
   {
-    u32* el = dalloc<u32>(VT + 1);
     u32* inc = dalloc<u32>(VT + 1);
     const u32* vv = P.vview; const u32* vb = P.vbase;
     const u16* vk = P.vkid;  // 2-byte kind/id per view position (not the 32-byte token)
-    par_for(VT, [=] EXS_HD (i64 i) {
+    // depth delta of every view position, with the view-head reset flag: the
+    // scan's input, computed inside the scan
+    auto delta = [=] EXS_HD (u32 i) -> u32 {
       const u16 t = vk[i];
       u32 d = 0;
       if ((t >> 8) == TK_PUNCT) {
@@ -215,37 +216,31 @@ inline void run_parse(LexState& L, ParseState& P, const WalkBufs& WB, Scratch& s
         if (id == P_LPAREN || id == P_LBRACE) d = 1;
         else if (id == P_RPAREN || id == P_RBRACE) d = 0x7FFFFFFFu;  // -1 mod 2^31
       }
-      bool head = vb[vv[i]] == (u32)i;
-      el[i] = d | (head ? 0x80000000u : 0u);
-    }, st);
+      return d | (vb[vv[i]] == i ? 0x80000000u : 0u);
+    };
     prof_mark(st);
-    incl_scan(el, inc, VT, DepthOp(), sc, st);
+    incl_scan_fn<u32>(delta, inc, VT, DepthOp(), sc, st);
     prof_mark(st);
-    u8* endf = (u8*)el;  // reuse as end flags (VT bytes)
-    par_for(VT, [=] EXS_HD (i64 i) {
-      const u16 t = vk[i];
-      const u32 dep = depth_of(inc[i]);
-      bool e = false;
-      if (dep == 0 && (t >> 8) == TK_PUNCT) {
-        if ((u8)t == P_SEMI) e = true;
-        else if ((u8)t == P_RBRACE) {
-          bool semi_next = (u32)i + 1 < vb[vv[i] + 1] && vk[i + 1] == (u16)((TK_PUNCT << 8) | P_SEMI);
-          e = !semi_next;
-        }
-      }
-      endf[i] = e;
-    }, st);
+    // item starts: a view's first token, or a token after one that ends an item
+    // (a depth-0 ';', or a depth-0 '}' not followed by ';') -- evaluated in the
+    // selection's own flag pass, no end-flag array
     P.item_start = dalloc<u32>(VT + 1);
+    const u32* dep = inc;
     auto pred = [=] EXS_HD (u32 i) -> bool {
       if (vb[vv[i]] == i) return true;
-      return endf[i - 1] && vv[i - 1] == vv[i];
+      const u32 e = i - 1;
+      if (vv[e] != vv[i] || depth_of(dep[e]) != 0) return false;
+      const u16 t = vk[e];
+      if ((t >> 8) != TK_PUNCT) return false;
+      if ((u8)t == P_SEMI) return true;
+      if ((u8)t != P_RBRACE) return false;
+      return !(i < vb[vv[e] + 1] && vk[i] == (u16)((TK_PUNCT << 8) | P_SEMI));
     };
     prof_mark(st);
     P.I = select_idx(VT, pred, P.item_start, L.cnt, sc, st);
     prof_mark(st);
     h2d(P.item_start + P.I, &VT, 4, st);  // sentinel: node_base(is, I) bounds the last view's arena
     sync(st);
-    dfree(el);
     depth_after = inc;  // kept for the statement segmentation of large bodies
   }
   const u32 I = P.I;

@@ -361,6 +361,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   WalkBufs B = bufs();
   prof_mark(st);
   // ---- roots (spacecheck.py:272-308)
+  bool roots_keyed = false;  // every root's creation key already in its record (no step 3)
   {
     const FnRec* fr = S.fns; const RecRec* rr = S.recs; const Node* nd = P.nodes; const Tok* tk = L.toks;
     const FP* fp = L.fp; const u32* vf = P.vfile; const u8* cfgs = L.cfg;
@@ -442,6 +443,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     // counter: at this rate one counter serialises the kernel)
     u32* rslot = dalloc<u32>(2ull * NRC + 1);
     RootStash* rstash = dalloc<RootStash>((u64)NRC + 1);
+    u32* nslow = dalloc<u32>(2);  // [0] candidates left to step 3, [1] step 2's id count
+    dzero(nslow, 8, st);
     const u32 nlog0 = get1(B.n_log, st);
     {
       u32* rs = rslot;
@@ -452,7 +455,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         rs[2 * kk] = rs[2 * kk + 1] = NONE;
         const RootCand q = cand(rcc[kk], (u32)kk, true);
         ro[kk] = q.ot.rec;
-        if (!q.fast) { rs[2 * kk] = NONE - 1; return; }  // evaluated in step 3
+        if (!q.fast) { rs[2 * kk] = NONE - 1; at_inc_agg(nslow); return; }  // evaluated in step 3
         const FnRec& r = fr[q.i];
         const u16 fl = nd[r.node].n;
         const u8 sides = (fl & FF_G) ? 2 : (static_spaces(fl, q.free_main, q.sf, q.mode, 0) & 3);
@@ -496,7 +499,15 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
       const u32* rs = rslot;
       par_for(NS2 + 1, [=] EXS_HD (i64 j) { ins[j] = j < NS2 && rs[j] < NONE - 1; }, st);
       excl_scan_u32(ins, ids, NS2 + 1, sc, st);
-      const u32 total = get1(ids + NS2, st);
+      {
+        const u32* idl = ids + NS2; u32* ns_ = nslow;
+        par_for(1, [=] EXS_HD (i64) { ns_[1] = *idl; }, st);
+      }
+      u32 two[2];
+      d2h(two, nslow, 8, st);
+      sync(st);
+      const u32 total = two[1];
+      roots_keyed = two[0] == 0;
       const u32* id_of = ids;
       const RootStash* rst = rstash;
       par_for(NS2, [=] EXS_HD (i64 j) {
@@ -516,6 +527,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         I.tb = vnone(); I.hb = vnone(); I.ot = ot;
         I.side = sd; I.spaces = z.sp[sd]; I.pad = 0; I.slot = slot;
         I.flags = z.iflags;  // fill_instance's flags, from the decl record
+        I.ckey = S_.sck;     // final: every root creator ran in step 1 (step 3 redoes it otherwise)
         S_.sid = id;
       }, st);
       u32* ni = B.n_inst;
@@ -574,6 +586,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     dfree(rcand);
     dfree(rslot);
     dfree(rstash);
+    dfree(nslow);
     dfree(rot);
     dfree(vd0);
   }
@@ -598,7 +611,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     if (!ovf_local) {
       // creation keys of this level's instances (min over creators), then the
       // first creator's location (spacecheck.py:331-337)
-      {
+      if (level > 0 || !roots_keyed) {  // the roots' keys were written with their records
         Inst* in = W.inst; const Slot* sl = W.slots; const u32 base = prev_n;
         par_for(n_now - prev_n, [=] EXS_HD (i64 j) { Inst& I = in[base + j]; I.ckey = sl[I.slot].sck; }, st);
       }

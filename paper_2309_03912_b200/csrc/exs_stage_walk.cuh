@@ -18,7 +18,7 @@ namespace exs {
 #endif
 
 // walk counters, each on its own 128-byte line (hot atomics must not share one)
-enum { CNT_INST = 0, CNT_PEND = 1, CNT_SEEDS = 2, CNT_LOG = 3, CNT_OVF = 4, CNT_N = 5 };
+enum { CNT_INST = 0, CNT_PEND = 1, CNT_SEEDS = 2, CNT_LOG = 3, CNT_OVF = 4, CNT_MAINS = 5, CNT_N = 6 };
 constexpr u32 CNT_STRIDE = 32;
 
 // The collective of one unit walked across GPUs: an
@@ -87,7 +87,9 @@ struct WalkState {
   u32 cap_log = 0;
   u32* main_inst = nullptr;
   unsigned long long* main_key = nullptr;
-  u32* counters = nullptr;  // [n_inst, n_pend, n_seeds, n_log, overflow]
+  u32* mains = nullptr;     // ids of the instances of main (few), in creation order
+  u32 cap_mains = 0;
+  u32* counters = nullptr;  // [n_inst, n_pend, n_seeds, n_log, overflow, n_mains]
   u8* visited = nullptr;
   // per walk statistics
   std::vector<u32> w_inst, w_edges, w_demands;
@@ -100,10 +102,10 @@ struct WalkState {
     return out;
   }
   void free_all() {
-    void* ps[] = {slots, inst, edges, pend, seeds, log, main_inst, main_key, counters, visited};
+    void* ps[] = {slots, inst, edges, pend, seeds, log, main_inst, main_key, mains, counters, visited};
     for (void* p : ps) dfree(p);
     slots = nullptr; inst = nullptr; edges = nullptr; pend = nullptr; seeds = nullptr;
-    log = nullptr; main_inst = nullptr; main_key = nullptr; counters = nullptr; visited = nullptr;
+    log = nullptr; main_inst = nullptr; main_key = nullptr; mains = nullptr; counters = nullptr; visited = nullptr;
   }
 };
 
@@ -181,6 +183,7 @@ inline WalkBufs make_bufs(WalkState& W, u32* n_diags, Diag* diags, u32 cap_diags
   B.seeds = W.seeds; B.n_seeds = W.ctr(CNT_SEEDS); B.cap_seeds = W.cap_seeds;
   B.log = W.log; B.n_log = W.ctr(CNT_LOG); B.cap_log = W.cap_log;
   B.main_inst = W.main_inst; B.main_key = W.main_key;
+  B.mains = W.mains; B.n_mains = W.ctr(CNT_MAINS); B.cap_mains = W.cap_mains;
   B.diags = diags; B.n_diags = n_diags; B.cap_diags = cap_diags; B.dset = dset; B.dmask = dmask;
   B.overflow = W.ctr(CNT_OVF);
   B.contract = contract;
@@ -346,6 +349,8 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
   W.main_key = dalloc<unsigned long long>(NW + 1);
   dfill_ff(W.main_inst, 4ull * (NW + 1), st);
   dzero(W.main_key, 8ull * (NW + 1), st);
+  W.cap_mains = 4 * NW + 1024;
+  W.mains = dalloc<u32>(W.cap_mains);
   u64 edge_cap = 0, pend_cap = 0, seed_cap = 0, log_cap = 0;
   W.edges = nullptr; W.pend = nullptr; W.seeds = nullptr; W.log = nullptr;
   // roots log only their non-inserting creators (duplicate decls): few
@@ -529,6 +534,7 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
         I.flags = z.iflags;  // fill_instance's flags, from the decl record
         I.ckey = S_.sck;     // final: every root creator ran in step 1 (step 3 redoes it otherwise)
         S_.sid = id;
+        if (z.iflags & IF_MAIN) note_main(B, id);
       }, st);
       u32* ni = B.n_inst;
       par_for(1, [=] EXS_HD (i64) { *ni = total; }, st);
@@ -946,11 +952,17 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
     dfree(ck); dfree(wk); dfree(cid);
   }
   prof_mark(st);
-  // ---- main instance per walk: the last created (max creation key)
+  // ---- main instance per walk: the last created (max creation key), over the
+  // list kept at creation (every instance in a sharded walk, whose merged
+  // instances were created on other ranks, or past the list's capacity)
   {
     const Inst* in = W.inst; unsigned long long* mk = W.main_key; u32* mi = W.main_inst;
-    u32 n = W.n_inst;
-    par_for(n, [=] EXS_D (i64 i) {
+    const u32 nm = W.read_counters(st)[CNT_MAINS];
+    const bool listed = !W.coll.on() && nm <= W.cap_mains;
+    const u32 n = listed ? nm : W.n_inst;
+    const u32* ml = listed ? W.mains : nullptr;
+    par_for(n, [=] EXS_D (i64 j) {
+      const u32 i = ml ? ml[j] : (u32)j;
       if (in[i].flags & IF_MAIN) {
 #ifndef EXS_EMU
         atomicMax(&mk[in[i].walk], in[i].ckey + 1);
@@ -959,8 +971,9 @@ inline bool run_walk(LexState& L, ParseState& P, SemaState& S, WalkState& W, Wal
 #endif
       }
     }, st);
-    par_for(n, [=] EXS_HD (i64 i) {
-      if ((in[i].flags & IF_MAIN) && mk[in[i].walk] == in[i].ckey + 1) mi[in[i].walk] = (u32)i;
+    par_for(n, [=] EXS_HD (i64 j) {
+      const u32 i = ml ? ml[j] : (u32)j;
+      if ((in[i].flags & IF_MAIN) && mk[in[i].walk] == in[i].ckey + 1) mi[in[i].walk] = i;
     }, st);
   }
   prof_mark(st);

@@ -83,6 +83,9 @@ struct WalkBufs {
   u32 cap_log;
   u32* main_inst;               // per walk: instance of main with the max creation key
   unsigned long long* main_key; // per walk
+  u32* mains;                   // ids of main's instances as created (n_mains may pass cap_mains)
+  u32* n_mains;
+  u32 cap_mains;
   // diagnostics
   Diag* diags;
   u32* n_diags;
@@ -212,6 +215,11 @@ EXS_HD inline void fill_instance(Inst& I, const Tables* T, const IKey& k, u32 fi
   I.flags = (fr.flags & FR_BODY) ? IF_BODY : 0;
   if (fr.flags & FR_MAIN) I.flags |= IF_MAIN;
 }
+// an instance of main (the per-walk main is picked from these after the walk)
+EXS_HD inline void note_main(const WalkBufs& B, u32 id) {
+  const u32 k = at_add(B.n_mains, 1u);
+  if (k < B.cap_mains) B.mains[k] = id;
+}
 // key insertion without an id (the level-0 roots allocate ids by a scan
 // afterwards instead of one shared counter): the slot, NONE if the table is full
 EXS_HD inline u32 slot_insert(const WalkBufs& B, const IKey& k, bool& inserted) {
@@ -243,6 +251,7 @@ EXS_HD EXS_FI u32 create_instance(const WalkBufs& B, const Tables* T, u32 fi, co
   if (inserted) {
     fill_instance(B.inst[id], T, k, fi, tb, hb, want_side, orec, ot, at_tok, walk, sp, slot);
     inst_publish(B, slot, id);
+    if (fr.flags & FR_MAIN) note_main(B, id);
   }
   if (id >= B.lvl_base) {
     // a creator in this level: the minimum creation key wins.  A creator

@@ -208,6 +208,18 @@ EXS_HD constexpr u64 nh_fin(u64 h, u32 len) {
   h ^= h >> 33; h *= 0xff51afd7ed558ccdull; h ^= h >> 33;
   return h;
 }
+// NameHash of a NUL-terminated word at compile time (vocabulary, builtin types)
+EXS_HD constexpr u64 name_hash_c(const char* w) {
+  u32 n = 0;
+  while (w[n]) n++;
+  u64 h = 1469598103934665603ull;
+  for (u32 q = 0; q < n; q += 4) {
+    u32 x = 0;
+    for (u32 k = 0; k < 4 && q + k < n; k++) x |= (u32)(u8)w[q + k] << (8 * k);
+    h = nh_mix(h, x);
+  }
+  return nh_fin(h, n);
+}
 struct NameHash {
   u64 h = 1469598103934665603ull;
   u32 acc = 0, n = 0;

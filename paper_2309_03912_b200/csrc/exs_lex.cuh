@@ -169,18 +169,6 @@ __constant__ char kVocabDev[] = EXS_VOCAB_TEXT;
 static const char kVocabHost[] = EXS_VOCAB_TEXT;
 
 constexpr u32 len_c(const char* s) { return *s ? 1 + len_c(s + 1) : 0; }
-// compile-time name hash of a vocabulary word (NameHash: the lexer's function)
-constexpr u64 name_hash_c(const char* s) {
-  u64 h = 1469598103934665603ull;
-  const u32 n = len_c(s);
-  for (u32 q = 0; q < n; q += 4) {
-    u32 x = 0;
-    for (u32 k = 0; k < 4 && q + k < n; k++) x |= (u32)(u8)s[q + k] << (8 * k);
-    h = nh_mix(h, x);
-  }
-  return nh_fin(h, n);
-}
-
 // Vocabulary id from the token's text hash and length: a perfect hash over
 // the 38 words (multiplier found offline: slot = (hv * K) >> 57, collision-
 // free) -- one table load, no divergent compare tree.

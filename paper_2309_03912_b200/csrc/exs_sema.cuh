@@ -12,19 +12,8 @@ namespace exs {
 enum { ST_OK = 0, ST_SUBST = 1, ST_SEMA = 2 };
 enum { V_NONE = 0, V_TYPE, V_HDC, V_BOOL, V_INT };
 // name hashes of fixed words (NameHash: the lexer computes the same for tokens)
-EXS_HD constexpr inline u64 word_hash(const char* w) {
-  u32 n = 0;
-  while (w[n]) n++;
-  u64 h = 1469598103934665603ull;
-  for (u32 q = 0; q < n; q += 4) {
-    u32 x = 0;
-    for (u32 k = 0; k < 4 && q + k < n; k++) x |= (u32)(u8)w[q + k] << (8 * k);
-    h = nh_mix(h, x);
-  }
-  return nh_fin(h, n);
-}
-constexpr u64 H_INT = word_hash("int"), H_BOOL = word_hash("bool"), H_HDC_MEMBER = word_hash("hdc"),
-              H_STD = word_hash("std::");
+constexpr u64 H_INT = name_hash_c("int"), H_BOOL = name_hash_c("bool"), H_HDC_MEMBER = name_hash_c("hdc"),
+              H_STD = name_hash_c("std::");
 
 struct Val {
   u8 k;      // V_*
@@ -309,7 +298,7 @@ struct Sema {
   EXS_HD u8 trait(const Val& t, bool f, Val& out) {
     if (t.bt == BT_INT || t.bt == BT_BOOL) { out = vhdc(f ? 3 : 1); return ST_OK; }
     if (t.rec == NONE) return subst(SF_NO_COMPAT, type_name_arg(t));
-    u32 mv = first_mvar(t.rec, word_hash("hdc"));
+    u32 mv = first_mvar(t.rec, H_HDC_MEMBER);
     if (mv == NONE) { out = vhdc(1); return ST_OK; }
     if (N(mv).sub != BT_HDC) return sema(C_E0103, M_S_HDC_MEMBER, N(mv).tok, type_name_arg(t));
     Env se;

@@ -589,9 +589,9 @@ struct Walker {
   EXS_HD EXS_FI Val expr_(u32 e) {
     const Node& n = N(e);
     switch (n.kind) {
-      case N_INT: { Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int"); return t; }
+      case N_INT: { Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = H_INT; return t; }
       case N_BOOL:
-      case N_ARCH: { Val t = vnone(); t.k = V_TYPE; t.bt = BT_BOOL; t.x = word_hash("bool"); return t; }
+      case N_ARCH: { Val t = vnone(); t.k = V_TYPE; t.bt = BT_BOOL; t.x = H_BOOL; return t; }
       case N_STR:
       case N_HDCV: return vnone();
       case N_NAME: {
@@ -628,13 +628,13 @@ struct Walker {
       }
       case N_NOT: {
         expr(n.c0);
-        Val t = vnone(); t.k = V_TYPE; t.bt = BT_BOOL; t.x = word_hash("bool");
+        Val t = vnone(); t.k = V_TYPE; t.bt = BT_BOOL; t.x = H_BOOL;
         return t;
       }
       case N_BIN: {
         expr(n.c0);
         expr(n.c1);
-        Val t = vnone(); t.k = V_TYPE; t.bt = BT_BOOL; t.x = word_hash("bool");
+        Val t = vnone(); t.k = V_TYPE; t.bt = BT_BOOL; t.x = H_BOOL;
         return t;
       }
       case N_CALL: return free_call(e);
@@ -676,7 +676,7 @@ struct Walker {
   }
   EXS_HD EXS_DISPATCH Val free_call_(const Node& n, const Val* tys, u32 na) {
     bool is_std = n.sub == CALL_STD;
-    u64 nm = is_std ? hcombine(word_hash("std::"), K(n.c0).hv) : n.hv;
+    u64 nm = is_std ? hcombine(H_STD, K(n.c0).hv) : n.hv;
     u32 run = is_std ? NONE : T->fmap.find(vkey(S.view, nm));
     if (run == NONE) {
       // builtin_spaces (sema.py:99-102)
@@ -688,7 +688,7 @@ struct Walker {
       else if (w == W_CUDASYNC) sp = S.plain ? 0 : 1;
       if (sp) {
         if (!(sp & (1u << side))) stray(sp == 1 ? 1 : 2, n.tok);
-        if (w == W_CUDASYNC) { Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int"); return t; }
+        if (w == W_CUDASYNC) { Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = H_INT; return t; }
       }
       return vnone();
     }
@@ -755,7 +755,7 @@ struct Walker {
         expr(n.c0);
         expr(n.c1);
         u32 mark = nloc;
-        Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = word_hash("int");
+        Val t = vnone(); t.k = V_TYPE; t.bt = BT_INT; t.x = H_INT;
         local_set(n.hv, t);
         stmts(n.c2);
         nloc = mark;
